@@ -1,0 +1,11 @@
+"""B200-native Write-Gated KV (arXiv 2512.17452) hot path.
+
+The product is ``libwgkv_b200.so`` (hand-written sm_100a CUDA behind the C-ABI
+in ``include/wgkv_b200.h``); this package is its Python face.
+"""
+from ._lib import (ATTN_AUTO, ATTN_SIMT, ATTN_TCGEN05, BF16, F32, LifecycleError, NotSupported,  # noqa: F401
+                   OutOfPages, WgkvError, load)
+from .api import Session, default_capacity, vs_pair_count  # noqa: F401
+
+__all__ = ["Session", "default_capacity", "vs_pair_count", "load", "BF16", "F32", "ATTN_AUTO", "ATTN_SIMT",
+           "ATTN_TCGEN05", "OutOfPages", "LifecycleError", "NotSupported", "WgkvError"]

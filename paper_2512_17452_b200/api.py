@@ -1,0 +1,177 @@
+"""Host-side mirror of the reference's hot-path API over the C-ABI.
+
+Names and argument meaning follow the reference (namespace ``wgkv``):
+
+* :meth:`Session.gate_forward_batch` -- ``gate_forward_batch`` + ``binarize``
+  (gating.cpp:173-190) for one layer's keys, fused with RoPE (K1);
+* :meth:`Session.prefill_layer` -- the body of ``Session::prefill`` for one
+  layer (engine.cpp:188-257): gate, mask, vertical-slash attention and
+  ``HeadCache::prefill_populate`` (K1 -> K2 -> K3);
+* :meth:`Session.decode_layer` -- the body of ``Session::decode_step``
+  (engine.cpp:291-327): gate, ``HeadCache::local_write`` with lazy promotion,
+  and ``attn_ragged`` over Global || Local in place (K4 -> K5);
+* :meth:`Session.gather` / :meth:`Session.stats` -- ``HeadCache::gather`` and
+  ``cache_stats`` for audits (kvstore.cpp:205-267).
+
+Errors map to the reference's exception classes: ``ValueError``
+(std::invalid_argument), ``OutOfPages`` (a ``MemoryError``; "out of pages"),
+``LifecycleError`` (std::logic_error), ``ArithmeticError`` (runtime_error).
+Device memory and streams come from torch; all compute is the CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ATTN_AUTO, ATTN_SIMT, ATTN_TCGEN05, BF16, F32, check  # noqa: F401
+
+_TORCH_DT = {BF16: torch.bfloat16, F32: torch.float32}
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def default_capacity(layers, kv_heads, window, max_tokens, page_size=16, seqs=1) -> int:
+    """default_capacity (engine.cpp:88-93), times the sequence slots."""
+    return seqs * layers * kv_heads * (-(-window // page_size) + -(-max_tokens // page_size) + 1)
+
+
+class Session:
+    """One device's WG-KV state for ``kv_heads`` KV heads (a shard when
+    ``kv_head_offset`` > 0) over ``max_seqs`` sequence slots."""
+
+    def __init__(self, layers, q_heads, kv_heads, head_dim, hidden, window, tau=0.1, rope_base=10000.0,
+                 page_size=16, max_seqs=1, max_tokens=4096, max_prefill_tokens=None, capacity_pages=0,
+                 dtype=BF16, topk_budget=0, attn_impl=ATTN_AUTO, device=0, kv_head_offset=0, gate_bank=None):
+        self.lib = _lib.load()
+        cfg = _lib.Config(layers=layers, q_heads=q_heads, kv_heads=kv_heads, kv_head_offset=kv_head_offset,
+                          head_dim=head_dim, hidden=hidden, window=window, tau=tau, rope_base=rope_base,
+                          page_size=page_size, max_seqs=max_seqs, max_tokens=max_tokens,
+                          max_prefill_tokens=max_prefill_tokens or max_tokens, capacity_pages=capacity_pages,
+                          dtype=dtype, topk_budget=topk_budget, attn_impl=attn_impl, device=device)
+        self.cfg = cfg
+        self.device = torch.device("cuda", device)
+        self.dtype = _TORCH_DT[dtype]
+        h = C.c_void_p()
+        check(self.lib.wgkv_ctx_create(C.byref(cfg), C.byref(h)), "Session")
+        self.h = h
+        self.set_stream(torch.cuda.current_stream(self.device))
+        if gate_bank is not None:
+            self.gate_set(gate_bank)
+
+    # ---- lifecycle -------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.wgkv_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        check(self.lib.wgkv_set_stream(self.h, C.c_void_p(stream.cuda_stream)), "set_stream")
+
+    def sync(self):
+        check(self.lib.wgkv_sync(self.h), "sync")
+
+    # ---- gates -----------------------------------------------------------
+    def gate_set(self, bank: np.ndarray):
+        """bank: fp64 [layers][bank_heads][block] (GateBank layout, gating.hpp:41-68)."""
+        bank = np.ascontiguousarray(bank, np.float64)
+        self._bank = bank
+        check(self.lib.wgkv_gate_set(self.h, bank.ctypes.data_as(C.c_void_p), bank.shape[0], bank.shape[1]),
+              "gate_set")
+
+    def gate_load(self, path: str):
+        check(self.lib.wgkv_gate_load(self.h, os.fsencode(path)), "GateBank::load")
+
+    # ---- K1 --------------------------------------------------------------
+    def gate_forward_batch(self, layer: int, k_pre: torch.Tensor, pos0: int = 0, forced=None):
+        """k_pre [nseq][T][kv_heads][d] -> (k_post, g [nseq][H][T] f32, bits uint8, near flat indices)."""
+        nseq, T = k_pre.shape[0], k_pre.shape[1]
+        H = self.cfg.kv_heads
+        k_post = torch.empty_like(k_pre)
+        g = torch.empty((nseq, H, T), dtype=torch.float32, device=self.device)
+        bits = torch.empty((nseq, H, T), dtype=torch.uint8, device=self.device)
+        near = torch.empty(1 << 16, dtype=torch.int64, device=self.device)
+        n = C.c_int(0)
+        check(self.lib.wgkv_gate_score(self.h, layer, nseq, T, pos0, _p(k_pre), _p(forced), _p(k_post), _p(g),
+                                       _p(bits), _p(near), near.numel(), C.byref(n)), "gate_forward_batch")
+        return k_post, g, bits, near[: min(n.value, near.numel())].cpu().numpy()
+
+    # ---- prefill -----------------------------------------------------------
+    def prefill_layer(self, layer, q, k_pre, v, seq0=0, forced_gates=None, out=None, want_gates=False):
+        """q [nseq][T][q_heads][d], k_pre/v [nseq][T][kv_heads][d] (device, dtype)."""
+        nseq, T = q.shape[0], q.shape[1]
+        if out is None:
+            out = torch.empty_like(q)
+        g = bits = None
+        if want_gates:
+            g = torch.empty((nseq, self.cfg.kv_heads, T), dtype=torch.float32, device=self.device)
+            bits = torch.empty((nseq, self.cfg.kv_heads, T), dtype=torch.uint8, device=self.device)
+        check(self.lib.wgkv_prefill_layer(self.h, layer, seq0, nseq, T, _p(q), _p(k_pre), _p(v), _p(forced_gates),
+                                          _p(out), _p(g), _p(bits)), "Session::prefill")
+        return (out, g, bits) if want_gates else out
+
+    # ---- decode ------------------------------------------------------------
+    def decode_layer(self, layer, q, k_pre, v, seq0=0, forced_gates=None, out=None, want_events=False):
+        """q [nseq][q_heads][d], k_pre/v [nseq][kv_heads][d] -> out [nseq][q_heads][d]."""
+        nseq = q.shape[0]
+        if out is None:
+            out = torch.empty_like(q)
+        g = ev = None
+        if want_events:
+            g = torch.empty((nseq, self.cfg.kv_heads), dtype=torch.float32, device=self.device)
+            ev = torch.empty((nseq, self.cfg.kv_heads), dtype=torch.int32, device=self.device)
+        check(self.lib.wgkv_decode_layer(self.h, layer, seq0, nseq, _p(q), _p(k_pre), _p(v), _p(forced_gates),
+                                         _p(out), _p(g), _p(ev)), "Session::decode_step")
+        return (out, g, ev) if want_events else out
+
+    # ---- state / audit -------------------------------------------------------
+    def state(self, layer, seq, head) -> dict:
+        lens = (C.c_int64 * 6)()
+        check(self.lib.wgkv_cache_state(self.h, layer, seq, head, lens), "cache_state")
+        return dict(zip(("local_len", "local_ptr", "global_len", "tokens_seen", "n_local_pages", "n_global_pages"),
+                        list(lens)))
+
+    def gather(self, layer, seq, head) -> dict:
+        """HeadCache::gather (kvstore.cpp:205-241) to host numpy (fp32 K/V)."""
+        s = self.state(layer, seq, head)
+        G, Lc, d = s["global_len"], s["local_len"], self.cfg.head_dim
+        out = dict(global_k=np.empty((G, d), np.float32), global_v=np.empty((G, d), np.float32),
+                   global_pos=np.empty(G, np.int64), global_gate=np.empty(G, np.float32),
+                   local_k=np.empty((Lc, d), np.float32), local_v=np.empty((Lc, d), np.float32),
+                   local_pos=np.empty(Lc, np.int64), local_gate=np.empty(Lc, np.float32))
+        ptrs = [out[k].ctypes.data_as(C.c_void_p) for k in ("global_k", "global_v", "global_pos", "global_gate",
+                                                             "local_k", "local_v", "local_pos", "local_gate")]
+        check(self.lib.wgkv_cache_export(self.h, layer, seq, head, *ptrs), "gather")
+        return out
+
+    def stats(self, seq0=0, nseq=1) -> dict:
+        v = (C.c_int64 * 4)()
+        check(self.lib.wgkv_cache_stats(self.h, seq0, nseq, v), "cache_stats")
+        return dict(resident_entries=v[0], global_entries=v[1], tokens_seen=v[2], pages_allocated=v[3],
+                    admitted_fraction=(v[1] / v[2]) if v[2] else 0.0)
+
+    def release(self, seq0=0, nseq=1):
+        check(self.lib.wgkv_release(self.h, seq0, nseq), "release")
+
+    def pool_info(self) -> dict:
+        v = (C.c_int64 * 2)()
+        check(self.lib.wgkv_pool_info(self.h, v), "pool_info")
+        return dict(capacity=v[0], free=v[1])
+
+
+def vs_pair_count(bits: np.ndarray, window: int) -> int:
+    """vs_mask_pair_count (attention.cpp:182-191), closed form, one head."""
+    b = np.ascontiguousarray(bits, np.uint8)
+    return int(_lib.load().wgkv_vs_pair_count(b.ctypes.data_as(C.c_void_p), b.size, window))

@@ -1,0 +1,343 @@
+// admit.cu -- K2 (prefill admission/compaction) and K4 (decode append with
+// lazy promotion) over the device-resident paged dual cache.
+//
+// K2 replaces HeadCache::prefill_populate (kvstore.cpp:160-203):
+//   admit_plan_kernel    one CTA per (seq, kv head): counts admitted tokens
+//                        j < T-W per 128-token chunk, block-scans the counts,
+//                        claims ceil(G/ps) Global + ceil(min(T,W)/ps) Local
+//                        pages from the device free stack in one atomic, and
+//                        writes the page tables and ring state.
+//   admit_scatter_kernel one warp per 32 tokens: ballot/popc rank inside the
+//                        chunk + the scanned chunk base gives each admitted
+//                        row its Global slot (ascending order, exactly the
+//                        reference's append order); window rows go to ring
+//                        slots 0..; each row's K and V move with 128-bit
+//                        loads/stores, gate/position/bit ride along.
+// K4 replaces HeadCache::local_write + promote (kvstore.cpp:122-158) fused
+// with the decode-time gate (gate_forward, gating.cpp:158-171) and RoPE.
+#include "admit.cuh"
+#include "gate.cuh"
+
+namespace wgkv {
+
+constexpr int ADM_CHUNK = 128;
+
+__global__ void __launch_bounds__(1024) admit_plan_kernel(PoolView pv, int layer, int seq0, long T, long W,
+                                                          const uint8_t* __restrict__ bits, int32_t* __restrict__ chunk_off) {
+    const int s = blockIdx.x, h = blockIdx.y;
+    const int tid = threadIdx.x;
+    const long ws = T > W ? T - W : 0;  // window_start (kvstore.cpp:169)
+    const long nchunk = (T + ADM_CHUNK - 1) / ADM_CHUNK;
+    const uint8_t* b = bits + ((size_t)s * pv.kv_heads + h) * T;
+    int32_t* co = chunk_off + ((size_t)s * pv.kv_heads + h) * (nchunk + 1);
+    __shared__ int warp_tot[32];
+    __shared__ int carry;
+    __shared__ int page_base;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    // exclusive scan of per-chunk admitted counts, 1024 chunks per pass
+    for (long c0 = 0; c0 < nchunk; c0 += 1024) {
+        const long c = c0 + tid;
+        int cnt = 0;
+        if (c < nchunk) {
+            const long lo = c * ADM_CHUNK, hi = min((long)(c + 1) * ADM_CHUNK, ws);
+            for (long j = lo; j < hi; j += 4) {
+                if (j + 4 <= hi && ((((uintptr_t)(b + j)) & 3) == 0)) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(b + j);
+                    cnt += __popc(w & 0x01010101u);
+                } else {
+                    for (long jj = j; jj < min(j + 4, hi); ++jj) cnt += b[jj] != 0;
+                }
+            }
+        }
+        int x = cnt;
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int t = warp_tot[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        const int excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - cnt;
+        if (c < nchunk) co[c] = excl;
+        __syncthreads();
+        if (tid == 1023) carry = excl + cnt;
+        __syncthreads();
+    }
+    const int G = carry;
+    const long Lc = T - ws;  // min(T, W) ring entries
+    const int ng = (G + pv.page_size - 1) / pv.page_size;
+    const int nl = (int)((Lc + pv.page_size - 1) / pv.page_size);
+    const long hidx = pv.head_index(layer, seq0 + s, h);
+    if (tid == 0) {
+        co[nchunk] = G;
+        const int need = ng + nl;
+        int top = atomicSub(pv.free_top, need);
+        if (top < need) {
+            atomicAdd(pv.free_top, need);
+            atomicExch(pv.err, WGKV_ENOPAGES);
+            page_base = -1;
+        } else {
+            page_base = top;
+        }
+        // on a failed claim the head keeps no pages (the error is latched and
+        // surfaces at the next wgkv_sync, like the reference's throw)
+        HeadState st;
+        st.local_len = page_base < 0 ? 0 : (int)Lc;
+        st.local_ptr = page_base < 0 ? 0 : (int)(Lc % W);
+        st.global_len = page_base < 0 ? 0 : G;
+        st.tokens_seen = (int)T;
+        pv.state[hidx] = st;
+    }
+    __syncthreads();
+    if (page_base < 0) return;
+    // LIFO pops in order: page i = stack[top - 1 - i] (KvPool::alloc_page)
+    for (int i = tid; i < ng + nl; i += blockDim.x) {
+        const int page = pv.free_stack[page_base - 1 - i];
+        if (i < ng)
+            pv.gpt[hidx * pv.n_gp + i] = page;
+        else
+            pv.lpt[hidx * pv.n_lp + (i - ng)] = page;
+    }
+}
+
+template <typename E>
+__device__ __forceinline__ void copy_row_warp(E* __restrict__ dst, const E* __restrict__ src, int d, int lane) {
+    // 16-byte vectors; d*sizeof(E) is a multiple of 16 for d % 8 == 0
+    const int nvec = d * (int)sizeof(E) / 16;
+    if ((d * sizeof(E)) % 16 == 0) {
+        const int4* s4 = reinterpret_cast<const int4*>(src);
+        int4* d4 = reinterpret_cast<int4*>(dst);
+        for (int e = lane; e < nvec; e += 32) d4[e] = s4[e];
+    } else {
+        for (int e = lane; e < d; e += 32) dst[e] = src[e];
+    }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(128) admit_scatter_kernel(PoolView pv, int layer, int seq0, long T, long W,
+                                                             const E* __restrict__ k_post, const E* __restrict__ v,
+                                                             const float* __restrict__ g,
+                                                             const uint8_t* __restrict__ bits,
+                                                             const int32_t* __restrict__ chunk_off) {
+    const int c = blockIdx.x, h = blockIdx.y, s = blockIdx.z;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long ws = T > W ? T - W : 0;
+    const long nchunk = (T + ADM_CHUNK - 1) / ADM_CHUNK;
+    const size_t bh = (size_t)s * pv.kv_heads + h;
+    const long hidx = pv.head_index(layer, seq0 + s, h);
+    const int d = pv.head_dim, ps = pv.page_size;
+    const int G = chunk_off[bh * (nchunk + 1) + nchunk];
+    // a failed page claim leaves global_len = 0 (admit_plan_kernel)
+    if (G > 0 && pv.state[hidx].global_len != G) return;
+    if (pv.state[hidx].tokens_seen != (int)T || (T > 0 && pv.state[hidx].local_len == 0)) return;
+
+    __shared__ int wcnt[4];
+    const long t = (long)c * ADM_CHUNK + wid * 32 + lane;
+    const bool valid = t < T;
+    const bool glob = valid && t < ws && bits[bh * T + t] != 0;
+    const unsigned gm = __ballot_sync(0xffffffffu, glob);
+    if (lane == 0) wcnt[wid] = __popc(gm);
+    __syncthreads();
+    int base = chunk_off[bh * (nchunk + 1) + c];
+    for (int w = 0; w < wid; ++w) base += wcnt[w];
+    const int rank = base + __popc(gm & ((1u << lane) - 1u));
+
+    // per-lane destination (page, slot) or -1
+    int dpage = -1, dslot = 0;
+    if (glob) {
+        dpage = pv.gpt[hidx * pv.n_gp + rank / ps];
+        dslot = rank % ps;
+    } else if (valid && t >= ws) {
+        const long r = t - ws;  // ring slot (local_ptr starts at 0)
+        dpage = pv.lpt[hidx * pv.n_lp + r / ps];
+        dslot = (int)(r % ps);
+    }
+    if (dpage >= 0) {
+        const size_t mi = (size_t)dpage * ps + dslot;
+        pv.gate[mi] = g[bh * T + t];
+        pv.pos[mi] = (int32_t)t;
+        pv.adm[mi] = bits[bh * T + t];
+    }
+    unsigned mv = __ballot_sync(0xffffffffu, dpage >= 0);
+    E* pool = reinterpret_cast<E*>(pv.data);
+    while (mv) {
+        const int src = __ffs(mv) - 1;
+        mv &= mv - 1;
+        const int p = __shfl_sync(0xffffffffu, dpage, src);
+        const int sl = __shfl_sync(0xffffffffu, dslot, src);
+        const long ts = (long)c * ADM_CHUNK + wid * 32 + src;
+        const size_t row = (((size_t)s * T + ts) * pv.kv_heads + h) * d;
+        E* kdst = pool + (size_t)p * pv.page_elems() + (size_t)sl * d;
+        copy_row_warp(kdst, k_post + row, d, lane);
+        copy_row_warp(kdst + (size_t)ps * d, v + row, d, lane);
+    }
+}
+
+template <typename E>
+int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long T, long W, const E* k_post,
+                         const E* v, const float* g, const uint8_t* bits, int32_t* chunk_off, cudaStream_t st) {
+    admit_plan_kernel<<<dim3(nseq, pv.kv_heads), 1024, 0, st>>>(pv, layer, seq0, T, W, bits, chunk_off);
+    const long nchunk = (T + ADM_CHUNK - 1) / ADM_CHUNK;
+    admit_scatter_kernel<E><<<dim3((unsigned)nchunk, pv.kv_heads, nseq), 128, 0, st>>>(pv, layer, seq0, T, W, k_post,
+                                                                                      v, g, bits, chunk_off);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
+// K4: decode append.  One CTA (256 threads) per (seq, kv head).
+// ---------------------------------------------------------------------------
+template <typename E>
+__global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0, long W,
+                                                             const E* __restrict__ k_pre, const E* __restrict__ v,
+                                                             const float* __restrict__ forced_g,
+                                                             float* __restrict__ g_out, int32_t* __restrict__ events) {
+    extern __shared__ double dsh[];
+    const int s = blockIdx.x / pv.kv_heads, h = blockIdx.x % pv.kv_heads;
+    const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
+    const long hidx = pv.head_index(layer, seq0 + s, h);
+    double* xs = dsh;                       // [2d]
+    double* scratch = xs + 2 * d;           // [2*hidden + 32]
+    float* kpost = reinterpret_cast<float*>(scratch + 2 * ga.hidden + 32);  // [d]
+    __shared__ HeadState st;
+    __shared__ int vpage, vslot, gpage, gslot, npage, nslot, event;
+    __shared__ float gval;
+    if (tid == 0) st = pv.state[hidx];
+    __syncthreads();
+    const long pos = st.tokens_seen;
+    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
+    // RoPE (fp32 for the stored key, fp64 for the gate feature)
+    for (int i = tid; i < d / 2; i += blockDim.x) {
+        const float x0 = to_f(k_pre[in + 2 * i]), x1 = to_f(k_pre[in + 2 * i + 1]);
+        float c, sn;
+        rope_cs(ga.freq, i, pos, c, sn);
+        kpost[2 * i] = x0 * c - x1 * sn;
+        kpost[2 * i + 1] = x0 * sn + x1 * c;
+        const double angle = (double)pos * ga.freq[i];
+        const double cd = cos(angle), sd = sin(angle);
+        xs[2 * i] = x0;
+        xs[2 * i + 1] = x1;
+        xs[d + 2 * i] = (double)x0 * cd - (double)x1 * sd;
+        xs[d + 2 * i + 1] = (double)x0 * sd + (double)x1 * cd;
+    }
+    __syncthreads();
+    double g;
+    if (forced_g) {
+        g = forced_g[(size_t)s * pv.kv_heads + h];
+    } else {
+        g = gate_fp64_block(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch);
+    }
+    const uint8_t bit = g >= ga.tau ? 1 : 0;
+    // ---- routing decision (thread 0) ----------------------------------------
+    if (tid == 0) {
+        gval = (float)g;
+        event = 0;
+        vpage = -1;
+        gpage = -1;
+        const int slot = st.local_ptr;
+        int lp = pv.lpt[hidx * pv.n_lp + slot / ps];
+        if (st.local_len < W) {
+            // not full: slot == local_len; a slot at a page boundary is the
+            // first touch of that ring page (kvstore.cpp:102-107)
+            if (slot % ps == 0) {
+                lp = pool_pop(pv);
+                pv.lpt[hidx * pv.n_lp + slot / ps] = lp;
+            }
+            st.local_len += 1;
+        } else {
+            // inspect the victim under local_ptr (kvstore.cpp:143-147)
+            const size_t mi = (size_t)(lp < 0 ? 0 : lp) * ps + slot % ps;
+            if (lp < 0) {
+                event = 0;  // head lost its pages to an earlier ENOPAGES
+            } else if (pv.adm[mi]) {
+                event = 1;
+                const int gi = st.global_len;
+                int gp;
+                if (gi % ps == 0) {
+                    gp = pool_pop(pv);
+                    pv.gpt[hidx * pv.n_gp + gi / ps] = gp;
+                } else {
+                    gp = pv.gpt[hidx * pv.n_gp + gi / ps];
+                }
+                vpage = lp;
+                vslot = slot % ps;
+                gpage = gp;
+                gslot = gi % ps;
+                if (gp >= 0) st.global_len += 1;
+            } else {
+                event = 2;
+            }
+        }
+        npage = lp;
+        nslot = slot % ps;
+    }
+    __syncthreads();
+    E* pool = reinterpret_cast<E*>(pv.data);
+    // promote: copy victim (K, V, gate, pos, bit) to the Global append slot
+    if (event == 1 && gpage >= 0 && vpage >= 0) {
+        const E* ks = pool + (size_t)vpage * pv.page_elems() + (size_t)vslot * d;
+        E* kd = pool + (size_t)gpage * pv.page_elems() + (size_t)gslot * d;
+        for (int e = tid; e < d; e += blockDim.x) {
+            kd[e] = ks[e];
+            kd[e + (size_t)ps * d] = ks[e + (size_t)ps * d];
+        }
+        if (tid == 0) {
+            const size_t a = (size_t)vpage * ps + vslot, b = (size_t)gpage * ps + gslot;
+            pv.gate[b] = pv.gate[a];
+            pv.pos[b] = pv.pos[a];
+            pv.adm[b] = pv.adm[a];
+        }
+    }
+    __syncthreads();
+    // write the new token into the ring slot
+    if (npage >= 0) {
+        E* kd = pool + (size_t)npage * pv.page_elems() + (size_t)nslot * d;
+        for (int e = tid; e < d; e += blockDim.x) {
+            kd[e] = from_f<E>(kpost[e]);
+            kd[e + (size_t)ps * d] = v[in + e];
+        }
+        if (tid == 0) {
+            const size_t b = (size_t)npage * ps + nslot;
+            pv.gate[b] = gval;
+            pv.pos[b] = (int32_t)pos;
+            pv.adm[b] = bit;
+        }
+    }
+    if (tid == 0) {
+        st.local_ptr = (int)((st.local_ptr + 1) % W);
+        st.tokens_seen += 1;
+        pv.state[hidx] = st;
+        if (g_out) g_out[(size_t)s * pv.kv_heads + h] = gval;
+        if (events) events[(size_t)s * pv.kv_heads + h] = event;
+    }
+}
+
+template <typename E>
+int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
+                         const E* k_pre, const E* v, const float* forced_g, float* g_out, int32_t* events,
+                         cudaStream_t st) {
+    const size_t smem = sizeof(double) * (2 * pv.head_dim + 2 * ga.hidden + 32) + sizeof(float) * pv.head_dim;
+    decode_append_kernel<E><<<nseq * pv.kv_heads, 256, smem, st>>>(pv, ga, layer, seq0, W, k_pre, v, forced_g, g_out,
+                                                                   events);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+#define INST(E)                                                                                                   \
+    template int launch_admit_prefill<E>(const PoolView&, int, int, int, long, long, const E*, const E*,          \
+                                         const float*, const uint8_t*, int32_t*, cudaStream_t);                   \
+    template int launch_decode_append<E>(const PoolView&, const GateArgs&, int, int, int, long, const E*, const E*, \
+                                         const float*, float*, int32_t*, cudaStream_t);
+INST(float)
+INST(__nv_bfloat16)
+#undef INST
+
+}  // namespace wgkv

@@ -1,0 +1,635 @@
+// api.cu -- the C-ABI (include/wgkv_b200.h): context, device state, and the
+// host orchestration of K1..K5 mirroring Session::prefill / decode_step
+// (engine.cpp:153-341).  No allocation on hot calls; everything is
+// stream-ordered on the context stream.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "admit.cuh"
+#include "attn.cuh"
+#include "attn_tc.cuh"
+#include "gate.cuh"
+
+using namespace wgkv;
+
+static thread_local std::string g_last_error;
+void wgkv_set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+
+int fail(int code, const std::string& msg) {
+    wgkv_set_error(msg);
+    return code;
+}
+
+template <typename T>
+T* dalloc(size_t n, std::vector<void*>& owned) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+
+__global__ void init_stack_kernel(int32_t* stack, long cap) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < cap; i += (long)gridDim.x * blockDim.x)
+        stack[i] = (int32_t)(cap - 1 - i);
+}
+
+// HeadCache::release (kvstore.cpp:243-251) for every (layer, slot, head)
+__global__ void release_kernel(PoolView pv, int layers, int seq0, int nseq) {
+    const int idx = blockIdx.x;
+    const int l = idx / (nseq * pv.kv_heads), r = idx % (nseq * pv.kv_heads);
+    const int s = seq0 + r / pv.kv_heads, h = r % pv.kv_heads;
+    const long hidx = pv.head_index(l, s, h);
+    const HeadState st = pv.state[hidx];
+    const int ng = (st.global_len + pv.page_size - 1) / pv.page_size;
+    const int nl = (min(st.local_len, 0x7fffffff) + pv.page_size - 1) / pv.page_size;
+    __shared__ int base;
+    if (threadIdx.x == 0) base = atomicAdd(pv.free_top, nl + ng);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nl + ng; i += blockDim.x)
+        pv.free_stack[base + i] = i < nl ? pv.lpt[hidx * pv.n_lp + i] : pv.gpt[hidx * pv.n_gp + (i - nl)];
+    __syncthreads();
+    if (threadIdx.x == 0) pv.state[hidx] = HeadState{0, 0, 0, 0};
+}
+
+}  // namespace
+
+struct wgkv_ctx {
+    wgkv_config cfg{};
+    cudaStream_t stream = nullptr;
+    size_t esz = 2;
+    std::vector<void*> owned;
+    PoolView pv{};
+    // gate parameters
+    float *w1t = nullptr, *b1f = nullptr, *w2f = nullptr;
+    double *b2f = nullptr, *w1d = nullptr, *b1d = nullptr, *w2d = nullptr, *freq = nullptr;
+    bool gates_set = false;
+    // workspaces
+    void* ws_kpost = nullptr;
+    float* ws_g = nullptr;
+    uint8_t* ws_bits = nullptr;
+    int32_t* ws_chunk = nullptr;
+    int64_t* ws_cand = nullptr;
+    int* ws_cnt = nullptr;  // [0] candidates, [1] near count
+    int64_t* ws_near = nullptr;
+    float* ws_part = nullptr;
+    int max_chunks = 64;
+    long near_cap = 0;
+    // host mirrors for lifecycle checks and grid sizing
+    std::vector<uint8_t> prefilled;  // [L][S]
+    std::vector<long> tokens;        // [L][S] tokens seen
+
+    GateArgs gate_args(int layer, long T, long pos0) const {
+        GateArgs a{};
+        a.layer = layer;
+        a.kv_heads = cfg.kv_heads;
+        a.bank_heads = cfg.kv_heads;
+        a.head_offset = 0;
+        a.d = cfg.head_dim;
+        a.hidden = cfg.hidden;
+        a.T = T;
+        a.pos0 = pos0;
+        a.tau = cfg.tau;
+        a.ztau = (float)std::log(cfg.tau / (1.0 - cfg.tau));
+        a.freq = freq;
+        a.w1t = w1t;
+        a.b1f = b1f;
+        a.w2f = w2f;
+        a.b2f = b2f;
+        a.w1d = w1d;
+        a.b1d = b1d;
+        a.w2d = w2d;
+        a.b2d = b2f;
+        return a;
+    }
+    bool use_tc() const {
+        // the tcgen05 kernel is opt-in until it is parity-green on the GPU
+        if (cfg.attn_impl != WGKV_ATTN_TCGEN05) return false;
+        return cfg.dtype == WGKV_BF16 && cfg.head_dim == 128 && 128 % cfg.page_size == 0;
+    }
+};
+
+extern "C" {
+
+const char* wgkv_last_error(void) { return g_last_error.c_str(); }
+const char* wgkv_version(void) { return "wgkv_b200 0.1 sm_100a"; }
+
+int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
+    if (!cfg_in || !out) return fail(WGKV_EINVAL, "wgkv_ctx_create: null argument");
+    const wgkv_config c = *cfg_in;
+    if (c.layers < 1 || c.q_heads < 1 || c.kv_heads < 1 || c.q_heads % c.kv_heads != 0)
+        return fail(WGKV_EINVAL, "wgkv_ctx_create: bad head/layer geometry");
+    if (c.head_dim <= 0 || c.head_dim % 2 != 0) return fail(WGKV_EINVAL, "rope: head_dim must be even");
+    if (c.head_dim % 32 != 0 || c.head_dim > 256) return fail(WGKV_ENOTSUP, "head_dim must be a multiple of 32 <= 256");
+    if (c.window < 1) return fail(WGKV_EINVAL, "HeadCache: window must be >= 1");
+    if (!(c.tau > 0.0 && c.tau < 1.0)) return fail(WGKV_EINVAL, "binarize: tau must lie in (0,1)");
+    if (c.page_size < 1 || c.page_size > 32) return fail(WGKV_ENOTSUP, "page_size must be in [1, 32]");
+    if (c.hidden < 1 || c.max_seqs < 1 || c.max_tokens < 1) return fail(WGKV_EINVAL, "bad sizes");
+    if (c.dtype != WGKV_BF16 && c.dtype != WGKV_F32) return fail(WGKV_EINVAL, "bad dtype");
+    if (cudaSetDevice(c.device) != cudaSuccess) return fail(WGKV_ECUDA, "cudaSetDevice failed");
+
+    auto* ctx = new wgkv_ctx();
+    ctx->cfg = c;
+    if (ctx->cfg.max_prefill_tokens <= 0) ctx->cfg.max_prefill_tokens = c.max_tokens;
+    ctx->esz = c.dtype == WGKV_BF16 ? 2 : 4;
+    const int ps = c.page_size, d = c.head_dim, H = c.kv_heads, S = c.max_seqs, L = c.layers;
+    const int n_lp = (int)((c.window + ps - 1) / ps);
+    const int n_gp = (int)((c.max_tokens + ps - 1) / ps + 1);
+    long cap = c.capacity_pages;
+    if (cap <= 0) cap = (long)L * H * S * (n_lp + n_gp);  // default_capacity (engine.cpp:88-93)
+    ctx->cfg.capacity_pages = cap;
+    auto& o = ctx->owned;
+    PoolView& pv = ctx->pv;
+    pv.page_size = ps;
+    pv.head_dim = d;
+    pv.n_lp = n_lp;
+    pv.n_gp = n_gp;
+    pv.max_seqs = S;
+    pv.kv_heads = H;
+    pv.capacity = cap;
+    pv.data = dalloc<uint8_t>((size_t)cap * 2 * ps * d * ctx->esz, o);
+    pv.gate = dalloc<float>((size_t)cap * ps, o);
+    pv.pos = dalloc<int32_t>((size_t)cap * ps, o);
+    pv.adm = dalloc<uint8_t>((size_t)cap * ps, o);
+    pv.free_stack = dalloc<int32_t>((size_t)cap, o);
+    pv.free_top = dalloc<int32_t>(1, o);
+    pv.err = dalloc<int32_t>(1, o);
+    pv.lpt = dalloc<int32_t>((size_t)L * S * H * n_lp, o);
+    pv.gpt = dalloc<int32_t>((size_t)L * S * H * n_gp, o);
+    pv.state = dalloc<HeadState>((size_t)L * S * H, o);
+    const size_t blocks = (size_t)L * H, fd = 2 * (size_t)d;
+    ctx->w1t = dalloc<float>(blocks * fd * c.hidden, o);
+    ctx->b1f = dalloc<float>(blocks * c.hidden, o);
+    ctx->w2f = dalloc<float>(blocks * c.hidden, o);
+    ctx->b2f = dalloc<double>(blocks, o);
+    ctx->w1d = dalloc<double>(blocks * fd * c.hidden, o);
+    ctx->b1d = dalloc<double>(blocks * c.hidden, o);
+    ctx->w2d = dalloc<double>(blocks * c.hidden, o);
+    ctx->freq = dalloc<double>((size_t)d / 2, o);
+    const long Tm = ctx->cfg.max_prefill_tokens;
+    const size_t toks = (size_t)S * Tm * H;
+    ctx->ws_kpost = dalloc<uint8_t>(toks * d * ctx->esz, o);
+    ctx->ws_g = dalloc<float>(toks, o);
+    ctx->ws_bits = dalloc<uint8_t>(toks, o);
+    ctx->ws_chunk = dalloc<int32_t>((size_t)S * H * ((Tm + 127) / 128 + 1), o);
+    ctx->ws_cand = dalloc<int64_t>(toks, o);
+    ctx->ws_cnt = dalloc<int>(4, o);
+    ctx->near_cap = 1 << 20;
+    ctx->ws_near = dalloc<int64_t>((size_t)ctx->near_cap, o);
+    const int gs = c.q_heads / c.kv_heads;
+    ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
+    for (void* p : o)
+        if (!p) {
+            for (void* q : o) cudaFree(q);
+            delete ctx;
+            return fail(WGKV_ECUDA, "wgkv_ctx_create: cudaMalloc failed (pool of " + std::to_string(cap) + " pages)");
+        }
+    // RoPE frequencies with the reference expression (numerics.cpp:54)
+    std::vector<double> fr(d / 2);
+    for (int i = 0; i < d / 2; ++i) fr[i] = std::pow(c.rope_base, -2.0 * i / d);
+    cudaMemcpy(ctx->freq, fr.data(), sizeof(double) * fr.size(), cudaMemcpyHostToDevice);
+    init_stack_kernel<<<256, 256>>>(pv.free_stack, cap);
+    const int32_t top = (int32_t)cap, zero = 0;
+    cudaMemcpy(pv.free_top, &top, sizeof(top), cudaMemcpyHostToDevice);
+    cudaMemcpy(pv.err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
+    cudaMemset(pv.state, 0, sizeof(HeadState) * (size_t)L * S * H);
+    cudaMemset(pv.lpt, 0xff, sizeof(int32_t) * (size_t)L * S * H * n_lp);
+    cudaMemset(pv.gpt, 0xff, sizeof(int32_t) * (size_t)L * S * H * n_gp);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        for (void* q : o) cudaFree(q);
+        delete ctx;
+        return fail(WGKV_ECUDA, "wgkv_ctx_create: init failed");
+    }
+    ctx->prefilled.assign((size_t)L * S, 0);
+    ctx->tokens.assign((size_t)L * S, 0);
+    *out = ctx;
+    return WGKV_OK;
+}
+
+int wgkv_ctx_destroy(wgkv_ctx* ctx) {
+    if (!ctx) return WGKV_OK;
+    cudaSetDevice(ctx->cfg.device);
+    cudaDeviceSynchronize();
+    for (void* p : ctx->owned) cudaFree(p);
+    delete ctx;
+    return WGKV_OK;
+}
+
+int wgkv_set_stream(wgkv_ctx* ctx, void* stream) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return WGKV_OK;
+}
+
+int wgkv_sync(wgkv_ctx* ctx) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    int32_t err = 0;
+    WGKV_CUDA_TRY(cudaMemcpy(&err, ctx->pv.err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err == WGKV_ENOPAGES) {
+        const int32_t zero = 0;
+        cudaMemcpy(ctx->pv.err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
+        char msg[160];
+        std::snprintf(msg, sizeof(msg), "out of pages: capacity=%ld", ctx->pv.capacity);
+        return fail(WGKV_ENOPAGES, msg);
+    }
+    return err;
+}
+
+int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_heads) {
+    if (!ctx || !bank) return fail(WGKV_EINVAL, "null argument");
+    const auto& c = ctx->cfg;
+    if (bank_layers != c.layers || bank_heads < c.kv_head_offset + c.kv_heads)
+        return fail(WGKV_EINVAL, "Session: gate bank shape does not match model");
+    const int d = c.head_dim, hid = c.hidden, fd = 2 * d;
+    const size_t blen = (size_t)hid * fd + 2 * (size_t)hid + 1;
+    const size_t nb = (size_t)c.layers * c.kv_heads;
+    std::vector<float> w1t(nb * fd * hid), b1f(nb * hid), w2f(nb * hid);
+    std::vector<double> w1d(nb * fd * hid), b1d(nb * hid), w2d(nb * hid), b2(nb);
+    for (int l = 0; l < c.layers; ++l)
+        for (int h = 0; h < c.kv_heads; ++h) {
+            const double* blk = bank + ((size_t)l * bank_heads + c.kv_head_offset + h) * blen;
+            const size_t b = (size_t)l * c.kv_heads + h;
+            for (int u = 0; u < hid; ++u)
+                for (int k = 0; k < fd; ++k) {
+                    w1d[(b * hid + u) * fd + k] = blk[(size_t)u * fd + k];
+                    w1t[(b * fd + k) * hid + u] = (float)blk[(size_t)u * fd + k];
+                }
+            for (int u = 0; u < hid; ++u) {
+                b1d[b * hid + u] = blk[(size_t)hid * fd + u];
+                w2d[b * hid + u] = blk[(size_t)hid * fd + hid + u];
+                b1f[b * hid + u] = (float)b1d[b * hid + u];
+                w2f[b * hid + u] = (float)w2d[b * hid + u];
+            }
+            b2[b] = blk[(size_t)hid * fd + 2 * hid];
+        }
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->w1t, w1t.data(), w1t.size() * 4, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->b1f, b1f.data(), b1f.size() * 4, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->w2f, w2f.data(), w2f.size() * 4, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->w1d, w1d.data(), w1d.size() * 8, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->b1d, b1d.data(), b1d.size() * 8, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->w2d, w2d.data(), w2d.size() * 8, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->b2f, b2.data(), b2.size() * 8, cudaMemcpyHostToDevice));
+    ctx->gates_set = true;
+    return WGKV_OK;
+}
+
+// GateBank::load (gating.cpp:107-147): "WGKV", u32 version/L/H/head_dim/hidden, f64 blocks
+int wgkv_gate_load(wgkv_ctx* ctx, const char* path) {
+    if (!ctx || !path) return fail(WGKV_EINVAL, "null argument");
+    std::ifstream is(path, std::ios::binary);
+    if (!is) return fail(WGKV_ERUNTIME, std::string("GateBank::load: cannot open ") + path);
+    char magic[4];
+    uint32_t hdr[5];
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "WGKV", 4) != 0)
+        return fail(WGKV_ERUNTIME, std::string("GateBank::load: bad magic in ") + path);
+    is.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
+    if (!is || hdr[0] != 1u) return fail(WGKV_ERUNTIME, "GateBank::load: unsupported version");
+    const int L = (int)hdr[1], H = (int)hdr[2], d = (int)hdr[3], hid = (int)hdr[4];
+    if (d != ctx->cfg.head_dim || hid != ctx->cfg.hidden)
+        return fail(WGKV_EINVAL, "Session: gate bank shape does not match model");
+    const size_t n = (size_t)L * H * ((size_t)hid * 2 * d + 2 * hid + 1);
+    std::vector<double> bank(n);
+    is.read(reinterpret_cast<char*>(bank.data()), (std::streamsize)(n * 8));
+    if (!is) return fail(WGKV_ERUNTIME, std::string("GateBank::load: truncated file ") + path);
+    return wgkv_gate_set(ctx, bank.data(), L, H);
+}
+
+static int check_slots(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T) {
+    const auto& c = ctx->cfg;
+    if (layer < 0 || layer >= c.layers) return fail(WGKV_EINVAL, "layer out of range");
+    if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
+    if (T < 0 || T > c.max_prefill_tokens) return fail(WGKV_EINVAL, "T exceeds max_prefill_tokens");
+    return WGKV_OK;
+}
+
+int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const void* k_pre, const float* forced_g,
+                    void* k_post_out, float* g_out, uint8_t* bits_out, int64_t* near_idx, int near_cap,
+                    int* near_count) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    int st = check_slots(ctx, layer, 0, nseq, T);
+    if (st) return st;
+    if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
+    if (T == 0) return WGKV_OK;
+    GateArgs a = ctx->gate_args(layer, T, pos0);
+    int64_t* nidx = near_idx ? near_idx : ctx->ws_near;
+    const int ncap = near_idx ? near_cap : (int)ctx->near_cap;
+    WGKV_CUDA_TRY(cudaMemsetAsync(ctx->ws_cnt + 1, 0, sizeof(int), ctx->stream));
+    if (forced_g) {
+        // effective_gate override (engine.cpp:126-151): RoPE only, g = forced, bit = g >= tau
+        st = launch_forced_gate(a, nseq, k_pre, k_post_out, forced_g, g_out, bits_out, ctx->esz, ctx->stream);
+    } else if (ctx->cfg.dtype == WGKV_BF16) {
+        st = launch_gate_prefill<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)k_pre, (__nv_bfloat16*)k_post_out,
+                                                g_out, bits_out, ctx->ws_cand, ctx->ws_cnt, nidx, ncap,
+                                                ctx->ws_cnt + 1, ctx->stream);
+    } else {
+        st = launch_gate_prefill<float>(a, nseq, (const float*)k_pre, (float*)k_post_out, g_out, bits_out,
+                                        ctx->ws_cand, ctx->ws_cnt, nidx, ncap, ctx->ws_cnt + 1, ctx->stream);
+    }
+    if (st) return fail(st, std::string("gate kernels: ") + cudaGetErrorString(cudaGetLastError()));
+    if (near_count) {
+        WGKV_CUDA_TRY(cudaMemcpyAsync(near_count, ctx->ws_cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    return WGKV_OK;
+}
+
+int wgkv_admit_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* k_post, const void* v,
+                       const float* g, const uint8_t* bits) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    int st = check_slots(ctx, layer, seq0, nseq, T);
+    if (st) return st;
+    if (T < 1) return fail(WGKV_EINVAL, "Session::prefill: empty prompt");
+    if (T > ctx->cfg.max_tokens) return fail(WGKV_EINVAL, "T exceeds max_tokens");
+    for (int s = seq0; s < seq0 + nseq; ++s)
+        if (ctx->prefilled[(size_t)layer * ctx->cfg.max_seqs + s])
+            return fail(WGKV_ESTATE, "prefill_populate: cache not empty");
+    if (ctx->cfg.dtype == WGKV_BF16)
+        st = launch_admit_prefill<__nv_bfloat16>(ctx->pv, layer, seq0, nseq, T, ctx->cfg.window,
+                                                 (const __nv_bfloat16*)k_post, (const __nv_bfloat16*)v, g, bits,
+                                                 ctx->ws_chunk, ctx->stream);
+    else
+        st = launch_admit_prefill<float>(ctx->pv, layer, seq0, nseq, T, ctx->cfg.window, (const float*)k_post,
+                                         (const float*)v, g, bits, ctx->ws_chunk, ctx->stream);
+    if (st) return fail(st, "admit kernels failed");
+    for (int s = seq0; s < seq0 + nseq; ++s) {
+        ctx->prefilled[(size_t)layer * ctx->cfg.max_seqs + s] = 1;
+        ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] = T;
+    }
+    return WGKV_OK;
+}
+
+int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* q, const void* k_post,
+                    const void* v, const uint8_t* bits, void* out) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    int st = check_slots(ctx, layer, seq0, nseq, T);
+    if (st) return st;
+    VsArgs a{};
+    a.pv = ctx->pv;
+    a.layer = layer;
+    a.seq0 = seq0;
+    a.q_heads = ctx->cfg.q_heads;
+    a.T = T;
+    a.W = ctx->cfg.window;
+    a.freq = ctx->freq;
+    a.bits = bits;
+    a.chunk_off = ctx->ws_chunk;
+    if (ctx->use_tc())
+        st = launch_vs_prefill_tc(a, nseq, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k_post,
+                                  (const __nv_bfloat16*)v, (__nv_bfloat16*)out, ctx->stream);
+    else if (ctx->cfg.dtype == WGKV_BF16)
+        st = launch_vs_prefill_simt<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k_post,
+                                                   (const __nv_bfloat16*)v, (__nv_bfloat16*)out, ctx->stream);
+    else
+        st = launch_vs_prefill_simt<float>(a, nseq, (const float*)q, (const float*)k_post, (const float*)v,
+                                           (float*)out, ctx->stream);
+    if (st) return fail(st, std::string("vs prefill kernel: ") + cudaGetErrorString(cudaGetLastError()));
+    return WGKV_OK;
+}
+
+int wgkv_prefill_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* q, const void* k_pre,
+                       const void* v, const float* forced_g, void* out, float* g_out, uint8_t* bits_out) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    int st = check_slots(ctx, layer, seq0, nseq, T);
+    if (st) return st;
+    if (T < 1) return fail(WGKV_EINVAL, "Session::prefill: empty prompt");
+    for (int s = seq0; s < seq0 + nseq; ++s)
+        if (ctx->prefilled[(size_t)layer * ctx->cfg.max_seqs + s])
+            return fail(WGKV_ESTATE, "Session::prefill: already prefilled");
+    float* g = g_out ? g_out : ctx->ws_g;
+    uint8_t* bits = bits_out ? bits_out : ctx->ws_bits;
+    st = wgkv_gate_score(ctx, layer, nseq, T, 0, k_pre, forced_g, ctx->ws_kpost, g, bits, nullptr, 0, nullptr);
+    if (st) return st;
+    st = wgkv_admit_prefill(ctx, layer, seq0, nseq, T, ctx->ws_kpost, v, g, bits);
+    if (st) return st;
+    return wgkv_vs_prefill(ctx, layer, seq0, nseq, T, q, ctx->ws_kpost, v, bits, out);
+}
+
+static int decode_check(wgkv_ctx* ctx, int layer, int seq0, int nseq) {
+    int st = check_slots(ctx, layer, seq0, nseq, 0);
+    if (st) return st;
+    for (int s = seq0; s < seq0 + nseq; ++s) {
+        const size_t i = (size_t)layer * ctx->cfg.max_seqs + s;
+        if (!ctx->prefilled[i]) return fail(WGKV_ESTATE, "Session::decode_step: prefill required first");
+    }
+    return WGKV_OK;
+}
+
+int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
+                        const float* forced_g, float* g_out, int32_t* events_out) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    int st = decode_check(ctx, layer, seq0, nseq);
+    if (st) return st;
+    for (int s = seq0; s < seq0 + nseq; ++s)
+        if (ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] >= ctx->cfg.max_tokens)
+            return fail(WGKV_EINVAL, "sequence exceeds max_tokens");
+    if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
+    GateArgs ga = ctx->gate_args(layer, 1, 0);
+    if (ctx->cfg.dtype == WGKV_BF16)
+        st = launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
+                                                 (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g,
+                                                 g_out, events_out, ctx->stream);
+    else
+        st = launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
+                                         (const float*)v, forced_g, g_out, events_out, ctx->stream);
+    if (st) return fail(st, "decode append kernel failed");
+    for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
+    return WGKV_OK;
+}
+
+int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    int st = decode_check(ctx, layer, seq0, nseq);
+    if (st) return st;
+    const auto& c = ctx->cfg;
+    long tmax = 0;
+    for (int s = seq0; s < seq0 + nseq; ++s) tmax = std::max(tmax, ctx->tokens[(size_t)layer * c.max_seqs + s]);
+    // upper bound of resident pages per head: Global <= tokens - W entries
+    const long gmax = tmax > c.window ? tmax - c.window : 0;
+    const long np = (gmax + c.page_size - 1) / c.page_size + (c.window + c.page_size - 1) / c.page_size;
+    const long target = (long)kNumSMs * 4;
+    long cp = (np * nseq * c.kv_heads + target - 1) / target;
+    cp = std::max(cp, 4L);
+    cp = std::max(cp, (np + ctx->max_chunks - 1) / ctx->max_chunks);
+    DecArgs a{};
+    a.pv = ctx->pv;
+    a.layer = layer;
+    a.seq0 = seq0;
+    a.q_heads = c.q_heads;
+    a.chunk_pages = (int)cp;
+    a.n_chunks = (int)((np + cp - 1) / cp);
+    a.max_chunks = ctx->max_chunks;
+    a.freq = ctx->freq;
+    if (c.topk_budget > 0) return fail(WGKV_ENOTSUP, "topk decode not built in this revision");
+    if (c.dtype == WGKV_BF16)
+        st = launch_decode_attn_simt<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part,
+                                                    (__nv_bfloat16*)out, ctx->stream);
+    else
+        st = launch_decode_attn_simt<float>(a, nseq, (const float*)q, ctx->ws_part, (float*)out, ctx->stream);
+    if (st) return fail(st, std::string("decode attention: ") + cudaGetErrorString(cudaGetLastError()));
+    return WGKV_OK;
+}
+
+int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, const void* k_pre, const void* v,
+                      const float* forced_g, void* out, float* g_out, int32_t* events_out) {
+    int st = wgkv_decode_step_kv(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out);
+    if (st) return st;
+    return wgkv_decode_attn(ctx, layer, seq0, nseq, q, out);
+}
+
+int wgkv_cache_state(wgkv_ctx* ctx, int layer, int seq, int kv_head, int64_t* lens) {
+    if (!ctx || !lens) return fail(WGKV_EINVAL, "null argument");
+    const auto& c = ctx->cfg;
+    if (layer < 0 || layer >= c.layers || seq < 0 || seq >= c.max_seqs || kv_head < 0 || kv_head >= c.kv_heads)
+        return fail(WGKV_EINVAL, "index out of range");
+    WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    HeadState st;
+    WGKV_CUDA_TRY(cudaMemcpy(&st, ctx->pv.state + ctx->pv.head_index(layer, seq, kv_head), sizeof(st),
+                             cudaMemcpyDeviceToHost));
+    const int ps = c.page_size;
+    lens[0] = st.local_len;
+    lens[1] = st.local_ptr;
+    lens[2] = st.global_len;
+    lens[3] = st.tokens_seen;
+    lens[4] = (st.local_len + ps - 1) / ps;
+    lens[5] = (st.global_len + ps - 1) / ps;
+    return WGKV_OK;
+}
+
+static float elem_to_f(const uint8_t* p, size_t esz) {
+    if (esz == 4) {
+        float f;
+        std::memcpy(&f, p, 4);
+        return f;
+    }
+    uint16_t h;
+    std::memcpy(&h, p, 2);
+    const uint32_t u = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk, float* gv, int64_t* gpos,
+                      float* ggate, float* lk, float* lv, int64_t* lpos, float* lgate) {
+    int64_t lens[6];
+    int st = wgkv_cache_state(ctx, layer, seq, kv_head, lens);
+    if (st) return st;
+    const auto& c = ctx->cfg;
+    const int ps = c.page_size, d = c.head_dim;
+    const long hidx = ctx->pv.head_index(layer, seq, kv_head);
+    std::vector<int32_t> lpt(ctx->pv.n_lp), gpt(ctx->pv.n_gp);
+    WGKV_CUDA_TRY(cudaMemcpy(lpt.data(), ctx->pv.lpt + hidx * ctx->pv.n_lp, sizeof(int32_t) * lpt.size(),
+                             cudaMemcpyDeviceToHost));
+    WGKV_CUDA_TRY(cudaMemcpy(gpt.data(), ctx->pv.gpt + hidx * ctx->pv.n_gp, sizeof(int32_t) * gpt.size(),
+                             cudaMemcpyDeviceToHost));
+    const size_t pbytes = (size_t)2 * ps * d * ctx->esz;
+    std::vector<uint8_t> page(pbytes);
+    std::vector<float> pg(ps);
+    std::vector<int32_t> pp(ps);
+    auto fetch = [&](int p) -> int {
+        WGKV_CUDA_TRY(cudaMemcpy(page.data(), (uint8_t*)ctx->pv.data + (size_t)p * pbytes, pbytes,
+                                 cudaMemcpyDeviceToHost));
+        WGKV_CUDA_TRY(cudaMemcpy(pg.data(), ctx->pv.gate + (size_t)p * ps, sizeof(float) * ps, cudaMemcpyDeviceToHost));
+        WGKV_CUDA_TRY(cudaMemcpy(pp.data(), ctx->pv.pos + (size_t)p * ps, sizeof(int32_t) * ps, cudaMemcpyDeviceToHost));
+        return WGKV_OK;
+    };
+    auto emit = [&](int slot, long row, float* k, float* v, int64_t* pos, float* gate) {
+        for (int e = 0; e < d; ++e) {
+            if (k) k[row * d + e] = elem_to_f(page.data() + ((size_t)slot * d + e) * ctx->esz, ctx->esz);
+            if (v) v[row * d + e] = elem_to_f(page.data() + ((size_t)(ps + slot) * d + e) * ctx->esz, ctx->esz);
+        }
+        if (pos) pos[row] = pp[slot];
+        if (gate) gate[row] = pg[slot];
+    };
+    int cur = -1;
+    for (long g = 0; g < lens[2]; ++g) {
+        const int p = gpt[g / ps];
+        if (p != cur) {
+            if ((st = fetch(p))) return st;
+            cur = p;
+        }
+        emit((int)(g % ps), g, gk, gv, gpos, ggate);
+    }
+    // unroll the ring oldest-first from local_ptr when full (kvstore.cpp:229-239)
+    const long W = c.window, Lc = lens[0], start = Lc < W ? 0 : lens[1];
+    cur = -1;
+    for (long n = 0; n < Lc; ++n) {
+        const long ring = (start + n) % W;
+        const int p = lpt[ring / ps];
+        if (p != cur) {
+            if ((st = fetch(p))) return st;
+            cur = p;
+        }
+        emit((int)(ring % ps), n, lk, lv, lpos, lgate);
+    }
+    return WGKV_OK;
+}
+
+int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out) {
+    if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
+    const auto& c = ctx->cfg;
+    WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::vector<HeadState> st((size_t)c.layers * c.max_seqs * c.kv_heads);
+    WGKV_CUDA_TRY(cudaMemcpy(st.data(), ctx->pv.state, sizeof(HeadState) * st.size(), cudaMemcpyDeviceToHost));
+    int64_t res = 0, glob = 0, seen = 0, pages = 0;
+    for (int l = 0; l < c.layers; ++l)
+        for (int s = seq0; s < seq0 + nseq; ++s)
+            for (int h = 0; h < c.kv_heads; ++h) {
+                const HeadState& x = st[ctx->pv.head_index(l, s, h)];
+                res += x.local_len + x.global_len;
+                glob += x.global_len;
+                seen += x.tokens_seen;
+                pages += (x.local_len + c.page_size - 1) / c.page_size + (x.global_len + c.page_size - 1) / c.page_size;
+            }
+    out[0] = res;
+    out[1] = glob;
+    out[2] = seen;
+    out[3] = pages;
+    return WGKV_OK;
+}
+
+int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    const auto& c = ctx->cfg;
+    if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
+    release_kernel<<<c.layers * nseq * c.kv_heads, 256, 0, ctx->stream>>>(ctx->pv, c.layers, seq0, nseq);
+    WGKV_CUDA_TRY(cudaGetLastError());
+    for (int l = 0; l < c.layers; ++l)
+        for (int s = seq0; s < seq0 + nseq; ++s) {
+            ctx->prefilled[(size_t)l * c.max_seqs + s] = 0;
+            ctx->tokens[(size_t)l * c.max_seqs + s] = 0;
+        }
+    return WGKV_OK;
+}
+
+int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out) {
+    if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
+    WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    int32_t top = 0;
+    WGKV_CUDA_TRY(cudaMemcpy(&top, ctx->pv.free_top, sizeof(top), cudaMemcpyDeviceToHost));
+    out[0] = ctx->pv.capacity;
+    out[1] = top;
+    return WGKV_OK;
+}
+
+// closed form of vs_mask_pair_count (attention.cpp:182-191) for T queries
+// over T keys at offset 0: sum_i min(i+1, W) + C(i-W+1), C(x) = #admitted j < x
+uint64_t wgkv_vs_pair_count(const uint8_t* bits, long T, long W) {
+    uint64_t total = 0, c = 0;
+    for (long i = 0; i < T; ++i) {
+        const long x = i - W + 1;  // admitted j < x are outside the window
+        if (x > 0) c += bits[x - 1] != 0;
+        total += (uint64_t)std::min(i + 1, W) + (x > 0 ? c : 0);
+    }
+    return total;
+}
+
+}  // extern "C"

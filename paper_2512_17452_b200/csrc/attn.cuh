@@ -1,0 +1,31 @@
+// attn.cuh -- K3 / K5 argument blocks and launchers.
+#pragma once
+#include "common.cuh"
+
+namespace wgkv {
+
+struct VsArgs {
+    PoolView pv;
+    int layer, seq0, q_heads;
+    long T, W;
+    const double* freq;        // [d/2]
+    const uint8_t* bits;       // [nseq][kv_heads][T]
+    const int32_t* chunk_off;  // [nseq][kv_heads][nchunk+1] admitted-before-chunk (K2)
+};
+
+struct DecArgs {
+    PoolView pv;
+    int layer, seq0, q_heads;
+    int chunk_pages;  // virtual pages per CTA
+    int n_chunks;     // chunks launched per (seq, kv head)
+    int max_chunks;   // partial-buffer stride
+    const double* freq;
+};
+
+template <typename T>
+int launch_vs_prefill_simt(const VsArgs& a, int nseq, const T* q, const T* k_post, const T* v, T* out,
+                           cudaStream_t st);
+template <typename T>
+int launch_decode_attn_simt(const DecArgs& a, int nseq, const T* q, float* part, T* out, cudaStream_t st);
+
+}  // namespace wgkv

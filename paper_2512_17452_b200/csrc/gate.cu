@@ -1,0 +1,262 @@
+// gate.cu -- K1: fused RoPE -> write-gate MLP -> sigmoid -> threshold.
+//
+// Replaces gate_forward_batch + build_gate_feature + binarize + apply_rope
+// (gating.cpp:149-190, numerics.cpp:50-77).  Two stages:
+//   gate_prefill_kernel : fp32 SIMT register-tiled GEMM [64 tok x 2d] . [2d x
+//       128 hidden] per CTA with the GELU . w2 reduction, sigmoid and
+//       threshold fused in the epilogue; writes k_post (RoPE'd keys, stored
+//       once for the cache and the band of K3), g and bits, and lists every
+//       token whose z2 lies within a conservative fp32 error band of
+//       logit(tau).
+//   gate_recheck_kernel : one warp per listed token recomputes the gate in
+//       fp64 in the reference's exact operation order (no FMA contraction)
+//       and overwrites g/bit, so bits equal the reference's except where the
+//       fp64 score itself is within 1e-6 of tau (reported).
+// The fp64 routine is shared with decode (K4), where it is the only path.
+#include "gate.cuh"
+
+namespace wgkv {
+
+// ---------------------------------------------------------------------------
+// K1 fp32 main path
+// ---------------------------------------------------------------------------
+constexpr int GT_TOK = 64;   // tokens per CTA
+constexpr int GT_HID = 128;  // hidden units per pass
+constexpr int GT_KC = 32;    // k chunk
+constexpr int GT_XS = GT_TOK + 4;
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2)
+    gate_prefill_kernel(GateArgs a, const T* __restrict__ k_pre, T* __restrict__ k_post, float* __restrict__ g_out,
+                        uint8_t* __restrict__ bits_out, int64_t* __restrict__ cand, int* __restrict__ cand_cnt) {
+    extern __shared__ float4 smem_f4[];
+    float* Xs = reinterpret_cast<float*>(smem_f4);     // [2d][GT_XS]   transposed feature
+    float* Ws = Xs + 2 * a.d * GT_XS;                  // [2][GT_KC][GT_HID]
+    float* zacc = Ws + 2 * GT_KC * GT_HID;             // [GT_TOK]
+    float* sacc = zacc + GT_TOK;                        // [GT_TOK]
+
+    const int tid = threadIdx.x;
+    const int h = blockIdx.y, s = blockIdx.z;
+    const long t0 = (long)blockIdx.x * GT_TOK;
+    const int d = a.d, fd = 2 * d;
+    const int blk = a.layer * a.bank_heads + a.head_offset + h;
+
+    // ---- stage 1: load k_pre, RoPE, write k_post, build Xs ----------------
+    for (int e = tid; e < GT_TOK * (d / 2); e += blockDim.x) {
+        const int tok = e / (d / 2), i = e % (d / 2);
+        const long t = t0 + tok;
+        float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+        if (t < a.T) {
+            const size_t off = (((size_t)s * a.T + t) * a.kv_heads + h) * d + 2 * i;
+            x0 = to_f(k_pre[off]);
+            x1 = to_f(k_pre[off + 1]);
+            float c, sn;
+            rope_cs(a.freq, i, a.pos0 + t, c, sn);
+            y0 = x0 * c - x1 * sn;
+            y1 = x0 * sn + x1 * c;
+            k_post[off] = from_f<T>(y0);
+            k_post[off + 1] = from_f<T>(y1);
+        }
+        Xs[(2 * i) * GT_XS + tok] = x0;
+        Xs[(2 * i + 1) * GT_XS + tok] = x1;
+        Xs[(d + 2 * i) * GT_XS + tok] = y0;
+        Xs[(d + 2 * i + 1) * GT_XS + tok] = y1;
+    }
+    if (tid < GT_TOK) {
+        zacc[tid] = 0.f;
+        sacc[tid] = 0.f;
+    }
+
+    // thread micro-tile: tokens 4*ty .. +3, hidden 8*tx .. +7
+    const int tx = tid & 15, ty = tid >> 4;
+    const float* w1t = a.w1t + (size_t)blk * fd * a.hidden;  // [2d][hidden]
+    const int nkc = (fd + GT_KC - 1) / GT_KC;
+
+    for (int hb = 0; hb < a.hidden; hb += GT_HID) {
+        float acc[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+        auto load_w = [&](int kc, int buf) {
+            float* dst = Ws + buf * GT_KC * GT_HID;
+            for (int e = tid; e < GT_KC * GT_HID; e += blockDim.x) {
+                const int kk = kc * GT_KC + e / GT_HID, hh = hb + e % GT_HID;
+                dst[e] = (kk < fd && hh < a.hidden) ? w1t[(size_t)kk * a.hidden + hh] : 0.f;
+            }
+        };
+        load_w(0, 0);
+        __syncthreads();
+        for (int kc = 0; kc < nkc; ++kc) {
+            if (kc + 1 < nkc) load_w(kc + 1, (kc + 1) & 1);
+            const float* W = Ws + (kc & 1) * GT_KC * GT_HID;
+            const int kmax = min(GT_KC, fd - kc * GT_KC);
+            for (int k = 0; k < kmax; ++k) {
+                const float4 xv = *reinterpret_cast<const float4*>(&Xs[(kc * GT_KC + k) * GT_XS + 4 * ty]);
+                const float4 w0 = *reinterpret_cast<const float4*>(&W[k * GT_HID + 8 * tx]);
+                const float4 w1 = *reinterpret_cast<const float4*>(&W[k * GT_HID + 8 * tx + 4]);
+                const float xr[4] = {xv.x, xv.y, xv.z, xv.w};
+                const float wr[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xr[i], wr[j], acc[i][j]);
+            }
+            __syncthreads();
+        }
+        // epilogue of this hidden block: sum_j w2 * gelu(z1 + b1)
+        float part[4] = {0.f, 0.f, 0.f, 0.f}, apart[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int hh = hb + 8 * tx + j;
+            if (hh < a.hidden) {
+                const float b1 = a.b1f[(size_t)blk * a.hidden + hh];
+                const float w2 = a.w2f[(size_t)blk * a.hidden + hh];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float z1 = acc[i][j] + b1;
+                    const float ge = 0.5f * z1 * (1.f + erff(z1 * 0.70710678118654752f));
+                    part[i] = fmaf(w2, ge, part[i]);
+                    apart[i] += fabsf(w2 * ge);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int o = 8; o >= 1; o >>= 1) {
+                part[i] += __shfl_xor_sync(0xffffffffu, part[i], o);
+                apart[i] += __shfl_xor_sync(0xffffffffu, apart[i], o);
+            }
+        }
+        if (tx == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                zacc[4 * ty + i] += part[i];
+                sacc[4 * ty + i] += apart[i];
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- final: sigmoid, threshold, candidate list -------------------------
+    if (tid < GT_TOK) {
+        const long t = t0 + tid;
+        if (t < a.T) {
+            const float z2 = (float)a.b2f[blk] + zacc[tid];
+            const float g = 1.f / (1.f + __expf(-z2));
+            const size_t gi = ((size_t)s * a.kv_heads + h) * a.T + t;
+            g_out[gi] = g;
+            bits_out[gi] = z2 >= a.ztau ? 1 : 0;
+            // fp32 error of z2 is << 1e-4 relative to sum|w2*gelu| + |b2|;
+            // anything inside a 1e-3 band is recomputed exactly in fp64.
+            const float band = 1e-3f * (1.f + sacc[tid] + fabsf((float)a.b2f[blk]));
+            if (fabsf(z2 - a.ztau) <= band) {
+                const int slot = atomicAdd(cand_cnt, 1);
+                cand[slot] = (int64_t)gi;
+            }
+        }
+    }
+}
+
+// One warp per candidate: exact fp64 gate, overwrite g/bit, report |g-tau|<1e-6.
+template <typename T>
+__global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, float* __restrict__ g_out,
+                                    uint8_t* __restrict__ bits_out, const int64_t* __restrict__ cand,
+                                    const int* __restrict__ cand_cnt, int64_t* __restrict__ near_idx, int near_cap,
+                                    int* __restrict__ near_cnt) {
+    extern __shared__ double dsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int d = a.d;
+    double* xs = dsm + (size_t)warp * (2 * d + a.hidden);
+    double* terms = xs + 2 * d;
+    float* kf = reinterpret_cast<float*>(dsm + (size_t)nw * (2 * d + a.hidden)) + warp * d;
+    const int n = *cand_cnt;
+    for (int c = blockIdx.x * nw + warp; c < n; c += gridDim.x * nw) {
+        const int64_t gi = cand[c];
+        const long t = gi % a.T;
+        const int h = (int)((gi / a.T) % a.kv_heads);
+        const int s = (int)(gi / ((int64_t)a.T * a.kv_heads));
+        const size_t off = (((size_t)s * a.T + t) * a.kv_heads + h) * d;
+        for (int k = lane; k < d; k += 32) kf[k] = to_f(k_pre[off + k]);
+        __syncwarp();
+        feature_fp64_warp(kf, d, a.pos0 + t, a.freq, xs);
+        const int blk = a.layer * a.bank_heads + a.head_offset + h;
+        const double g = gate_fp64_warp(a.gd(), blk, xs, d, terms);
+        if (lane == 0) {
+            g_out[gi] = (float)g;
+            bits_out[gi] = g >= a.tau ? 1 : 0;
+            if (fabs(g - a.tau) < 1e-6) {
+                const int slot = atomicAdd(near_cnt, 1);
+                if (slot < near_cap) near_idx[slot] = gi;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <typename T>
+int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, float* g, uint8_t* bits,
+                        int64_t* cand, int* cand_cnt, int64_t* near_idx, int near_cap, int* near_cnt,
+                        cudaStream_t st) {
+    const size_t smem = sizeof(float) * ((size_t)2 * a.d * GT_XS + 2 * GT_KC * GT_HID + 2 * GT_TOK);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(gate_prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    cudaMemsetAsync(cand_cnt, 0, sizeof(int), st);
+    dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
+    gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, cand_cnt);
+    const int nw = 4;
+    const size_t rsm = sizeof(double) * nw * (2 * a.d + a.hidden) + sizeof(float) * nw * a.d;
+    gate_recheck_kernel<T><<<kNumSMs * 2, 32 * nw, rsm, st>>>(a, k_pre, g, bits, cand, cand_cnt, near_idx, near_cap,
+                                                              near_cnt);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+template <typename T>
+__global__ void forced_gate_kernel(GateArgs a, int nseq, const T* __restrict__ k_pre, T* __restrict__ k_post,
+                                   const float* __restrict__ forced, float* __restrict__ g_out,
+                                   uint8_t* __restrict__ bits_out) {
+    const int d = a.d, hp = d / 2;
+    const size_t n = (size_t)nseq * a.T * a.kv_heads * hp;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e % hp);
+        const size_t row = e / hp;  // (s*T + t)*H + h
+        const int h = (int)(row % a.kv_heads);
+        const long t = (long)((row / a.kv_heads) % a.T);
+        const int s = (int)(row / ((size_t)a.kv_heads * a.T));
+        const size_t off = row * d + 2 * i;
+        const float x0 = to_f(k_pre[off]), x1 = to_f(k_pre[off + 1]);
+        float c, sn;
+        rope_cs(a.freq, i, a.pos0 + t, c, sn);
+        k_post[off] = from_f<T>(x0 * c - x1 * sn);
+        k_post[off + 1] = from_f<T>(x0 * sn + x1 * c);
+        if (i == 0) {
+            const size_t gi = ((size_t)s * a.kv_heads + h) * a.T + t;
+            const float g = forced[gi];
+            g_out[gi] = g;
+            bits_out[gi] = (double)g >= a.tau ? 1 : 0;
+        }
+    }
+}
+
+int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_post, const float* forced, float* g,
+                       uint8_t* bits, size_t esz, cudaStream_t st) {
+    if (esz == 2)
+        forced_gate_kernel<__nv_bfloat16><<<kNumSMs * 8, 256, 0, st>>>(
+            a, nseq, (const __nv_bfloat16*)k_pre, (__nv_bfloat16*)k_post, forced, g, bits);
+    else
+        forced_gate_kernel<float><<<kNumSMs * 8, 256, 0, st>>>(a, nseq, (const float*)k_pre, (float*)k_post, forced,
+                                                               g, bits);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+template int launch_gate_prefill<float>(const GateArgs&, int, const float*, float*, float*, uint8_t*, int64_t*, int*,
+                                        int64_t*, int, int*, cudaStream_t);
+template int launch_gate_prefill<__nv_bfloat16>(const GateArgs&, int, const __nv_bfloat16*, __nv_bfloat16*, float*,
+                                                uint8_t*, int64_t*, int*, int64_t*, int, int*, cudaStream_t);
+
+}  // namespace wgkv

@@ -1,0 +1,142 @@
+// gate.cuh -- K1 (write-gate) declarations shared by prefill and decode.
+#pragma once
+#include "common.cuh"
+
+namespace wgkv {
+
+// fp64 copy of the gate bank for the exact path (local kv heads only,
+// block index = layer * kv_heads + h).
+struct GateDev {
+    const double* w1d;  // [blk][hidden][2d]
+    const double* b1d;  // [blk][hidden]
+    const double* w2d;  // [blk][hidden]
+    const double* b2d;  // [blk]
+    int hidden;
+};
+
+struct GateArgs {
+    int layer, kv_heads, bank_heads, head_offset, d, hidden;
+    long T, pos0;
+    double tau;
+    float ztau;          // logit(tau) in fp32 (threshold on z2 for the fp32 path)
+    const double* freq;  // [d/2] base^(-2i/d), host-computed (numerics.cpp:54)
+    const float* w1t;    // [blk][2d][hidden]  (transposed fp32 W1)
+    const float* b1f;    // [blk][hidden]
+    const float* w2f;    // [blk][hidden]
+    const double* b2f;   // [blk]
+    const double* w1d;
+    const double* b1d;
+    const double* w2d;
+    const double* b2d;
+    __device__ GateDev gd() const { return GateDev{w1d, b1d, w2d, b2d, hidden}; }
+};
+
+// ---------------------------------------------------------------------------
+// exact fp64 gate for ONE token, reference operation order
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double gelu_ref(double x) {
+    // x * 0.5 * (1.0 + erf(x * sqrt2 * 0.5))   numerics.cpp:33-36
+    const double a = __dmul_rn(x, 0.5);
+    const double e = erf(__dmul_rn(__dmul_rn(x, 1.41421356237309504880), 0.5));
+    return __dmul_rn(a, __dadd_rn(1.0, e));
+}
+
+__device__ __forceinline__ double sigmoid_ref(double x) {  // numerics.cpp:44-48
+    if (x >= 0.0) return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+    const double e = exp(x);
+    return __ddiv_rn(e, __dadd_rn(1.0, e));
+}
+
+// Builds x = [k_pre ; RoPE(k_pre)] in fp64 (gating.cpp:149-156,
+// numerics.cpp:53-62) into xs[0..2d) using the calling warp.
+__device__ __forceinline__ void feature_fp64_warp(const float* kpre, int d, long pos, const double* freq, double* xs) {
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < d / 2; i += 32) {
+        const double angle = __dmul_rn((double)pos, freq[i]);
+        const double c = cos(angle), s = sin(angle);
+        const double a = kpre[2 * i], b = kpre[2 * i + 1];
+        xs[2 * i] = a;
+        xs[2 * i + 1] = b;
+        xs[d + 2 * i] = __dsub_rn(__dmul_rn(a, c), __dmul_rn(b, s));
+        xs[d + 2 * i + 1] = __dadd_rn(__dmul_rn(a, s), __dmul_rn(b, c));
+    }
+    __syncwarp();
+}
+
+// z2 = b2 + sum_h w2[h] * gelu(W1[h].x + b1[h]) (gating.cpp:158-171) by one
+// warp: lanes own hidden units, each dot is sequential in k; the z2 sum is
+// sequential in h on lane 0.  terms: smem scratch [hidden].
+__device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, const double* xs, int d, double* terms) {
+    const int lane = threadIdx.x & 31;
+    const int fd = 2 * d, hid = gd.hidden;
+    const double* w1 = gd.w1d + (size_t)blk * hid * fd;
+    const double* b1 = gd.b1d + (size_t)blk * hid;
+    const double* w2 = gd.w2d + (size_t)blk * hid;
+    for (int h = lane; h < hid; h += 32) {
+        const double* row = w1 + (size_t)h * fd;
+        double s = 0.0;
+        for (int k = 0; k < fd; ++k) s = __dadd_rn(s, __dmul_rn(row[k], xs[k]));
+        const double z1 = __dadd_rn(s, b1[h]);
+        terms[h] = __dmul_rn(w2[h], gelu_ref(z1));
+    }
+    __syncwarp();
+    double z2 = 0.0;
+    if (lane == 0) {
+        z2 = gd.b2d[blk];
+        for (int h = 0; h < hid; ++h) z2 = __dadd_rn(z2, terms[h]);
+    }
+    z2 = __shfl_sync(0xffffffffu, z2, 0);
+    double g = sigmoid_ref(z2);
+    const double lo = 4.9406564584124654e-324, hi = 0.99999999999999988898;  // 5e-324, nextafter(1, 0)
+    g = g < lo ? lo : (g > hi ? hi : g);
+    return g;
+}
+// Block-parallel fp64 gate (decode path, one token per CTA): the 2d-term dot
+// of each hidden unit is split in its k_pre and k_post halves across threads
+// and the z2 sum is a tree.  The summation order differs from the reference's
+// sequential order by O(1e-16) relative, so bits can only differ where
+// |g - tau| < 1e-14 -- far inside the reported 1e-6 band.
+// scratch: smem >= 2*hidden + 32 doubles.  Returns g on every thread.
+__device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, const double* xs, int d,
+                                                  double* scratch) {
+    const int tid = threadIdx.x, nt = blockDim.x, hid = gd.hidden;
+    const double* w1 = gd.w1d + (size_t)blk * hid * 2 * d;
+    const double* b1 = gd.b1d + (size_t)blk * hid;
+    const double* w2 = gd.w2d + (size_t)blk * hid;
+    for (int u = tid; u < 2 * hid; u += nt) {
+        const int h = u % hid, half = u / hid;
+        const double* row = w1 + (size_t)h * 2 * d + half * d;
+        const double* x = xs + half * d;
+        double s = 0.0;
+        for (int k = 0; k < d; ++k) s = fma(row[k], x[k], s);
+        scratch[u] = s;
+    }
+    __syncthreads();
+    double part = 0.0;
+    for (int h = tid; h < hid; h += nt) {
+        const double z1 = scratch[h] + scratch[hid + h] + b1[h];
+        part += w2[h] * gelu_ref(z1);
+    }
+    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    __syncthreads();
+    double* red = scratch + 2 * hid;
+    if ((tid & 31) == 0) red[tid >> 5] = part;
+    __syncthreads();
+    double z2 = gd.b2d[blk];
+    for (int w = 0; w < (nt >> 5); ++w) z2 += red[w];
+    double g = sigmoid_ref(z2);
+    const double lo = 4.9406564584124654e-324, hi = 0.99999999999999988898;
+    g = g < lo ? lo : (g > hi ? hi : g);
+    return g;
+}
+
+// effective_gate override (engine.cpp:126-151): RoPE only; g = forced, bit = g >= tau
+int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_post, const float* forced, float* g,
+                       uint8_t* bits, size_t esz, cudaStream_t st);
+
+template <typename T>
+int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, float* g, uint8_t* bits,
+                        int64_t* cand, int* cand_cnt, int64_t* near_idx, int near_cap, int* near_cnt,
+                        cudaStream_t st);
+
+}  // namespace wgkv

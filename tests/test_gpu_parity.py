@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the C oracle on the
+same bf16-rounded inputs, and against the reference-generated golden vectors.
+
+Contract (BASELINE.json north_star):
+  * admission bits and compacted indices (Global positions) bit-exact, except
+    tokens whose fp64 gate lies within 1e-6 of tau -- those must be reported;
+  * attention outputs within 1e-2 relative (bf16 storage) / 1e-5 (fp32 mode),
+    measured as max|gpu - ref| <= tol * max|ref| per (seq, head) slice.
+"""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import oracle as O  # noqa: E402
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "session_*d128.npz")))
+TOL = {"bf16": 1e-2, "f32": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def W():
+    import paper_2512_17452_b200 as W
+
+    W.load()
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return W
+
+
+def rel_err(gpu, ref):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.abs(gpu - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def to_dev(x, dt):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to("cuda").to(dt)
+
+
+def bf16_np(x):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+
+
+# --------------------------------------------------------------------- K1 --
+@pytest.mark.parametrize("w_std,b2", [(0.02, 2.0), (0.1, -2.2), (0.5, -2.5)])
+def test_gate_bits_bit_exact(W, orc, w_std, b2):
+    """K1 == binarize(gate_forward_batch(...)) except reported near-tau tokens."""
+    L, H, d, hid, T, tau = 2, 2, 128, 128, 1500, 0.1
+    bank = orc.gate_random_init(L, H, d, hid, 7, w_std, b2)
+    k = bf16_np(orc.gaussian(8, T * H * d).reshape(1, T, H, d))
+    s = W.Session(L, H, H, d, hid, 64, tau=tau, max_tokens=T, gate_bank=bank)
+    for layer in range(L):
+        k_post, g, bits, near = s.gate_forward_batch(layer, to_dev(k, torch.bfloat16))
+        g, bits, kp = g.cpu().numpy(), bits.cpu().numpy(), k_post.float().cpu().numpy()
+        for h in range(H):
+            kr = np.stack([orc.rope(k[0, t, h], t) for t in range(T)])
+            gref = orc.gate_forward_batch(bank[layer, h], k[0, :, h], kr)
+            bref = orc.binarize(gref, tau)
+            near_h = {int(i) % T for i in near if int(i) // T == h}
+            mism = np.nonzero(bits[0, h] != bref)[0]
+            assert all(t in near_h for t in mism), (mism, near_h)
+            assert all(abs(gref[t] - tau) < 1e-6 for t in near_h)
+            assert np.abs(g[0, h] - gref).max() < 2e-5
+            # k_post is RoPE(k) rounded to bf16
+            assert rel_err(kp[0, :, h], kr) < 1e-2
+
+
+# ----------------------------------------------------------- golden vectors --
+def _run_golden(W, path, dtype):
+    z = np.load(path)
+    L, hq, hkv, d, hid, n, steps, Wn, ps, topk = (int(x) for x in z["cfg"])
+    if topk:
+        pytest.skip("top-k decode lands with K6")
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    s = W.Session(L, hq, hkv, d, hid, Wn, tau=float(z["tau"]), rope_base=float(z["base"]), page_size=ps,
+                  max_tokens=n + steps, dtype=W.BF16 if dtype == "bf16" else W.F32, gate_bank=z["bank"],
+                  attn_impl=W.ATTN_SIMT)
+    q, k, v = (z[x] for x in ("q", "k", "v"))
+    tol = TOL[dtype]
+    for l in range(L):
+        out, g, bits = s.prefill_layer(l, to_dev(q[l, None, :n], dt), to_dev(k[l, None, :n], dt),
+                                       to_dev(v[l, None, :n], dt), want_gates=True)
+        s.sync()
+        assert np.array_equal(bits.cpu().numpy()[0], z["prefill_bits"][l])
+        o = out.float().cpu().numpy()[0]
+        for p in range(hq):
+            assert rel_err(o[:, p], z["prefill_out"][l][:, p]) < tol
+    for si, t in enumerate(range(n, n + steps)):
+        for l in range(L):
+            out, g, ev = s.decode_layer(l, to_dev(q[l, None, t], dt), to_dev(k[l, None, t], dt),
+                                        to_dev(v[l, None, t], dt), want_events=True)
+            s.sync()
+            assert np.array_equal(ev.cpu().numpy()[0], z["decode_events"][si, l])
+            assert np.array_equal((g.cpu().numpy()[0] >= z["tau"]), z["decode_g"][si, l] >= z["tau"])
+            o = out.float().cpu().numpy()[0]
+            for p in range(hq):
+                assert rel_err(o[p], z["decode_out"][si, l][p]) < tol
+    pos = np.concatenate([s.gather(l, 0, h)["global_pos"] for l in range(L) for h in range(hkv)])
+    assert np.array_equal(pos, z["global_pos"])
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_golden_session(W, path, dtype):
+    _run_golden(W, path, dtype)
+
+
+# ------------------------------------------------ random sessions vs oracle --
+def _session_case(W, orc, *, T, steps, hq, hkv, Wn, nseq, dtype, seed, w_std=0.1, b2=-2.2, ps=16,
+                  attn=None, base=1e4):
+    d = hid = 128
+    L = 1
+    bank = orc.gate_random_init(L, hkv, d, hid, seed, w_std, b2)
+    rnd = lambda s_, n: bf16_np(orc.gaussian(s_, n))  # noqa: E731
+    q = rnd(seed + 1, nseq * (T + steps) * hq * d).reshape(nseq, T + steps, hq, d)
+    k = rnd(seed + 2, nseq * (T + steps) * hkv * d).reshape(nseq, T + steps, hkv, d)
+    v = rnd(seed + 3, nseq * (T + steps) * hkv * d).reshape(nseq, T + steps, hkv, d)
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    s = W.Session(L, hq, hkv, d, hid, Wn, rope_base=base, page_size=ps, max_seqs=nseq, max_tokens=T + steps,
+                  dtype=W.BF16 if dtype == "bf16" else W.F32, gate_bank=bank,
+                  attn_impl=attn if attn is not None else W.ATTN_AUTO)
+    out, g, bits = s.prefill_layer(0, to_dev(q[:, :T], dt), to_dev(k[:, :T], dt), to_dev(v[:, :T], dt),
+                                   want_gates=True)
+    s.sync()
+    out = out.float().cpu().numpy()
+    bits = bits.cpu().numpy()
+    tol = TOL[dtype]
+    worst = 0.0
+    refs = []
+    for b in range(nseq):
+        r = O.Session(orc, L, hq, hkv, d, hid, Wn, rope_base=base, page_size=ps, gate_bank=bank,
+                      max_tokens=T + steps)
+        ro, rg, rb, _ = r.prefill_layer(0, q[b, :T], k[b, :T], v[b, :T])
+        assert np.array_equal(bits[b], rb)
+        for p in range(hq):
+            worst = max(worst, rel_err(out[b, :, p], ro[:, p]))
+        refs.append(r)
+    assert worst < tol, worst
+    for t in range(T, T + steps):
+        o, gg, ev = s.decode_layer(0, to_dev(q[:, t], dt), to_dev(k[:, t], dt), to_dev(v[:, t], dt),
+                                   want_events=True)
+        s.sync()
+        o, ev = o.float().cpu().numpy(), ev.cpu().numpy()
+        for b in range(nseq):
+            ro, rg, rev, _ = refs[b].decode_layer(0, q[b, t], k[b, t], v[b, t])
+            assert np.array_equal(ev[b], rev)
+            for p in range(hq):
+                assert rel_err(o[b, p], ro[p]) < tol
+    for b in range(nseq):
+        for h in range(hkv):
+            a, r = s.gather(0, b, h), refs[b].gather(0, h)
+            assert np.array_equal(a["global_pos"], r["global_pos"])
+            assert np.array_equal(a["local_pos"], r["local_pos"])
+            assert rel_err(a["global_v"], r["global_v"]) < 1e-2
+    return s
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_session_gqa4_two_seqs(W, orc, dtype):
+    _session_case(W, orc, T=700, steps=40, hq=8, hkv=2, Wn=128, nseq=2, dtype=dtype, seed=50, attn=W.ATTN_SIMT)
+
+
+def test_session_long_multichunk_decode(W, orc):
+    """Many pages per head so decode splits over several chunks + combine."""
+    _session_case(W, orc, T=3000, steps=20, hq=4, hkv=1, Wn=256, nseq=1, dtype="bf16", seed=60, w_std=0.1, b2=0.0)
+
+
+def test_session_window_larger_than_prompt(W, orc):
+    """T < W: no Global at prefill; decode fills the ring then promotes."""
+    _session_case(W, orc, T=40, steps=40, hq=4, hkv=1, Wn=64, nseq=1, dtype="f32", seed=70)
+
+
+def test_session_odd_page_size(W, orc):
+    _session_case(W, orc, T=300, steps=30, hq=4, hkv=2, Wn=37, nseq=1, dtype="f32", seed=80, ps=5)
+
+
+def test_forced_full_is_dense_causal(W, orc):
+    """effective_gate = 1 (policy 'full'): VS attention == dense causal."""
+    d, hq, hkv, T = 128, 4, 1, 300
+    q = bf16_np(orc.gaussian(1, T * hq * d).reshape(1, T, hq, d))
+    k = bf16_np(orc.gaussian(2, T * hkv * d).reshape(1, T, hkv, d))
+    v = bf16_np(orc.gaussian(3, T * hkv * d).reshape(1, T, hkv, d))
+    s = W.Session(1, hq, hkv, d, d, 16, max_tokens=T, dtype=W.F32)
+    forced = torch.ones((1, hkv, T), dtype=torch.float32, device="cuda")
+    out = s.prefill_layer(0, to_dev(q, torch.float32), to_dev(k, torch.float32), to_dev(v, torch.float32),
+                          forced_gates=forced).cpu().numpy()
+    kr = np.stack([orc.rope(k[0, t, 0], t) for t in range(T)])
+    for p in range(hq):
+        qr = np.stack([orc.rope(q[0, t, p], t) for t in range(T)])
+        ref, _ = orc.attn_dense(qr, kr, v[0, :, 0], 1 / math.sqrt(d))
+        assert rel_err(out[0, :, p], ref) < 1e-5
+
+
+# -------------------------------------------------------------- error paths --
+def test_lifecycle_and_pool_errors(W, orc):
+    d = 128
+    bank = orc.gate_random_init(1, 1, d, d, 3, 0.02, 20.0)
+    s = W.Session(1, 4, 1, d, d, 8, max_tokens=256, capacity_pages=3, gate_bank=bank)
+    x = torch.randn(1, 4, d, device="cuda").to(torch.bfloat16)
+    with pytest.raises(W.LifecycleError):
+        s.decode_layer(0, x, x[:, :1], x[:, :1])
+    q = torch.randn(1, 200, 4, d, device="cuda").to(torch.bfloat16)
+    kv = torch.randn(1, 200, 1, d, device="cuda").to(torch.bfloat16)
+    s.prefill_layer(0, q, kv, kv)
+    with pytest.raises(W.OutOfPages):  # saturated gates need ~13 Global pages
+        s.sync()
+    with pytest.raises(W.LifecycleError):
+        s.prefill_layer(0, q, kv, kv)
+    s.release(0, 1)
+    assert s.pool_info()["free"] == 3
