@@ -199,6 +199,9 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     cudaMemcpy(pv.free_top, &top, sizeof(top), cudaMemcpyHostToDevice);
     cudaMemcpy(pv.err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
     cudaMemset(pv.state, 0, sizeof(HeadState) * (size_t)L * S * H);
+    // zeroed pages: K3/K5 may stream stale slots of a partially filled page
+    // (masked out), which must at least be finite
+    cudaMemset(pv.data, 0, (size_t)cap * 2 * ps * d * ctx->esz);
     cudaMemset(pv.lpt, 0xff, sizeof(int32_t) * (size_t)L * S * H * n_lp);
     cudaMemset(pv.gpt, 0xff, sizeof(int32_t) * (size_t)L * S * H * n_gp);
     if (cudaDeviceSynchronize() != cudaSuccess) {

@@ -1,10 +1,430 @@
-// attn_tc.cu -- K3 tcgen05 path (work in progress; selected only with
-// attn_impl = WGKV_ATTN_TCGEN05 until it is parity-green).
+// attn_tc.cu -- K3: vertical-slash prefill attention on the 5th-gen tensor
+// cores (tcgen05 + TMEM + TMA), bf16 inputs, fp32 accumulation, d = 128.
+//
+// Replaces build_vs_mask + attn_vertical_slash (attention.cpp:116-153) for
+// the Session::prefill call site (engine.cpp:222-240).  One CTA owns a
+// 128-row query tile of NT = 2 query heads of the same GQA group (they share
+// every K/V tile and every mask), and visits exactly the key set
+//   vertical : the admitted Global prefix j < i0-W+1 (all rows see it; read in
+//              place from the pages K2 filled, one TMA per page half)
+//   band     : keys [i0-W+1, i0+127] of k_post / v (TMA tiles), with per
+//              element masks only on the <= 2 edge tiles
+// (SURVEY.md App. A.9).  Warp roles, 384 threads, 1 CTA / SM:
+//   warps 0-3 / 4-7 : softmax for tile 0 / 1 (one TMEM lane = one row each):
+//                     RoPE(q) in smem, then per key tile tcgen05.ld S, mask,
+//                     online softmax (lazy rescale, threshold 2^8), P as bf16
+//                     written back into TMEM over S, O rescale in TMEM
+//   warp 8          : TMA producer (Q once, K/V double-buffered ring)
+//   warp 9          : TMEM allocator + single-thread MMA issuer (warps 10-11 idle;
+//                     warpgroup 2 runs at 40 registers, the softmax ones at 232):
+//                     S_t = Q_t K^T (SS, K-major x K-major, M=N=128, K=128)
+//                     O_t += P_t V  (TS: P from TMEM, V MN-major from smem)
+// TMEM: tile t owns O_t = cols [256t, 256t+128) and S_t/P_t = [256t+128, 256t+256).
+#include <cuda.h>
+
+#include <cstdio>
+
 #include "attn_tc.cuh"
+#include "tc.cuh"
 
 namespace wgkv {
-int launch_vs_prefill_tc(const VsArgs&, int, const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
-                         __nv_bfloat16*, cudaStream_t) {
-    return WGKV_ENOTSUP;
+
+namespace {
+
+constexpr int NT = 2;       // query heads (128-row tiles) per CTA
+constexpr int NSTAGE = 2;   // K/V ring depth
+constexpr uint32_t TILE_BYTES = 128 * 128 * 2;        // one [128][128] bf16 tile
+constexpr uint32_t SUB_BYTES = TILE_BYTES / 2;        // [128][64] SW128 sub-tile
+constexpr uint32_t OFF_Q = 0;
+constexpr uint32_t OFF_KV = NT * TILE_BYTES;
+constexpr uint32_t STAGE_BYTES = 2 * TILE_BYTES;      // K then V
+constexpr uint32_t OFF_BAR = OFF_KV + NSTAGE * STAGE_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 512 + 1024;  // + barriers/meta + alignment slack
+constexpr int NTHREADS = 320;  // 3 full warpgroups (setmaxnreg is per warpgroup)
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct Bars {
+    uint64_t q_full, q_ready;
+    uint64_t kv_full[NSTAGE], kv_empty[NSTAGE];
+    uint64_t s_full[NT], p_full[NT], o_final[NT];
+    uint32_t mask[NSTAGE][4];
+    uint32_t tmem;
+    int C;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
+
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_saddr, int kk) {
+    // K-major SW128 operand, K step kk (16 bf16 = 32 bytes); sub-tile per 64 K
+    return tc::smem_desc_sw128(tile_saddr + (uint32_t)(kk >> 2) * SUB_BYTES + (uint32_t)(kk & 3) * 32u, 16, 1024);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    vs_prefill_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                         const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tpool, VsArgs a,
+                         __nv_bfloat16* __restrict__ out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars* bar = reinterpret_cast<Bars*>(sm + OFF_BAR);
+    const uint32_t sbase = smem_u32(sm);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long i0 = (long)(gridDim.x - 1 - blockIdx.x) * 128;  // longest tiles first
+    const int p0 = blockIdx.y * NT;
+    const int s = blockIdx.z;
+    const int Hq = a.q_heads, Hkv = a.pv.kv_heads;
+    const int h = p0 / (Hq / Hkv);
+    const long T = a.T, W = a.W;
+    const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
+    const uint8_t* bits = a.bits + ((size_t)s * Hkv + h) * T;
+    const long nchunk = (T + 127) / 128;
+    const int32_t* co = a.chunk_off + ((size_t)s * Hkv + h) * (nchunk + 1);
+
+    // ---- key-set geometry (identical in every role) ----------------------
+    const long s_lo = i0 - W + 1 > 0 ? i0 - W + 1 : 0;
+    int cnt = 0;
+    {
+        const long c = s_lo / 128, rem = s_lo - c * 128;
+        cnt = __syncthreads_count(threadIdx.x < rem && bits[c * 128 + threadIdx.x] != 0);
+    }
+    if (threadIdx.x == 0) {
+        int C = s_lo > 0 ? co[s_lo / 128] + cnt : 0;
+        C = min(C, a.pv.state[hidx].global_len);  // 0 after a failed page claim
+        bar->C = C;
+        tc::mbar_init(&bar->q_full, 1);
+        tc::mbar_init(&bar->q_ready, NT * 128);
+        for (int i = 0; i < NSTAGE; ++i) {
+            tc::mbar_init(&bar->kv_full[i], 1);
+            tc::mbar_init(&bar->kv_empty[i], 1);
+        }
+        for (int t = 0; t < NT; ++t) {
+            tc::mbar_init(&bar->s_full[t], 1);
+            tc::mbar_init(&bar->p_full[t], 128);
+            tc::mbar_init(&bar->o_final[t], 1);
+        }
+        tc::fence_barrier_init();
+    }
+    if (warp == 9) tc::tmem_alloc(&bar->tmem, 512);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const int C = bar->C;
+    const uint32_t tmem = bar->tmem;
+    const long band_hi = min(i0 + 127, T - 1);
+    const int nv = (C + 127) / 128;
+    const int nb = (int)((band_hi - s_lo + 1 + 127) / 128);
+    const int nblk = nv + nb;
+    const int ps = a.pv.page_size;
+
+    if (warp == 8) {
+        // ================================ TMA producer ===========================
+        if (lane == 0) {
+            tc::tma_prefetch(&tq);
+            tc::tma_prefetch(&tk);
+            tc::tma_prefetch(&tv);
+            tc::tma_prefetch(&tpool);
+            tc::mbar_arrive_expect_tx(&bar->q_full, NT * TILE_BYTES);
+            for (int t = 0; t < NT; ++t)
+                for (int hh = 0; hh < 2; ++hh)
+                    tc::tma_load_3d(sm + OFF_Q + t * TILE_BYTES + hh * SUB_BYTES, &tq, &bar->q_full, hh * 64, p0 + t,
+                                    (int)(s * T + i0));
+        }
+        for (int j = 0; j < nblk; ++j) {
+            const int st = j & 1;
+            if (j >= NSTAGE) tc::mbar_wait(&bar->kv_empty[st], ((j - NSTAGE) >> 1) & 1);
+            const bool band = j >= nv;
+            const long kb0 = band ? s_lo + 128L * (j - nv) : 0;
+            const bool masked = band && !(kb0 + 127 <= i0 && i0 + 127 - kb0 < W);
+            if (masked) {
+                for (int w = 0; w < 4; ++w) {
+                    const long key = kb0 + 32 * w + lane;
+                    const unsigned m = __ballot_sync(0xffffffffu, key < T && bits[key] != 0);
+                    if (lane == 0) bar->mask[st][w] = m;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                uint8_t* kdst = sm + OFF_KV + st * STAGE_BYTES;
+                uint8_t* vdst = kdst + TILE_BYTES;
+                tc::mbar_arrive_expect_tx(&bar->kv_full[st], STAGE_BYTES);
+                if (!band) {
+                    const int e0 = 128 * j, last = (C - 1) / ps;
+                    const int32_t* gpt = a.pv.gpt + hidx * a.pv.n_gp;
+                    for (int pi = 0; pi < 128 / ps; ++pi) {
+                        const int lp = min(e0 / ps + pi, last);
+                        const int page = gpt[lp];
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const uint32_t o = hh * SUB_BYTES + pi * ps * 128;
+                            tc::tma_load_3d(kdst + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page);
+                            tc::tma_load_3d(vdst + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page + 1);
+                        }
+                    }
+                } else {
+                    for (int hh = 0; hh < 2; ++hh) {
+                        tc::tma_load_3d(kdst + hh * SUB_BYTES, &tk, &bar->kv_full[st], hh * 64, h, (int)(s * T + kb0));
+                        tc::tma_load_3d(vdst + hh * SUB_BYTES, &tv, &bar->kv_full[st], hh * 64, h, (int)(s * T + kb0));
+                    }
+                }
+            }
+        }
+    } else if (warp == 9) {
+        // ================================ MMA issuer =============================
+        if (lane == 0) {
+            constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
+            constexpr uint32_t idPV = tc::idesc_bf16(128, 128, false, true);
+            auto issue_S = [&](int t, int st) {
+                const uint32_t qa = sbase + OFF_Q + t * TILE_BYTES;
+                const uint32_t ka = sbase + OFF_KV + st * STAGE_BYTES;
+                const uint32_t d = tmem + 256 * t + 128;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(d, kmajor_desc(qa, kk), kmajor_desc(ka, kk), idS, kk > 0);
+            };
+            auto issue_PV = [&](int t, int st, bool acc) {
+                const uint32_t va = sbase + OFF_KV + st * STAGE_BYTES + TILE_BYTES;
+                const uint32_t d = tmem + 256 * t, pa = tmem + 256 * t + 128;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc::mma_ts(d, pa + 8 * kk, tc::smem_desc_sw128(va + kk * 2048u, SUB_BYTES, 1024), idPV,
+                               (acc || kk > 0) ? 1u : 0u);
+            };
+            tc::mbar_wait(&bar->q_ready, 0);
+            tc::mbar_wait(&bar->kv_full[0], 0);
+            tc::fence_after_sync();
+            for (int t = 0; t < NT; ++t) {
+                issue_S(t, 0);
+                tc::mma_commit(&bar->s_full[t]);
+            }
+            for (int j = 0; j < nblk; ++j) {
+                const int st = j & 1;
+                for (int t = 0; t < NT; ++t) {
+                    tc::mbar_wait(&bar->p_full[t], j & 1);
+                    tc::fence_after_sync();
+                    issue_PV(t, st, j > 0);
+                    if (j == nblk - 1) tc::mma_commit(&bar->o_final[t]);
+                    if (t == NT - 1) tc::mma_commit(&bar->kv_empty[st]);
+                    if (j + 1 < nblk) {
+                        if (t == 0) {
+                            tc::mbar_wait(&bar->kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                            tc::fence_after_sync();
+                        }
+                        issue_S(t, (j + 1) & 1);
+                        tc::mma_commit(&bar->s_full[t]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < 8) {
+        // ================================ softmax ================================
+        const int t = warp >> 2;
+        const int r = (warp & 3) * 32 + lane;  // row inside the tile == TMEM lane
+        const long i = i0 + r;
+        const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t colO = 256 * t, colS = 256 * t + 128;
+        // RoPE(q) in place (engine.cpp:229), pre-scaled by log2(e)/sqrt(d)
+        tc::mbar_wait(&bar->q_full, 0);
+        {
+            const float qs = rsqrtf(128.f) * LOG2E;
+            uint8_t* qt = sm + OFF_Q + t * TILE_BYTES;
+            for (int hh = 0; hh < 2; ++hh)
+                for (int c = 0; c < 8; ++c) {
+                    uint4* p = reinterpret_cast<uint4*>(qt + hh * SUB_BYTES + tc::sw128_off(r, c));
+                    uint4 v = *p;
+                    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float x0 = __uint_as_float(w[u] << 16), x1 = __uint_as_float(w[u] & 0xffff0000u);
+                        float cs, sn;
+                        rope_cs_fast(a.freq, hh * 32 + c * 4 + u, i, cs, sn);
+                        w[u] = tc::pack_bf16x2((x0 * cs - x1 * sn) * qs, (x0 * sn + x1 * cs) * qs);
+                    }
+                    *p = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+        }
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&bar->q_ready);
+
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nblk; ++j) {
+            tc::mbar_wait(&bar->s_full[t], j & 1);
+            tc::fence_after_sync();
+            // S row -> registers (four named 32-column chunks keep it in registers)
+            uint32_t s0[32], s1[32], s2[32], s3[32];
+            tc::tmem_ld32(trow + colS, s0);
+            tc::tmem_ld32(trow + colS + 32, s1);
+            tc::tmem_ld32(trow + colS + 64, s2);
+            tc::tmem_ld32(trow + colS + 96, s3);
+            tc::tmem_ld_wait();
+            const uint32_t NEG_INF = 0xff800000u;
+            // ---- masks -------------------------------------------------------
+            if (j < nv) {
+                const int vc = min(128, C - 128 * j);
+                if (vc < 128) {
+                    auto cut = [&](uint32_t(&x)[32], int base) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (base + e >= vc) x[e] = NEG_INF;
+                    };
+                    cut(s0, 0);
+                    cut(s1, 32);
+                    cut(s2, 64);
+                    cut(s3, 96);
+                }
+            } else {
+                const long kb0 = s_lo + 128L * (j - nv);
+                if (!(kb0 + 127 <= i0 && i0 + 127 - kb0 < W)) {
+                    tc::mbar_wait(&bar->kv_full[j & 1], (j >> 1) & 1);
+                    const long dd = i - kb0;  // key c is causal iff c <= dd; in-window iff dd - c < W
+                    auto cut = [&](uint32_t(&x)[32], int w) {
+                        const uint32_t mw = bar->mask[j & 1][w];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            const long c = 32 * w + e;
+                            const bool ok = c <= dd && ((dd - c) < W || ((mw >> e) & 1u));
+                            if (!ok) x[e] = NEG_INF;
+                        }
+                    };
+                    cut(s0, 0);
+                    cut(s1, 1);
+                    cut(s2, 2);
+                    cut(s3, 3);
+                }
+            }
+            float mx = -INFINITY;
+            auto rmax = [&](const uint32_t(&x)[32]) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(x[e]));
+            };
+            rmax(s0);
+            rmax(s1);
+            rmax(s2);
+            rmax(s3);
+            // ---- lazy rescale: only when the max grows by more than 2^8 -----
+            const bool rescale = __any_sync(0xffffffffu, mx > m + 8.f);
+            float alpha = 1.f;
+            if (rescale) {
+                const float mn = fmaxf(m, mx);
+                alpha = (m == -INFINITY) ? 0.f : ex2(m - mn);
+                l *= alpha;
+                m = mn;
+            }
+            const float mu = (m == -INFINITY) ? 0.f : m;
+            float ls = 0.f;
+            uint32_t pa[32], pb[32];
+            auto expo = [&](const uint32_t(&x)[32], uint32_t(&dst)[32], int off) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const float e0 = ex2(__uint_as_float(x[2 * e]) - mu), e1 = ex2(__uint_as_float(x[2 * e + 1]) - mu);
+                    ls += e0 + e1;
+                    dst[off + e] = tc::pack_bf16x2(e0, e1);
+                }
+            };
+            expo(s0, pa, 0);
+            expo(s1, pa, 16);
+            expo(s2, pb, 0);
+            expo(s3, pb, 16);
+            l += ls;
+            tc::tmem_st32(trow + colS, pa);
+            tc::tmem_st32(trow + colS + 32, pb);
+            // O_t is complete up to PV(j-1) (s_full(j) was committed after it);
+            // PV(j) waits for p_full below, so the rescale lands in between
+            if (rescale && j > 0) {
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t o[32];
+                    tc::tmem_ld32(trow + colO + 32 * c, o);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    tc::tmem_st32(trow + colO + 32 * c, o);
+                }
+            }
+            tc::tmem_st_wait();
+            tc::fence_before_sync();
+            tc::mbar_arrive(&bar->p_full[t]);
+        }
+        // ---- epilogue: O / l -> bf16 ------------------------------------------
+        tc::mbar_wait(&bar->o_final[t], 0);
+        tc::fence_after_sync();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow = out + (((size_t)s * T + i) * Hq + p0 + t) * 128;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tc::tmem_ld32(trow + colO + 32 * c, o);
+            tc::tmem_ld_wait();
+            if (i < T) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+                    dst[q4] = make_uint4(tc::pack_bf16x2(__uint_as_float(o[8 * q4]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
+                                         tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
+                                         tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
+                                         tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 9) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc(tmem, 512);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0, uint32_t box1, uint32_t box2) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return WGKV_ECUDA;
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+    const cuuint32_t box[3] = {box0, box1, box2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? WGKV_OK : WGKV_ECUDA;
+}
+
+int launch_vs_prefill_tc(const VsArgs& a, int nseq, const __nv_bfloat16* q, const __nv_bfloat16* k_post,
+                         const __nv_bfloat16* v, __nv_bfloat16* out, cudaStream_t st) {
+    const int d = a.pv.head_dim, ps = a.pv.page_size;
+    const int Hq = a.q_heads, Hkv = a.pv.kv_heads;
+    if (d != 128 || 128 % ps != 0 || ps < 8 || (Hq / Hkv) % NT != 0) return WGKV_ENOTSUP;
+    CUtensorMap tq, tk, tv, tp;
+    const uint64_t rows = (uint64_t)nseq * a.T;
+    int r = make_tmap_3d_bf16(&tq, q, 128, Hq, rows, 256, (uint64_t)Hq * 256, 64, 1, 128);
+    r |= make_tmap_3d_bf16(&tk, k_post, 128, Hkv, rows, 256, (uint64_t)Hkv * 256, 64, 1, 128);
+    r |= make_tmap_3d_bf16(&tv, v, 128, Hkv, rows, 256, (uint64_t)Hkv * 256, 64, 1, 128);
+    r |= make_tmap_3d_bf16(&tp, a.pv.data, 128, ps, 2 * (uint64_t)a.pv.capacity, 256, (uint64_t)ps * 256, 64, ps, 1);
+    if (r) return WGKV_ECUDA;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(vs_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.T + 127) / 128), Hq / NT, nseq);
+    vs_prefill_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tq, tk, tv, tp, a, out);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
 }  // namespace wgkv

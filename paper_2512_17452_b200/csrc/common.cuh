@@ -82,6 +82,15 @@ __device__ __forceinline__ void rope_cs(const double* __restrict__ freq, int i, 
     r = fma(-k, 2.44929359829470635445213186455000e-16, r);
     sincosf((float)r, &s, &c);
 }
+// same angle, MUFU sin/cos (|error| < 1e-6 on the reduced range): used where
+// the rotated value is stored as bf16 anyway (K3's in-smem RoPE of q)
+__device__ __forceinline__ void rope_cs_fast(const double* __restrict__ freq, int i, long pos, float& c, float& s) {
+    const double angle = (double)pos * freq[i];
+    const double k = rint(angle * 0.15915494309189533576888376337251436);
+    double r = fma(-k, 6.28318530717958623199592693708837032, angle);
+    r = fma(-k, 2.44929359829470635445213186455000e-16, r);
+    __sincosf((float)r, &s, &c);
+}
 
 // ---------------------------------------------------------------------------
 // misc

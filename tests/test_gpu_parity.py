@@ -213,3 +213,27 @@ def test_lifecycle_and_pool_errors(W, orc):
         s.prefill_layer(0, q, kv, kv)
     s.release(0, 1)
     assert s.pool_info()["free"] == 3
+
+
+# ------------------------------------------------ tcgen05 prefill (K3 fast) --
+@pytest.mark.parametrize("T,Wn,hq,hkv,nseq,ps", [(700, 128, 8, 2, 2, 16), (3000, 256, 4, 1, 1, 16),
+                                                  (1500, 1024, 4, 1, 1, 32), (129, 64, 4, 1, 1, 8)])
+def test_tc_prefill_vs_oracle(W, orc, T, Wn, hq, hkv, nseq, ps):
+    _session_case(W, orc, T=T, steps=4, hq=hq, hkv=hkv, Wn=Wn, nseq=nseq, dtype="bf16", seed=90 + T, ps=ps,
+                  attn=W.ATTN_TCGEN05)
+
+
+def test_tc_matches_simt_bitwise_bits_close_outputs(W, orc):
+    """Same device inputs through both K3 implementations."""
+    d, hq, hkv, T, Wn = 128, 8, 2, 2048, 512
+    bank = orc.gate_random_init(1, hkv, d, d, 5, 0.1, -2.2)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q = torch.randn(1, T, hq, d, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(1, T, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(1, T, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for impl in (W.ATTN_SIMT, W.ATTN_TCGEN05):
+        s = W.Session(1, hq, hkv, d, d, Wn, max_tokens=T, gate_bank=bank, attn_impl=impl, rope_base=5e5)
+        outs.append(s.prefill_layer(0, q, k, v).float().cpu().numpy())
+        s.sync()
+    assert rel_err(outs[1], outs[0]) < 1e-2
