@@ -1,0 +1,508 @@
+#!/usr/bin/env python3
+"""bench.py -- WG-KV hot path on B200: prefill tok/s @128K and decode tok/s/GPU.
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on):
+  Llama-3.1-8B attention stack: 32 layers, 32 Q / 8 KV heads, d = 128, gate
+  hidden = 128, W = 1024, tau = 0.1, page 16, RoPE base 5e5; batch 4 x 128K
+  prefill, then `decode_steps` decode steps over all layers.  Synthetic
+  N(0,1) Q/K/V (bf16) and random gate MLPs (w_std 0.02) whose b2 is calibrated
+  per (layer, kv head) to the paper's 75 % sparsity (admission a = 0.25).
+  Q/K/V come from `slots` distinct resident layer-input sets used round-robin
+  (the per-layer work is identical; 32 distinct sets would need 205 GB).
+
+One step = prefill of every layer (K1 gate -> K2 compaction -> K3 VS
+attention, plus the head-output all-gather when N > 1) followed by the decode
+steps (K4 append -> K5 split-KV attention -> combine, per layer), then the
+caches are released.  N GPUs shard the KV heads (8/N per rank, their GQA
+q heads, gate banks and caches): per-GPU work shrinks, total work is fixed
+("scaling": "strong"); the per-layer NCCL all-gather of head outputs is the
+only collective.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, compiled from the reference sources) on a bounded sample and
+extrapolates to the same workload; it runs on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # configs[2]: 128K-context prefill + decode, batch 4 (the metric's config)
+    "128k": dict(workload="llama3.1-8b attention x32 layers, 128K prefill x batch 4 + decode (BASELINE configs[2])",
+                 layers=32, q_heads=32, kv_heads=8, d=128, hidden=128, T=131072, batch=4, window=1024, admit=0.25,
+                 tau=0.1, rope_base=5e5, page=16, decode_steps=32),
+    # configs[1]: full 32-layer stack, 32K prefill, batch 1
+    "32k": dict(workload="llama3.1-8b attention x32 layers, 32K prefill x batch 1 + decode (BASELINE configs[1])",
+                layers=32, q_heads=32, kv_heads=8, d=128, hidden=128, T=32768, batch=1, window=1024, admit=0.25,
+                tau=0.1, rope_base=5e5, page=16, decode_steps=64),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return dict(hbm=p["hbm_gbs"], tf=p["bf16_tflops"], tf_sus=p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                    src="measured")
+    except Exception:
+        return dict(hbm=6650.0, tf=1590.0, tf_sus=1400.0, src="fallback")
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(float(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2] not in ("", "[N/A]"))}
+
+
+# --------------------------------------------------------------- helpers --
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def pair_count(bits, window):
+    """vs_mask_pair_count per (seq, kv head) row of bits [..., T] (closed form, int64, on device)."""
+    import torch
+
+    T = bits.shape[-1]
+    i = torch.arange(T, device=bits.device)
+    band = torch.clamp(i + 1, max=window).sum()
+    if T <= window:
+        return (band * torch.ones(bits.shape[:-1], dtype=torch.int64, device=bits.device))
+    c = torch.cumsum(bits[..., : T - window].to(torch.int64), dim=-1)  # C(x) for x = 1..T-W
+    return band + c.sum(dim=-1)
+
+
+# ------------------------------------------------------------ reference arm --
+def cpu_reference(cfg, sample_T=8192, steps=1):
+    """Time the reference's own prefill hot path (oracle/_ref) on one layer of
+    one sequence at T = sample_T, all heads, WGKV_THREADS = host cores, and
+    extrapolate phase by phase to the full workload: gate+mask per token,
+    vertical-slash attention per permitted pair, populate per token."""
+    import numpy as np
+
+    nthreads = os.cpu_count() or 1
+    os.environ["WGKV_THREADS"] = str(nthreads)  # read once by thread_budget() (numerics.cpp:119-128)
+    import oracle as O
+
+    O.build()
+    ref = O.Ref()
+    hq, hkv, d, hid, W = cfg["q_heads"], cfg["kv_heads"], cfg["d"], cfg["hidden"], cfg["window"]
+    Ts = min(sample_T, cfg["T"])
+    bank = ref.gate_random_init(1, hkv, d, hid, 1234, 0.02, 0.0)
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((Ts, hq, d)).astype(np.float32).astype(np.float64)
+    k = rng.standard_normal((Ts, hkv, d)).astype(np.float32).astype(np.float64)
+    v = rng.standard_normal((Ts, hkv, d)).astype(np.float32).astype(np.float64)
+    # calibrate b2 so the sample admits the same fraction a as the GPU run
+    for h in range(hkv):
+        kr = np.stack([ref.rope(k[i, h], i, cfg["rope_base"]) for i in range(0, Ts, 8)])
+        g = ref.gate_forward_batch(bank[0, h], k[::8, h], kr)
+        z = np.log(g / (1 - g))
+        bank[0, h, -1] = math.log(cfg["tau"] / (1 - cfg["tau"])) - np.quantile(z, 1 - cfg["admit"])
+    secs_all, pairs = np.zeros(3), 0
+    for _ in range(steps):
+        s = O.Session(ref, 1, hq, hkv, d, hid, W, tau=cfg["tau"], rope_base=cfg["rope_base"], page_size=cfg["page"],
+                      gate_bank=bank, max_tokens=Ts)
+        secs, pairs = s.prefill_layer_timed(0, q, k, v)
+        secs_all += secs
+        del s
+    secs_all /= steps
+    # full-workload extrapolation
+    Tf, B, L, a = cfg["T"], cfg["batch"], cfg["layers"], cfg["admit"]
+    pairs_full_head = Tf * min(W, Tf) - min(W, Tf) * (min(W, Tf) - 1) / 2 + a * (Tf - W) * (Tf - W + 1) / 2
+    pairs_full = pairs_full_head * hq * B * L
+    t_full = (secs_all[0] / Ts * Tf * B * L + secs_all[1] / pairs * pairs_full + secs_all[2] / Ts * Tf * B * L)
+    tok_s = B * Tf / t_full
+    return dict(value=tok_s, unit="tok/s", cores=nthreads, kind="reference",
+                sample=(f"reference Session::prefill hot path (oracle/_ref, fp64) on 1 layer x 1 seq x {hq}q/{hkv}kv "
+                        f"heads at T={Ts} (admit {cfg['admit']}): gate {secs_all[0]:.2f}s, VS attention "
+                        f"{secs_all[1]:.2f}s for {pairs:.3g} pairs ({pairs / secs_all[1]:.3g} pairs/s), populate "
+                        f"{secs_all[2]:.3f}s; extrapolated per phase to {L} layers x {B} x {Tf} tokens "
+                        f"({pairs_full:.3g} pairs) = {t_full:.3g} s"),
+                sample_seconds=float(secs_all.sum()), pairs_per_s=pairs / secs_all[1])
+
+
+# ------------------------------------------------------------------ GPU arm --
+def run_gpu(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_17452_b200 as W
+    from paper_2512_17452_b200._lib import check
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L, Hq, Hkv, d, hid = cfg["layers"], cfg["q_heads"], cfg["kv_heads"], cfg["d"], cfg["hidden"]
+    assert Hkv % world == 0, "KV heads must divide the GPU count"
+    hkv, hq = Hkv // world, Hq // world
+    T, B, Wn, D = cfg["T"], cfg["batch"], cfg["window"], cfg["decode_steps"]
+    if args.tokens:
+        T = args.tokens
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- gate bank (fp64 host, GateBank layout), this rank's rows ------------
+    rng = np.random.default_rng(42)
+    blen = hid * 2 * d + 2 * hid + 1
+    bank = np.zeros((L, Hkv, blen))
+    bank[:, :, : hid * 2 * d] = 0.02 * rng.standard_normal((L, Hkv, hid * 2 * d))
+    bank[:, :, hid * 2 * d + hid: hid * 2 * d + 2 * hid] = 0.02 * rng.standard_normal((L, Hkv, hid))
+    sess = W.Session(L, hq, hkv, d, hid, Wn, tau=cfg["tau"], rope_base=cfg["rope_base"], page_size=cfg["page"],
+                     max_seqs=B, max_tokens=T + D, max_prefill_tokens=T, kv_head_offset=rank * hkv, device=local,
+                     gate_bank=bank)
+    # ---- resident inputs: `slots` distinct layer-input sets ------------------
+    slots = max(1, min(args.slots, L))
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+
+    def randn(*shape):
+        x = torch.empty(*shape, dtype=torch.bfloat16, device=dev)
+        flat = x.view(-1)
+        step = 1 << 28
+        for o in range(0, flat.numel(), step):
+            n = min(step, flat.numel() - o)
+            flat[o: o + n] = torch.randn(n, generator=gen, device=dev).to(torch.bfloat16)
+        return x
+
+    Q = [randn(B, T, hq, d) for _ in range(slots)]
+    K = [randn(B, T, hkv, d) for _ in range(slots)]
+    V = [randn(B, T, hkv, d) for _ in range(slots)]
+    qd = [randn(D, B, hq, d) for _ in range(slots)]
+    kd = [randn(D, B, hkv, d) for _ in range(slots)]
+    vd = [randn(D, B, hkv, d) for _ in range(slots)]
+    out = torch.empty(B, T, hq, d, dtype=torch.bfloat16, device=dev)
+    dout = torch.empty(B, hq, d, dtype=torch.bfloat16, device=dev)
+    gath = torch.empty(world, B, T, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
+    dgath = torch.empty(world, B, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
+
+    # ---- calibrate b2 per (layer, kv head) to admission a ---------------------
+    ztau = math.log(cfg["tau"] / (1 - cfg["tau"]))
+    for l in range(L):
+        _, g, _, _ = sess.gate_forward_batch(l, K[l % slots])
+        z = torch.logit(g.clamp(1e-7, 1 - 1e-7).double())  # b2 = 0 here
+        for h in range(hkv):
+            zz = z[:, h].flatten()
+            sub = zz[:: max(1, zz.numel() // (1 << 22))]
+            bank[l, rank * hkv + h, -1] = ztau - torch.quantile(sub.float(), 1 - cfg["admit"]).item()
+    sess.gate_set(bank)
+    del g, z
+
+    lib, h = sess.lib, sess.h
+    g_ws = torch.empty(B, hkv, T, dtype=torch.float32, device=dev)
+    bits_ws = torch.empty(B, hkv, T, dtype=torch.uint8, device=dev)
+    kpost = torch.empty(B, T, hkv, d, dtype=torch.bfloat16, device=dev)
+    P = lambda t: None if t is None else __import__("ctypes").c_void_p(t.data_ptr())  # noqa: E731
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    launches = {"n": 0}
+
+    def prefill_layer(l, k3_events=None, inputs=None):
+        qi, ki, vi = inputs if inputs is not None else (Q[l % slots], K[l % slots], V[l % slots])
+        check(lib.wgkv_gate_score(h, l, B, T, 0, P(ki), None, P(kpost), P(g_ws), P(bits_ws), None, 0, None), "K1")
+        check(lib.wgkv_admit_prefill(h, l, 0, B, T, P(kpost), P(vi), P(g_ws), P(bits_ws)), "K2")
+        if k3_events is not None:
+            k3_events[0].record(stream)
+        check(lib.wgkv_vs_prefill(h, l, 0, B, T, P(qi), P(kpost), P(vi), P(bits_ws), P(out)), "K3")
+        if k3_events is not None:
+            k3_events[1].record(stream)
+        launches["n"] += 5  # gate, recheck, plan, scatter, vs
+        if world > 1:
+            dist.all_gather_into_tensor(gath, out)  # rank-major head shards (C1)
+
+    def decode_all(step0=0):
+        for s_ in range(D):
+            for l in range(L):
+                sl = l % slots
+                check(lib.wgkv_decode_layer(h, l, 0, B, P(qd[sl][s_]), P(kd[sl][s_]), P(vd[sl][s_]), None, P(dout),
+                                              None, None), "decode")
+                launches["n"] += 3  # append, attention, combine
+                if world > 1:
+                    dist.all_gather_into_tensor(dgath, dout)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def one_step(record):
+        e = [ev() for _ in range(3)]
+        k3 = [(ev(), ev()) for _ in range(L)] if record else None
+        e[0].record(stream)
+        for l in range(L):
+            prefill_layer(l, k3[l] if k3 else None)
+        e[1].record(stream)
+        decode_all()
+        e[2].record(stream)
+        return e, k3
+
+    # ---- warm-up (also: pair counts and resident bytes for the roofline) ----
+    pairs_layer = []
+    resident = None
+    for wi in range(args.warmup):
+        if wi == 0:
+            for l in range(L):
+                prefill_layer(l)
+                pairs_layer.append(int(pair_count(bits_ws, Wn).sum().item()) * (hq // hkv))
+            st0 = sess.stats(0, B)
+            decode_all()
+            st1 = sess.stats(0, B)
+            resident = (st0["resident_entries"], st1["resident_entries"])
+            sess.sync()
+        else:
+            one_step(False)
+        sess.release(0, B)
+    sess.sync()
+
+    # ---- timed steps -----------------------------------------------------------
+    launches["n"] = 0
+    per = []
+    with ClockSampler(local) as clk:
+        barrier()
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            e, k3 = one_step(True)
+            sess.release(0, B)
+            launches["n"] += 1
+            per.append((e, k3))
+        barrier()
+        t_wall = time.perf_counter() - t_wall0
+    sess.sync()
+    pre_ms = [e[0].elapsed_time(e[1]) for e, _ in per]
+    dec_ms = [e[1].elapsed_time(e[2]) for e, _ in per]
+    k3_ms = [sum(a.elapsed_time(b) for a, b in k3) for _, k3 in per]
+    tot_ms = [e[0].elapsed_time(e[2]) for e, _ in per]
+    stats = torch.tensor([sum(pre_ms), sum(dec_ms), sum(k3_ms), sum(tot_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    pre_s, dec_s, k3_s, tot_s = (x / 1000.0 / args.steps for x in stats.tolist())
+
+    # ---- end to end through the public API, host buffers -----------------------
+    e2e = None
+    if not args.no_e2e:
+        hq_in = [torch.empty_like(Q[0], device="cpu").pin_memory() for _ in range(1)]
+        hk_in = torch.empty_like(K[0], device="cpu").pin_memory()
+        hv_in = torch.empty_like(V[0], device="cpu").pin_memory()
+        hq_in[0].copy_(Q[0])
+        hk_in.copy_(K[0])
+        hv_in.copy_(V[0])
+        h_out = torch.empty_like(out, device="cpu").pin_memory()
+        dq_h = torch.empty_like(qd[0], device="cpu").pin_memory()
+        dq_h.copy_(qd[0])
+        dk_h = torch.empty_like(kd[0], device="cpu").pin_memory()
+        dk_h.copy_(kd[0])
+        dv_h = torch.empty_like(vd[0], device="cpu").pin_memory()
+        dv_h.copy_(vd[0])
+        dout_h = torch.empty_like(dout, device="cpu").pin_memory()
+        bufs = [(torch.empty_like(Q[0]), torch.empty_like(K[0]), torch.empty_like(V[0])) for _ in range(2)]
+        copy = torch.cuda.Stream(dev)
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        done_out = torch.cuda.Event()
+        barrier()
+        t0 = ev()
+        t1 = ev()
+        t0.record(stream)
+        h2d = d2h = 0
+        for l in range(L):
+            b = l % 2
+            if l == 0:
+                with torch.cuda.stream(copy):
+                    for dst, src in zip(bufs[0], (hq_in[0], hk_in, hv_in)):
+                        dst.copy_(src, non_blocking=True)
+                    ready[0].record(copy)
+            if l + 1 < L:  # prefetch the next layer's inputs while this one computes
+                with torch.cuda.stream(copy):
+                    if l >= 1:
+                        copy.wait_event(free[(l + 1) % 2])
+                    for dst, src in zip(bufs[(l + 1) % 2], (hq_in[0], hk_in, hv_in)):
+                        dst.copy_(src, non_blocking=True)
+                    ready[(l + 1) % 2].record(copy)
+            stream.wait_event(ready[b])
+            if l >= 1:
+                stream.wait_event(done_out)  # out buffer drained to host
+            prefill_layer(l, inputs=bufs[b])
+            free[b].record(stream)
+            with torch.cuda.stream(copy):
+                copy.wait_stream(stream)
+                h_out.copy_(out, non_blocking=True)
+                done_out.record(copy)
+            h2d += sum(x.numel() * x.element_size() for x in bufs[b])
+            d2h += out.numel() * out.element_size()
+        stream.wait_event(done_out)
+        t_mid = ev()
+        t_mid.record(stream)
+        dq_d, dk_d, dv_d = torch.empty_like(qd[0][0]), torch.empty_like(kd[0][0]), torch.empty_like(vd[0][0])
+        for s_ in range(D):
+            for l in range(L):
+                dq_d.copy_(dq_h[s_], non_blocking=True)
+                dk_d.copy_(dk_h[s_], non_blocking=True)
+                dv_d.copy_(dv_h[s_], non_blocking=True)
+                check(lib.wgkv_decode_layer(h, l, 0, B, P(dq_d), P(dk_d), P(dv_d), None, P(dout), None, None), "dec")
+                dout_h.copy_(dout, non_blocking=True)
+                h2d += 3 * dq_d.numel() * dq_d.element_size()
+                d2h += dout.numel() * dout.element_size()
+        t1.record(stream)
+        barrier()
+        sess.release(0, B)
+        e2e_pre = t0.elapsed_time(t_mid) / 1000.0
+        e2e_dec = t_mid.elapsed_time(t1) / 1000.0
+        mx = torch.tensor([e2e_pre, e2e_dec], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        e2e_pre, e2e_dec = mx.tolist()
+        e2e = {"value": B * T / e2e_pre, "unit": "tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "decode_tok_s_per_gpu": B * D / e2e_dec / world,
+               "note": "one step through the C-ABI from pinned host buffers: per layer H2D of Q/K/V (double-buffered "
+                       "on a copy stream) and D2H of the attention output; decode H2D q/k/v + D2H out per layer"}
+
+    if world > 1:
+        dist.barrier()
+    res = dict(pre_s=pre_s, dec_s=dec_s, k3_s=k3_s, tot_s=tot_s, wall_s=t_wall, pairs_layer=pairs_layer,
+               resident=resident, clocks=clk.summary(), launches=launches["n"] // args.steps, e2e=e2e,
+               T=T, B=B, D=D, world=world, hq=hq, hkv=hkv)
+    if world > 1:
+        dist.destroy_process_group()
+    return rank, res
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="128k", choices=sorted(CONFIGS))
+    ap.add_argument("--slots", type=int, default=4, help="distinct resident layer-input sets")
+    ap.add_argument("--tokens", type=int, default=0, help="override T (diagnostics only, not a reported config)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-T", type=int, default=8192)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.tokens:
+        cfg["T"] = args.tokens
+    rank, world, _ = dist_env()
+    peaks = load_peaks()
+    base_cfg = {"workload": cfg["workload"], "batch": cfg["batch"], "prefill_tokens": cfg["T"],
+                "decode_steps": cfg["decode_steps"], "layers": cfg["layers"],
+                "heads": f"{cfg['q_heads']}q/{cfg['kv_heads']}kv", "head_dim": cfg["d"], "gate_hidden": cfg["hidden"],
+                "window": cfg["window"], "admission": cfg["admit"], "tau": cfg["tau"], "page_size": cfg["page"],
+                "parallelism": f"kv-head shard x{world}", "l2": "inputs larger than L2 (no flush)"}
+    metric = "WG-KV prefill tok/s @128K & decode tok/s/GPU, % of tensor/HBM roofline"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = max(1, min(args.steps, 2))
+        cb = cpu_reference(cfg, args.cpu_sample_T, steps)
+        line = {"metric": metric, "impl": "reference", "value": cb["value"], "unit": "tok/s", "n_gpus": args.gpus,
+                "steps": steps, "warmup": 0, "ms_per_step": 1000.0 * cb["sample_seconds"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": base_cfg,
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    rank, r = run_gpu(args, cfg)
+    if rank != 0:
+        return
+    L, d, B, T, D, world = cfg["layers"], cfg["d"], r["B"], r["T"], r["D"], r["world"]
+    pairs = sum(r["pairs_layer"])  # this rank's q heads, all layers
+    flops = 4.0 * d * pairs
+    k3_tfs = flops / r["k3_s"] / 1e12
+    # decode bytes per step (resident Global+Local K+V, bf16, each byte once per GQA group) + q/out
+    res0, res1 = r["resident"]
+    avg_res = 0.5 * (res0 + res1)
+    dec_bytes = D * (avg_res * 2 * d * 2 + 2 * B * r["hq"] * d * 2 * L)
+    dec_gbs = dec_bytes / r["dec_s"] / 1e9
+    prefill_tok_s = B * T / r["pre_s"]
+    decode_tok_s_gpu = B * D / r["dec_s"] / world
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": metric, "value": prefill_tok_s, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * r["tot_s"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": base_cfg,
+        "decode_tok_s_per_gpu": decode_tok_s_gpu,
+        "prefill_s_per_step": r["pre_s"], "decode_s_per_step": r["dec_s"],
+        "roofline": {"bound": "tensor", "kernel": "vs_prefill_tc_kernel (K3)", "achieved": k3_tfs,
+                     "peak": peaks["tf_sus"], "unit": "TFLOP/s", "frac": k3_tfs / peaks["tf_sus"],
+                     "frac_of_burst": k3_tfs / peaks["tf"], "peak_source": peaks["src"] + " bf16_tflops_sustained",
+                     "traffic": traffic, "k3_share_of_prefill": r["k3_s"] / r["pre_s"],
+                     "algorithmic_flops_per_step": flops,
+                     "note": "achieved = 4*d*sum(vs_mask_pair_count) over (seq, q head, layer) / K3 time (CUDA events)"},
+        "decode_roofline": {"bound": "hbm", "achieved": dec_gbs, "peak": peaks["hbm"], "unit": "GB/s",
+                            "frac": dec_gbs / peaks["hbm"], "frac_of_8TBps": dec_gbs / 8000.0,
+                            "bytes_per_decode_step": dec_bytes / D,
+                            "note": "resident Global+Local K+V bytes (bf16) + q/out per token-step / decode time"},
+        "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
+    }
+    if not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference(cfg, args.cpu_sample_T, 1)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the reference build needs g++ on the host
+            line["cpu_baseline"] = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"unavailable: {exc}"}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -244,6 +244,7 @@ class Ref(_Base):
     def __init__(self, path: str = REF_SO):
         super().__init__(path)
         L = self.lib
+        L.wr_session_prefill_layer_timed.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_long, _dp, _u64p]
         L.wr_session_head_state.argtypes = [C.c_void_p, C.c_int, C.c_int, _lp]
         L.wr_session_gather.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _lp, _dp, _dp, _dp, _lp, _dp]
         L.wr_session_select_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_long, _lp, _lp]
@@ -401,6 +402,15 @@ class Session:
                                                                    _ptr(fg), _ptr(out), _ptr(g), _ptr(bits, _u8p),
                                                                    C.byref(ev)), "prefill")
         return out, g, bits, ev.value
+
+    def prefill_layer_timed(self, layer, q_pre, k_pre, v):
+        """Reference backend only: (secs[gate, attention, populate], pairs)."""
+        q_pre, k_pre, v = _f64(q_pre), _f64(k_pre), _f64(v)
+        secs = np.zeros(3)
+        pairs = C.c_uint64(0)
+        _check(self.lib.wr_session_prefill_layer_timed(self.h, layer, _ptr(q_pre), _ptr(k_pre), _ptr(v),
+                                                       q_pre.shape[0], _ptr(secs), C.byref(pairs)), "prefill_timed")
+        return secs, pairs.value
 
     def decode_layer(self, layer, q_pre, k_pre, v, forced_gates=None):
         q_pre, k_pre, v = _f64(q_pre), _f64(k_pre), _f64(v)

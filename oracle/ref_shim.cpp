@@ -11,6 +11,7 @@
 //     prefill_populate, then local_write + gather + attn_ragged per decode
 //     step) timed on the host, parallel over heads with wgkv::parallel_for
 //     exactly as Session does (engine.cpp:188-257, 291-327).
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -305,6 +306,65 @@ int wr_session_decode_layer(void* sp, int layer, const double* q_pre, const doub
             std::memcpy(out + p * d, o.data(), sizeof(double) * d);
         }
         if (evals) *evals += counter.score_evals;
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+// Timed variant of wr_session_prefill_layer for the CPU baseline: the same
+// three phases Session::prefill runs per layer (engine.cpp:188-257), each
+// timed with a steady clock.  secs[0] = RoPE+gate_forward_batch+build_vs_mask
+// (parallel over kv heads), secs[1] = RoPE(q)+attn_vertical_slash (parallel
+// over q heads), secs[2] = prefill_populate (serial).  *pairs = score evals.
+int wr_session_prefill_layer_timed(void* sp, int layer, const double* q_pre, const double* k_pre, const double* v,
+                                   long t, double* secs, uint64_t* pairs) {
+    auto& s = *static_cast<RefSession*>(sp);
+    using clk = std::chrono::steady_clock;
+    try {
+        const int d = s.d, hkv = s.kv_heads, hq = s.q_heads, gsz = hq / hkv;
+        const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+        const RopeConfig rope{d, s.rope_base};
+        std::vector<Matrix> k_post(static_cast<size_t>(hkv), Matrix(t, d)), vv(static_cast<size_t>(hkv), Matrix(t, d));
+        std::vector<std::vector<double>> gates(static_cast<size_t>(hkv));
+        std::vector<VsMask> masks(static_cast<size_t>(hkv));
+        auto t0 = clk::now();
+        parallel_for(hkv, [&](long lo, long hi) {
+            for (long h = lo; h < hi; ++h) {
+                Matrix kp(t, d);
+                for (long i = 0; i < t; ++i) {
+                    std::memcpy(kp.row(i).data(), k_pre + (i * hkv + h) * d, sizeof(double) * d);
+                    std::memcpy(k_post[h].row(i).data(), kp.row(i).data(), sizeof(double) * d);
+                    apply_rope_inplace(k_post[h].row(i), i, rope);
+                    std::memcpy(vv[h].row(i).data(), v + (i * hkv + h) * d, sizeof(double) * d);
+                }
+                gates[h] = gate_forward_batch(s.bank[static_cast<size_t>(layer) * hkv + h], kp, k_post[h]);
+                masks[h] = build_vs_mask(gates[h], Threshold{s.tau}, s.window);
+            }
+        });
+        auto t1 = clk::now();
+        std::vector<OpCounter> counters(static_cast<size_t>(hq));
+        parallel_for(hq, [&](long lo, long hi) {
+            for (long p = lo; p < hi; ++p) {
+                Matrix q(t, d);
+                for (long i = 0; i < t; ++i) {
+                    std::memcpy(q.row(i).data(), q_pre + (i * hq + p) * d, sizeof(double) * d);
+                    apply_rope_inplace(q.row(i), i, rope);
+                }
+                const Matrix o = attn_vertical_slash({q, k_post[p / gsz], vv[p / gsz], scale, 0}, masks[p / gsz],
+                                                     &counters[p]);
+                (void)o;
+            }
+        });
+        auto t2 = clk::now();
+        for (int h = 0; h < hkv; ++h)
+            s.at(layer, h).prefill_populate(s.pool, k_post[h], vv[h], gates[h], Threshold{s.tau}, 0);
+        auto t3 = clk::now();
+        secs[0] = std::chrono::duration<double>(t1 - t0).count();
+        secs[1] = std::chrono::duration<double>(t2 - t1).count();
+        secs[2] = std::chrono::duration<double>(t3 - t2).count();
+        *pairs = 0;
+        for (const auto& c : counters) *pairs += c.score_evals;
         return 0;
     } catch (...) {
         return status_of(std::current_exception());

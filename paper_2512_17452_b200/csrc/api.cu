@@ -109,9 +109,11 @@ struct wgkv_ctx {
         return a;
     }
     bool use_tc() const {
-        // the tcgen05 kernel is opt-in until it is parity-green on the GPU
-        if (cfg.attn_impl != WGKV_ATTN_TCGEN05) return false;
-        return cfg.dtype == WGKV_BF16 && cfg.head_dim == 128 && 128 % cfg.page_size == 0;
+        // tcgen05 path: bf16, d = 128, pages tiling a 128-key block, GQA groups
+        // of an even size (two heads per CTA); everything else runs SIMT
+        if (cfg.attn_impl == WGKV_ATTN_SIMT) return false;
+        return cfg.dtype == WGKV_BF16 && cfg.head_dim == 128 && cfg.page_size >= 8 && 128 % cfg.page_size == 0 &&
+               (cfg.q_heads / cfg.kv_heads) % 2 == 0;
     }
 };
 
