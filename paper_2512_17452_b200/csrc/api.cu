@@ -79,6 +79,7 @@ struct wgkv_ctx {
     int* ws_cnt = nullptr;  // [0] candidates, [1] near count
     int64_t* ws_near = nullptr;
     float* ws_part = nullptr;
+    int* ws_nchunks = nullptr;
     int max_chunks = 64;
     long near_cap = 0;
     // host mirrors for lifecycle checks and grid sizing
@@ -186,6 +187,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->ws_near = dalloc<int64_t>((size_t)ctx->near_cap, o);
     const int gs = c.q_heads / c.kv_heads;
     ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
+    ctx->ws_nchunks = dalloc<int>((size_t)S * H, o);
     for (void* p : o)
         if (!p) {
             for (void* q : o) cudaFree(q);
@@ -472,8 +474,15 @@ int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q
     a.n_chunks = (int)((np + cp - 1) / cp);
     a.max_chunks = ctx->max_chunks;
     a.freq = ctx->freq;
+    a.n_pairs = nseq * c.kv_heads;
+    a.nchunks = nullptr;
     if (c.topk_budget > 0) return fail(WGKV_ENOTSUP, "topk decode not built in this revision");
-    if (c.dtype == WGKV_BF16)
+    const bool fast = c.dtype == WGKV_BF16 && c.head_dim == 128 && c.page_size == 16 &&
+                      c.q_heads / c.kv_heads <= 16 && c.attn_impl != WGKV_ATTN_SIMT;
+    if (fast)
+        st = launch_decode_attn_mma(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part, ctx->ws_nchunks,
+                                    (__nv_bfloat16*)out, ctx->stream);
+    else if (c.dtype == WGKV_BF16)
         st = launch_decode_attn_simt<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part,
                                                     (__nv_bfloat16*)out, ctx->stream);
     else

@@ -20,7 +20,12 @@ struct DecArgs {
     int n_chunks;     // chunks launched per (seq, kv head)
     int max_chunks;   // partial-buffer stride
     const double* freq;
+    int n_pairs;          // nseq * kv_heads (persistent kernel)
+    const int* nchunks;   // per (seq, kv head) chunk count written on device, or null (use n_chunks)
 };
+
+int launch_decode_attn_mma(const DecArgs& a, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
+                           __nv_bfloat16* out, cudaStream_t st);
 
 template <typename T>
 int launch_vs_prefill_simt(const VsArgs& a, int nseq, const T* q, const T* k_post, const T* v, T* out,

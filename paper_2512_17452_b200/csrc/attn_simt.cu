@@ -322,11 +322,12 @@ __global__ void decode_combine_kernel(DecArgs a, const float* __restrict__ part,
     const size_t pstride = (size_t)gs * (d + 2);
     const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
     __shared__ float M, invL;
+    const int nch = a.nchunks ? a.nchunks[bh] : a.n_chunks;
     if (threadIdx.x == 0) {
         float mx = -INFINITY;
-        for (int c = 0; c < a.n_chunks; ++c) mx = fmaxf(mx, base[(size_t)c * pstride + d]);
+        for (int c = 0; c < nch; ++c) mx = fmaxf(mx, base[(size_t)c * pstride + d]);
         float L = 0.f;
-        for (int c = 0; c < a.n_chunks; ++c) {
+        for (int c = 0; c < nch; ++c) {
             const float mc = base[(size_t)c * pstride + d];
             if (mc != -INFINITY) L += __expf(mc - mx) * base[(size_t)c * pstride + d + 1];
         }
@@ -336,7 +337,7 @@ __global__ void decode_combine_kernel(DecArgs a, const float* __restrict__ part,
     __syncthreads();
     for (int e = threadIdx.x; e < d; e += blockDim.x) {
         float acc = 0.f;
-        for (int c = 0; c < a.n_chunks; ++c) {
+        for (int c = 0; c < nch; ++c) {
             const float mc = base[(size_t)c * pstride + d];
             if (mc != -INFINITY) acc += __expf(mc - M) * base[(size_t)c * pstride + e];
         }
@@ -352,6 +353,11 @@ int launch_decode_attn_simt(const DecArgs& a, int nseq, const E* q, float* part,
     cudaFuncSetAttribute(decode_attn_simt_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     decode_attn_simt_kernel<E><<<dim3(a.n_chunks, nseq * a.pv.kv_heads), 128, smem, st>>>(a, q, part);
     decode_combine_kernel<E><<<nseq * a.q_heads, 128, 0, st>>>(a, part, out);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+int launch_decode_combine_bf16(const DecArgs& a, int nseq, const float* part, __nv_bfloat16* out, cudaStream_t st) {
+    decode_combine_kernel<__nv_bfloat16><<<nseq * a.q_heads, 128, 0, st>>>(a, part, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 

@@ -1,0 +1,303 @@
+// decode_mma.cu -- K5: memory-bound split-KV decode attention over the paged
+// Global + Local cache, read in place (no gather copy).
+//
+// Replaces HeadCache::gather + attn_ragged (kvstore.cpp:205-241,
+// attention.cpp:155-180) for Session::decode_step (engine.cpp:309-326).
+// Grid = (page chunks, seq x kv head).  Each CTA serves the whole GQA group
+// (every K/V byte is read from HBM once per group), 4 warps stream pages
+// independently through a 4-deep per-warp TMA ring (one 16-token page = K 4 KB
+// + V 4 KB, SWIZZLE_128B so ldmatrix is conflict-free), and compute with
+// mma.sync m16n8k16 (bf16 -> fp32): S = Q K^T with the group's q heads as
+// rows, P V with P re-used from the S accumulators in registers.  The CTA
+// merges its warps; decode_combine_kernel (attn_simt.cu) merges chunks.
+#include <cuda.h>
+
+#include "attn.cuh"
+#include "tc.cuh"
+
+namespace wgkv {
+
+namespace {
+
+constexpr int DW = 4;        // warps per CTA
+constexpr int DNS = 3;       // ring stages per warp (2 CTAs / SM)
+constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
+constexpr int QROW = 136;    // padded Q row (bf16 elements)
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// address of the 16-byte chunk (row, chunk 0..7) of a [rows][64] SW128 tile
+__device__ __forceinline__ uint32_t swz(uint32_t base, uint32_t row, uint32_t chunk) {
+    return base + row * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __grid_constant__ CUtensorMap tpool,
+                                                                      DecArgs a, const __nv_bfloat16* __restrict__ q,
+                                                                      float* __restrict__ part,
+                                                                      int* __restrict__ nchunks) {
+    extern __shared__ uint8_t dsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int d = 128;
+    const int ps = 16;
+    const int gs = a.q_heads / a.pv.kv_heads;
+    const int npairs = a.n_pairs;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint8_t* ring = sm;                                                                    // [DW][DNS][8 KB]
+    __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm + DW * DNS * PAGE_B);          // [16][QROW]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + DW * DNS * PAGE_B + 16 * QROW * 2);  // [DW][DNS]
+    float* red = reinterpret_cast<float*>(full + DW * DNS);                                // [DW][16][d + 2]
+    int* item_base = reinterpret_cast<int*>(red + DW * 16 * (d + 2));                      // [npairs + 1]
+    __shared__ int s_cp, s_items;
+
+    // ---- device-side split: uniform chunk size from the actual page counts --
+    if (tid == 0) {
+        long total = 0;
+        int npmax = 0;
+        for (int p = 0; p < npairs; ++p) {
+            const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
+            const int np = (st.global_len + ps - 1) / ps + (st.local_len + ps - 1) / ps;
+            total += np;
+            npmax = max(npmax, np);
+        }
+        int cp = (int)((total + gridDim.x - 1) / gridDim.x);
+        cp = max(cp, 8);
+        cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
+        s_cp = cp;
+        int acc = 0;
+        for (int p = 0; p < npairs; ++p) {
+            const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
+            const int np = (st.global_len + ps - 1) / ps + (st.local_len + ps - 1) / ps;
+            item_base[p] = acc;
+            const int nc = max(1, (np + cp - 1) / cp);
+            acc += nc;
+            if (blockIdx.x == 0) nchunks[p] = nc;
+        }
+        item_base[npairs] = acc;
+        s_items = acc;
+    }
+    if (tid < DW * DNS) tc::mbar_init(&full[tid], 1);
+    tc::fence_barrier_init();
+    __syncthreads();
+    const int cp = s_cp, nitems = s_items;
+    const float qs = rsqrtf((float)d) * 1.4426950408889634f;
+    const float LN2 = 0.6931471805599453f;
+    const uint32_t wring = smem_u32(ring) + warp * DNS * PAGE_B;
+    uint32_t kq = 0;  // pages this warp has issued / consumed so far (ring position + parity)
+
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int bh = 0;
+        while (item_base[bh + 1] <= item) ++bh;
+        const int chunk = item - item_base[bh];
+        const int s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
+        const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
+        const HeadState st = a.pv.state[hidx];
+        const long pos = st.tokens_seen - 1;
+        const int ng = (st.global_len + ps - 1) / ps;
+        const int NP = ng + (st.local_len + ps - 1) / ps;
+        const int vp0 = chunk * cp, vp1 = min(NP, vp0 + cp);
+        const size_t pstride = (size_t)gs * (d + 2);
+        float* pout = part + ((size_t)bh * a.max_chunks + chunk) * pstride;
+
+        // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d); rows >= gs are zero
+        for (int e = tid; e < 16 * (d / 2); e += blockDim.x) {
+            const int r = e / (d / 2), i = e % (d / 2);
+            float y0 = 0.f, y1 = 0.f;
+            if (r < gs) {
+                const size_t off = ((size_t)s * a.q_heads + h * gs + r) * d + 2 * i;
+                const float x0 = __bfloat162float(q[off]), x1 = __bfloat162float(q[off + 1]);
+                float c, sn;
+                rope_cs(a.freq, i, pos, c, sn);
+                y0 = (x0 * c - x1 * sn) * qs;
+                y1 = (x0 * sn + x1 * c) * qs;
+            }
+            Qs[r * QROW + 2 * i] = __float2bfloat16_rn(y0);
+            Qs[r * QROW + 2 * i + 1] = __float2bfloat16_rn(y1);
+        }
+        __syncthreads();
+
+        const int nmine = vp1 > vp0 ? (vp1 - vp0 - warp + DW - 1) / DW : 0;  // pages vp0+warp, +DW, ...
+        auto page_of = [&](int vp, int& valid) -> int {
+            if (vp < ng) {
+                valid = min(ps, st.global_len - vp * ps);
+                return a.pv.gpt[hidx * a.pv.n_gp + vp];
+            }
+            valid = min(ps, st.local_len - (vp - ng) * ps);
+            return a.pv.lpt[hidx * a.pv.n_lp + (vp - ng)];
+        };
+        auto issue = [&](int k) {  // k-th page of this warp (ring slot (kq + k) % DNS)
+            int valid;
+            int page = page_of(vp0 + warp + k * DW, valid);
+            if (page < 0) page = 0;  // failed allocation (latched ENOPAGES): stream a harmless page
+            const uint32_t slot = (kq + k) % DNS;
+            uint8_t* dst = ring + (warp * DNS + slot) * PAGE_B;
+            uint64_t* bar = &full[warp * DNS + slot];
+            tc::mbar_arrive_expect_tx(bar, PAGE_B);
+            tc::tma_load_3d(dst, &tpool, bar, 0, 0, 2 * page);
+            tc::tma_load_3d(dst + 2048, &tpool, bar, 64, 0, 2 * page);
+            tc::tma_load_3d(dst + 4096, &tpool, bar, 0, 0, 2 * page + 1);
+            tc::tma_load_3d(dst + 6144, &tpool, bar, 64, 0, 2 * page + 1);
+        };
+        if (lane == 0) {
+            tc::fence_proxy_async_smem();
+            for (int k = 0; k < min(DNS, nmine); ++k) issue(k);
+        }
+        // Q A-fragments: 8 k-steps of 16 dims (rows 0..15, only < gs nonzero)
+        uint32_t qa[8][4];
+        {
+            const uint32_t qb = smem_u32(Qs);
+            const int r = lane & 15, cb = (lane >> 4) * 8;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                ldsm_x4(qb + (uint32_t)(r * QROW + kk * 16 + cb) * 2u, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+        }
+        float o[16][4];
+#pragma unroll
+        for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+        float m = -INFINITY, l = 0.f;  // row (head) lane/4, log2 domain
+        const int t0 = (lane & 3) * 2;
+        for (int k = 0; k < nmine; ++k) {
+            int valid;
+            page_of(vp0 + warp + k * DW, valid);
+            const uint32_t slot = (kq + k) % DNS;
+            tc::mbar_wait(&full[warp * DNS + slot], ((kq + k) / DNS) & 1);
+            const uint32_t kb = wring + slot * PAGE_B, vb = kb + 4096;
+            // ---- S = Q K^T : two n8 tiles (tokens 0-7, 8-15) ------------------
+            float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                // matrices: (tok 0-7, dims lo), (tok 0-7, hi), (tok 8-15, lo), (tok 8-15, hi)
+                const int mi = lane >> 3, rr = lane & 7;
+                const uint32_t tok = (mi >> 1) * 8 + rr;
+                const uint32_t dch = (kk & 3) * 2 + (mi & 1);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(swz(kb + (kk >> 2) * 2048u, tok, dch), b0, b1, b2, b3);
+                mma16816(sc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
+                mma16816(sc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+            }
+            if (valid < 16) {  // partial page: token = nt*8 + t0 + e
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (nt * 8 + t0 + e >= valid) sc[nt][e] = -INFINITY;
+            }
+            float mx = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float mn = fmaxf(m, mx);
+            const float alpha = (m == -INFINITY) ? 0.f : ex2f(m - mn);
+            const float p00 = ex2f(sc[0][0] - mn), p01 = ex2f(sc[0][1] - mn);
+            const float p10 = ex2f(sc[1][0] - mn), p11 = ex2f(sc[1][1] - mn);
+            float ls = p00 + p01 + p10 + p11;
+            ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+            ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+            l = l * alpha + ls;
+            m = mn;
+            const uint32_t pa0 = tc::pack_bf16x2(p00, p01), pa2 = tc::pack_bf16x2(p10, p11);
+            // ---- O += P V : 16 n8 tiles over d, one k16 step over the tokens -----
+#pragma unroll
+            for (int n2 = 0; n2 < 8; ++n2) {
+                // x4.trans: (tok 0-7, dims 16n2..+7), (tok 8-15, same), (tok 0-7, +8..15), (tok 8-15, +8..15)
+                const int mi = lane >> 3, rr = lane & 7;
+                const uint32_t tok = (mi & 1) * 8 + rr;
+                const uint32_t dim0 = n2 * 16 + (mi >> 1) * 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(swz(vb + (dim0 >> 6) * 2048u, tok, (dim0 & 63) >> 3), b0, b1, b2, b3);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    o[2 * n2][e] *= alpha;
+                    o[2 * n2 + 1][e] *= alpha;
+                }
+                mma16816(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
+                mma16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
+            }
+            __syncwarp();
+            if (lane == 0 && k + DNS < nmine) {
+                tc::fence_proxy_async_smem();
+                issue(k + DNS);
+            }
+        }
+        kq += nmine;
+        // ---- merge warps: rows h = lane/4 < gs hold (m, l, O[h][:]) -------------
+        const int hrow = lane >> 2;
+        float* rw = red + (size_t)warp * 16 * (d + 2);
+        if (hrow < gs) {
+#pragma unroll
+            for (int n = 0; n < 16; ++n) {
+                rw[hrow * (d + 2) + n * 8 + t0] = o[n][0];
+                rw[hrow * (d + 2) + n * 8 + t0 + 1] = o[n][1];
+            }
+            if ((lane & 3) == 0) {
+                rw[hrow * (d + 2) + d] = nmine > 0 ? m : -INFINITY;
+                rw[hrow * (d + 2) + d + 1] = nmine > 0 ? l : 0.f;
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < gs * d; e += blockDim.x) {
+            const int g = e / d, c = e % d;
+            float M = -INFINITY;
+            for (int w = 0; w < DW; ++w) M = fmaxf(M, red[(size_t)w * 16 * (d + 2) + g * (d + 2) + d]);
+            float acc = 0.f, L = 0.f;
+            for (int w = 0; w < DW; ++w) {
+                const float* r = red + (size_t)w * 16 * (d + 2) + g * (d + 2);
+                const float sc = r[d] == -INFINITY ? 0.f : ex2f(r[d] - M);
+                acc += sc * r[c];
+                L += sc * r[d + 1];
+            }
+            pout[g * (d + 2) + c] = acc;
+            if (c == 0) {  // partials carry m in natural-log units for decode_combine_kernel
+                pout[g * (d + 2) + d] = M == -INFINITY ? -INFINITY : M * LN2;
+                pout[g * (d + 2) + d + 1] = L;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
+                           __nv_bfloat16* out, cudaStream_t st) {
+    DecArgs a = a0;
+    const int gs = a.q_heads / a.pv.kv_heads;
+    if (a.pv.head_dim != 128 || a.pv.page_size != 16 || gs > 16) return WGKV_ENOTSUP;
+    static CUtensorMap tp;
+    static const void* tp_base = nullptr;
+    if (tp_base != a.pv.data) {
+        if (make_tmap_3d_bf16(&tp, a.pv.data, 128, 16, 2 * (uint64_t)a.pv.capacity, 256, 16 * 256, 64, 16, 1))
+            return WGKV_ECUDA;
+        tp_base = a.pv.data;
+    }
+    a.n_pairs = nseq * a.pv.kv_heads;
+    const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + (size_t)DW * 16 * (128 + 2) * 4 +
+                        4 * ((size_t)a.n_pairs + 1);
+    if (smem > 113 * 1024) return WGKV_ENOTSUP;
+    cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    decode_attn_mma_kernel<<<2 * kNumSMs, DW * 32, smem, st>>>(tp, a, q, part, nchunks);
+    a.nchunks = nchunks;
+    extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
+    return launch_decode_combine_bf16(a, nseq, part, out, st);
+}
+
+}  // namespace wgkv
