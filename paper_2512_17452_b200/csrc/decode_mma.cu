@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
     uint8_t* ring = sm;                                                                    // [DW][DNS][8 KB]
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm + DW * DNS * PAGE_B);          // [16][QROW]
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + DW * DNS * PAGE_B + 16 * QROW * 2);  // [DW][DNS]
-    float* red = reinterpret_cast<float*>(full + DW * DNS);                                // [DW][16][d + 2]
-    int* item_base = reinterpret_cast<int*>(red + DW * 16 * (d + 2));                      // [npairs + 1]
+    float* red = reinterpret_cast<float*>(ring);  // [DW][16][d + 2], aliases the idle ring at merge time
+    int* item_base = reinterpret_cast<int*>(full + DW * DNS);                              // [npairs + 1]
     __shared__ int s_cp, s_items;
 
     // ---- device-side split: uniform chunk size from the actual page counts --
@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         }
         kq += nmine;
         // ---- merge warps: rows h = lane/4 < gs hold (m, l, O[h][:]) -------------
+        __syncthreads();  // every warp is done with its ring slots (red aliases them)
         const int hrow = lane >> 2;
         float* rw = red + (size_t)warp * 16 * (d + 2);
         if (hrow < gs) {
@@ -290,8 +291,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         tp_base = a.pv.data;
     }
     a.n_pairs = nseq * a.pv.kv_heads;
-    const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + (size_t)DW * 16 * (128 + 2) * 4 +
-                        4 * ((size_t)a.n_pairs + 1);
+    const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1);
     if (smem > 113 * 1024) return WGKV_ENOTSUP;
     cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     decode_attn_mma_kernel<<<2 * kNumSMs, DW * 32, smem, st>>>(tp, a, q, part, nchunks);
