@@ -223,8 +223,9 @@ def run_gpu(args, cfg):
     vd = [randn(D, B, hkv, d) for _ in range(slots)]
     out = torch.empty(B, T, hq, d, dtype=torch.bfloat16, device=dev)
     dout = torch.empty(B, hq, d, dtype=torch.bfloat16, device=dev)
-    gath = torch.empty(world, B, T, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
-    dgath = torch.empty(world, B, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
+    # rank-major head-shard blocks (concatenated along dim 0; see sharding.gather_heads)
+    gath = torch.empty(world * B, T, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
+    dgath = torch.empty(world * B, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
 
     # ---- calibrate b2 per (layer, kv head) to admission a ---------------------
     ztau = math.log(cfg["tau"] / (1 - cfg["tau"]))

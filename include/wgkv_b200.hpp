@@ -1,0 +1,98 @@
+// wgkv_b200.hpp -- header-only C++ face of the C-ABI with the reference's
+// names, argument meaning and exception classes (namespace wgkv::b200).
+//
+// A reference user replaces, per layer, the calls Session::prefill /
+// Session::decode_step make (engine.cpp:188-257, 291-327):
+//   gate_forward_batch + binarize      -> Device::gate_forward_batch   (K1)
+//   HeadCache::prefill_populate        -> Device::prefill_populate     (K2)
+//   build_vs_mask + attn_vertical_slash-> Device::attn_vertical_slash  (K3)
+//   gate_forward + HeadCache::local_write -> Device::local_write       (K4)
+//   HeadCache::gather + attn_ragged    -> Device::attn_ragged          (K5)
+//   (select_topk_pages when topk_budget > 0)
+// or the fused per-layer bodies Device::prefill_layer / decode_layer.
+// Status codes map back to std::invalid_argument / std::runtime_error
+// ("out of pages ...") / std::logic_error like the reference throws them
+// (SURVEY.md §5).  All tensors are device pointers (see wgkv_b200.h).
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "wgkv_b200.h"
+
+namespace wgkv {
+namespace b200 {
+
+inline void throw_on(int status, const char* what) {
+    if (status == WGKV_OK) return;
+    const std::string msg = std::string(what) + ": " + wgkv_last_error();
+    switch (status) {
+        case WGKV_EINVAL: throw std::invalid_argument(msg);
+        case WGKV_ESTATE: throw std::logic_error(msg);
+        case WGKV_ENOPAGES:  // the reference's message starts with "out of pages"
+            throw std::runtime_error(std::string(wgkv_last_error()));
+        default: throw std::runtime_error(msg);
+    }
+}
+
+class Device {
+public:
+    explicit Device(const wgkv_config& cfg) { throw_on(wgkv_ctx_create(&cfg, &ctx_), "Session::Session"); }
+    ~Device() { wgkv_ctx_destroy(ctx_); }
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+
+    void set_stream(void* cuda_stream) { throw_on(wgkv_set_stream(ctx_, cuda_stream), "set_stream"); }
+    void sync() { throw_on(wgkv_sync(ctx_), "sync"); }
+    // GateBank::load (gating.cpp:107-147)
+    void load_gates(const std::string& path) { throw_on(wgkv_gate_load(ctx_, path.c_str()), "GateBank::load"); }
+    void set_gates(const double* bank, int layers, int heads) {
+        throw_on(wgkv_gate_set(ctx_, bank, layers, heads), "GateBank");
+    }
+
+    // gate_forward_batch + binarize (gating.cpp:173-190), RoPE fused
+    void gate_forward_batch(int layer, int nseq, long T, long pos0, const void* k_pre, void* k_post, float* g,
+                            uint8_t* bits) {
+        throw_on(wgkv_gate_score(ctx_, layer, nseq, T, pos0, k_pre, nullptr, k_post, g, bits, nullptr, 0, nullptr),
+                 "gate_forward_batch");
+    }
+    // HeadCache::prefill_populate (kvstore.cpp:160-203) for every kv head of the slots
+    void prefill_populate(int layer, int seq0, int nseq, long T, const void* k_post, const void* v, const float* g,
+                          const uint8_t* bits) {
+        throw_on(wgkv_admit_prefill(ctx_, layer, seq0, nseq, T, k_post, v, g, bits), "prefill_populate");
+    }
+    // build_vs_mask + attn_vertical_slash (attention.cpp:116-153); q pre-RoPE
+    void attn_vertical_slash(int layer, int seq0, int nseq, long T, const void* q, const void* k_post, const void* v,
+                             const uint8_t* bits, void* out) {
+        throw_on(wgkv_vs_prefill(ctx_, layer, seq0, nseq, T, q, k_post, v, bits, out), "attn_vertical_slash");
+    }
+    void prefill_layer(int layer, int seq0, int nseq, long T, const void* q, const void* k_pre, const void* v,
+                       void* out, const float* forced_g = nullptr, float* g = nullptr, uint8_t* bits = nullptr) {
+        throw_on(wgkv_prefill_layer(ctx_, layer, seq0, nseq, T, q, k_pre, v, forced_g, out, g, bits),
+                 "Session::prefill");
+    }
+    // gate_forward + HeadCache::local_write with lazy promotion (kvstore.cpp:122-158)
+    void local_write(int layer, int seq0, int nseq, const void* k_pre, const void* v, const float* forced_g = nullptr,
+                     float* g = nullptr, int32_t* events = nullptr) {
+        throw_on(wgkv_decode_step_kv(ctx_, layer, seq0, nseq, k_pre, v, forced_g, g, events), "local_write");
+    }
+    // HeadCache::gather + attn_ragged (kvstore.cpp:205-241, attention.cpp:155-180), in place
+    void attn_ragged(int layer, int seq0, int nseq, const void* q, void* out) {
+        throw_on(wgkv_decode_attn(ctx_, layer, seq0, nseq, q, out), "attn_ragged");
+    }
+    void decode_layer(int layer, int seq0, int nseq, const void* q, const void* k_pre, const void* v, void* out,
+                      const float* forced_g = nullptr, float* g = nullptr, int32_t* events = nullptr) {
+        throw_on(wgkv_decode_layer(ctx_, layer, seq0, nseq, q, k_pre, v, forced_g, out, g, events),
+                 "Session::decode_step");
+    }
+    // HeadCache::release (kvstore.cpp:243-251) for every head of the slots
+    void release(int seq0, int nseq) { throw_on(wgkv_release(ctx_, seq0, nseq), "release"); }
+
+    wgkv_ctx* handle() const { return ctx_; }
+
+private:
+    wgkv_ctx* ctx_ = nullptr;
+};
+
+}  // namespace b200
+}  // namespace wgkv

@@ -187,7 +187,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->ws_near = dalloc<int64_t>((size_t)ctx->near_cap, o);
     const int gs = c.q_heads / c.kv_heads;
     ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
-    ctx->ws_nchunks = dalloc<int>((size_t)S * H, o);
+    ctx->ws_nchunks = dalloc<int>((size_t)S * H + 1, o);  // + work-stealing counter
     for (void* p : o)
         if (!p) {
             for (void* q : o) cudaFree(q);

@@ -57,7 +57,8 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, uint32_t row, uint32_t ch
 __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __grid_constant__ CUtensorMap tpool,
                                                                       DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                       float* __restrict__ part,
-                                                                      int* __restrict__ nchunks) {
+                                                                      int* __restrict__ nchunks,
+                                                                      int* __restrict__ work_counter) {
     extern __shared__ uint8_t dsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     constexpr int d = 128;
@@ -82,7 +83,8 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
             total += np;
             npmax = max(npmax, np);
         }
-        int cp = (int)((total + gridDim.x - 1) / gridDim.x);
+        // ~2 items per CTA, taken dynamically (work stealing) for balance
+        int cp = (int)((total + 2 * gridDim.x - 1) / (2 * gridDim.x));
         cp = max(cp, 8);
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         s_cp = cp;
@@ -107,7 +109,12 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
     const uint32_t wring = smem_u32(ring) + warp * DNS * PAGE_B;
     uint32_t kq = 0;  // pages this warp has issued / consumed so far (ring position + parity)
 
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    __shared__ int s_item;
+    for (;;) {
+        if (tid == 0) s_item = atomicAdd(work_counter, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= nitems) break;
         int bh = 0;
         while (item_base[bh + 1] <= item) ++bh;
         const int chunk = item - item_base[bh];
@@ -294,7 +301,9 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1);
     if (smem > 113 * 1024) return WGKV_ENOTSUP;
     cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    decode_attn_mma_kernel<<<2 * kNumSMs, DW * 32, smem, st>>>(tp, a, q, part, nchunks);
+    int* counter = nchunks + a.n_pairs;  // one int past the per-pair chunk counts
+    cudaMemsetAsync(counter, 0, sizeof(int), st);
+    decode_attn_mma_kernel<<<2 * kNumSMs, DW * 32, smem, st>>>(tp, a, q, part, nchunks, counter);
     a.nchunks = nchunks;
     extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
     return launch_decode_combine_bf16(a, nseq, part, out, st);

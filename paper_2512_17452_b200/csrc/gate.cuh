@@ -99,22 +99,25 @@ __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, con
 // scratch: smem >= 2*hidden + 32 doubles.  Returns g on every thread.
 __device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, const double* xs, int d,
                                                   double* scratch) {
-    const int tid = threadIdx.x, nt = blockDim.x, hid = gd.hidden;
-    const double* w1 = gd.w1d + (size_t)blk * hid * 2 * d;
+    const int tid = threadIdx.x, nt = blockDim.x, hid = gd.hidden, lane = tid & 31, nw = nt >> 5;
+    const int fd = 2 * d;
+    const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
-    for (int u = tid; u < 2 * hid; u += nt) {
-        const int h = u % hid, half = u / hid;
-        const double* row = w1 + (size_t)h * 2 * d + half * d;
-        const double* x = xs + half * d;
+    // one warp per hidden unit at a time: coalesced W1 row reads, many loads
+    // in flight per lane, shuffle-tree reduction of the 2d products
+    for (int h = tid >> 5; h < hid; h += nw) {
+        const double* row = w1 + (size_t)h * fd;
         double s = 0.0;
-        for (int k = 0; k < d; ++k) s = fma(row[k], x[k], s);
-        scratch[u] = s;
+#pragma unroll 8
+        for (int k = lane; k < fd; k += 32) s = fma(row[k], xs[k], s);
+        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) scratch[h] = s;
     }
     __syncthreads();
     double part = 0.0;
     for (int h = tid; h < hid; h += nt) {
-        const double z1 = scratch[h] + scratch[hid + h] + b1[h];
+        const double z1 = scratch[h] + b1[h];
         part += w2[h] * gelu_ref(z1);
     }
     for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
