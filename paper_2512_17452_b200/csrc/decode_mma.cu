@@ -23,6 +23,7 @@ constexpr int DW = 4;        // warps per CTA
 constexpr int DNS = 3;       // ring stages per warp (2 CTAs / SM)
 constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
 constexpr int QROW = 136;    // padded Q row (bf16 elements)
+constexpr int PID_CAP = 2048;  // pages per work item (staged page ids)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + DW * DNS * PAGE_B + 16 * QROW * 2);  // [DW][DNS]
     float* red = reinterpret_cast<float*>(ring);  // [DW][16][d + 2], aliases the idle ring at merge time
     int* item_base = reinterpret_cast<int*>(full + DW * DNS);                              // [npairs + 1]
+    int* pids = item_base + npairs + 1;                                                    // [PID_CAP]
     __shared__ int s_cp, s_items;
 
     // ---- device-side split: uniform chunk size from the actual page counts --
@@ -87,6 +89,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         int cp = (int)((total + 2 * gridDim.x - 1) / (2 * gridDim.x));
         cp = max(cp, 8);
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
+        cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
         s_cp = cp;
         int acc = 0;
         for (int p = 0; p < npairs; ++p) {
@@ -143,16 +146,16 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
             Qs[r * QROW + 2 * i] = __float2bfloat16_rn(y0);
             Qs[r * QROW + 2 * i + 1] = __float2bfloat16_rn(y1);
         }
+        // stage this item's physical page ids (coalesced) so the TMA issue
+        // never waits on a dependent global load
+        for (int v = vp0 + tid; v < vp1; v += blockDim.x)
+            pids[v - vp0] = v < ng ? a.pv.gpt[hidx * a.pv.n_gp + v] : a.pv.lpt[hidx * a.pv.n_lp + (v - ng)];
         __syncthreads();
 
         const int nmine = vp1 > vp0 ? (vp1 - vp0 - warp + DW - 1) / DW : 0;  // pages vp0+warp, +DW, ...
         auto page_of = [&](int vp, int& valid) -> int {
-            if (vp < ng) {
-                valid = min(ps, st.global_len - vp * ps);
-                return a.pv.gpt[hidx * a.pv.n_gp + vp];
-            }
-            valid = min(ps, st.local_len - (vp - ng) * ps);
-            return a.pv.lpt[hidx * a.pv.n_lp + (vp - ng)];
+            valid = vp < ng ? min(ps, st.global_len - vp * ps) : min(ps, st.local_len - (vp - ng) * ps);
+            return pids[vp - vp0];
         };
         auto issue = [&](int k) {  // k-th page of this warp (ring slot (kq + k) % DNS)
             int valid;
@@ -298,7 +301,8 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         tp_base = a.pv.data;
     }
     a.n_pairs = nseq * a.pv.kv_heads;
-    const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1);
+    const size_t smem =
+        1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
     if (smem > 113 * 1024) return WGKV_ENOTSUP;
     cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int* counter = nchunks + a.n_pairs;  // one int past the per-pair chunk counts

@@ -1,0 +1,75 @@
+#!/usr/bin/env python3
+"""Decode micro-benchmark: time K4 (append+gate) and K5 (attention+combine)
+separately on one layer of the 128K x 4 configuration (admission a = 0.25 via
+forced gates, so the cache geometry matches the bench).  GPU only.
+    python profiles/decode_breakdown.py [--T 131072] [--batch 4] [--iters 200]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2512_17452_b200 as W  # noqa: E402
+from paper_2512_17452_b200._lib import check  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--T", type=int, default=131072)
+    ap.add_argument("--batch", type=int, default=4)
+    ap.add_argument("--iters", type=int, default=200)
+    ap.add_argument("--admit", type=float, default=0.25)
+    ap.add_argument("--impl", type=int, default=0, help="attn_impl (0 auto, 1 simt)")
+    args = ap.parse_args()
+    B, T, Hq, Hkv, d = args.batch, args.T, 32, 8, 128
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    s = W.Session(1, Hq, Hkv, d, d, 1024, rope_base=5e5, max_seqs=B, max_tokens=T + args.iters + 8,
+                  max_prefill_tokens=T, attn_impl=args.impl)
+    q = torch.randn(B, T, Hq, d, device=dev, generator=g).to(torch.bfloat16)
+    k = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    v = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    forced = (torch.rand(B, Hkv, T, device=dev, generator=g) < args.admit).float()
+    s.prefill_layer(0, q, k, v, forced_gates=forced)
+    del q, k, v
+    s.sync()
+    qd = torch.randn(B, Hq, d, device=dev, generator=g).to(torch.bfloat16)
+    kd = torch.randn(B, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    vd = torch.randn(B, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
+    fz = torch.zeros(B, Hkv, device=dev)
+    out = torch.empty_like(qd)
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    lib, h = s.lib, s.h
+    st = s.stats(0, B)
+    res_bytes = st["resident_entries"] * 2 * d * 2
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    for _ in range(5):
+        check(lib.wgkv_decode_attn(h, 0, 0, B, P(qd), P(out)))
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(args.iters):
+        check(lib.wgkv_decode_attn(h, 0, 0, B, P(qd), P(out)))
+    ev[1].record()
+    for _ in range(args.iters // 2):
+        check(lib.wgkv_decode_step_kv(h, 0, 0, B, P(kd), P(vd), P(fz), None, None))
+    ev[2].record()
+    for _ in range(args.iters // 2):
+        check(lib.wgkv_decode_step_kv(h, 0, 0, B, P(kd), P(vd), None, None, None))
+    ev[3].record()
+    torch.cuda.synchronize()
+    t_attn = ev[0].elapsed_time(ev[1]) / args.iters * 1e3
+    t_app_forced = ev[1].elapsed_time(ev[2]) / (args.iters // 2) * 1e3
+    t_app_gate = ev[2].elapsed_time(ev[3]) / (args.iters // 2) * 1e3
+    s.sync()
+    print(json.dumps({"T": T, "batch": B, "resident_entries": st["resident_entries"],
+                      "k5_attn_us": t_attn, "k5_GBps": res_bytes / t_attn / 1e3,
+                      "k4_append_forced_us": t_app_forced, "k4_append_fp64_gate_us": t_app_gate}))
+
+
+if __name__ == "__main__":
+    main()
