@@ -260,15 +260,34 @@ def run_gpu(args, cfg):
         if world > 1:
             dist.all_gather_into_tensor(gath, out)  # rank-major head shards (C1)
 
+    # One decode token-step over all layers, issued eagerly or replayed from a
+    # CUDA graph captured once (kills per-kernel launch gaps); the step's new
+    # q/k/v are copied into static buffers first, so every replay is a real step.
+    sq = [torch.empty_like(qd[i][0]) for i in range(slots)]
+    sk = [torch.empty_like(kd[i][0]) for i in range(slots)]
+    sv = [torch.empty_like(vd[i][0]) for i in range(slots)]
+
+    def decode_token_step():
+        for l in range(L):
+            sl = l % slots
+            check(lib.wgkv_decode_layer(h, l, 0, B, P(sq[sl]), P(sk[sl]), P(sv[sl]), None, P(dout), None, None),
+                  "decode")
+            if world > 1:
+                dist.all_gather_into_tensor(dgath, dout)
+
+    graph = {"g": None}
+
     def decode_all(step0=0):
         for s_ in range(D):
-            for l in range(L):
-                sl = l % slots
-                check(lib.wgkv_decode_layer(h, l, 0, B, P(qd[sl][s_]), P(kd[sl][s_]), P(vd[sl][s_]), None, P(dout),
-                                              None, None), "decode")
-                launches["n"] += 3  # append, attention, combine
-                if world > 1:
-                    dist.all_gather_into_tensor(dgath, dout)
+            for i in range(slots):
+                sq[i].copy_(qd[i][s_], non_blocking=True)
+                sk[i].copy_(kd[i][s_], non_blocking=True)
+                sv[i].copy_(vd[i][s_], non_blocking=True)
+            if graph["g"] is not None:
+                graph["g"].replay()
+            else:
+                decode_token_step()
+            launches["n"] += 3 * L  # append, attention, combine kernels (+ a counter memset node)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -296,6 +315,16 @@ def run_gpu(args, cfg):
                 prefill_layer(l)
                 pairs_layer.append(int(pair_count(bits_ws, Wn).sum().item()) * (hq // hkv))
             st0 = sess.stats(0, B)
+            if not args.no_graphs:  # capture one token-step over all layers (recorded, not executed)
+                gstream = torch.cuda.Stream(dev)
+                gstream.wait_stream(stream)
+                sess.set_stream(gstream)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=gstream):
+                    decode_token_step()
+                sess.set_stream(stream)
+                stream.wait_stream(gstream)
+                graph["g"] = g
             decode_all()
             st1 = sess.stats(0, B)
             resident = (st0["resident_entries"], st1["resident_entries"])
@@ -427,6 +456,7 @@ def main():
     ap.add_argument("--slots", type=int, default=4, help="distinct resident layer-input sets")
     ap.add_argument("--tokens", type=int, default=0, help="override T (diagnostics only, not a reported config)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="issue decode kernels eagerly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-T", type=int, default=8192)
     args = ap.parse_args()

@@ -304,7 +304,11 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     const size_t smem =
         1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
     if (smem > 113 * 1024) return WGKV_ENOTSUP;
-    cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static size_t smem_set = 0;  // host-side only; keeps graph capture free of attribute calls
+    if (smem > smem_set) {
+        cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_set = smem;
+    }
     int* counter = nchunks + a.n_pairs;  // one int past the per-pair chunk counts
     cudaMemsetAsync(counter, 0, sizeof(int), st);
     decode_attn_mma_kernel<<<2 * kNumSMs, DW * 32, smem, st>>>(tp, a, q, part, nchunks, counter);

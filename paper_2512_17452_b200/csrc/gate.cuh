@@ -104,15 +104,22 @@ __device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, co
     const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
-    // one warp per hidden unit at a time: coalesced W1 row reads, many loads
-    // in flight per lane, shuffle-tree reduction of the 2d products
-    for (int h = tid >> 5; h < hid; h += nw) {
-        const double* row = w1 + (size_t)h * fd;
-        double s = 0.0;
-#pragma unroll 8
-        for (int k = lane; k < fd; k += 32) s = fma(row[k], xs[k], s);
-        for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) scratch[h] = s;
+    // four hidden units per warp at a time: coalesced W1 row reads with
+    // 4 x (2d/32) independent loads in flight per lane, shuffle-tree reductions
+    const int G4 = 4;
+    for (int h0 = (tid >> 5) * G4; h0 < hid; h0 += nw * G4) {
+        double s[G4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = lane; k < fd; k += 32) {
+            const double x = xs[k];
+#pragma unroll
+            for (int g = 0; g < G4; ++g)
+                if (h0 + g < hid) s[g] = fma(w1[(size_t)(h0 + g) * fd + k], x, s[g]);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int g = 0; g < G4; ++g) s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
+        if (lane < G4 && h0 + lane < hid) scratch[h0 + lane] = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
     }
     __syncthreads();
     double part = 0.0;

@@ -29,8 +29,12 @@ def main():
     B, T, Hq, Hkv, d = args.batch, args.T, 32, 8, 128
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
+    import numpy as np
+
+    bank = np.zeros((1, Hkv, d * 2 * d + 2 * d + 1))
+    bank[..., : d * 2 * d] = 0.02 * np.random.default_rng(0).standard_normal((1, Hkv, d * 2 * d))
     s = W.Session(1, Hq, Hkv, d, d, 1024, rope_base=5e5, max_seqs=B, max_tokens=T + args.iters + 8,
-                  max_prefill_tokens=T, attn_impl=args.impl)
+                  max_prefill_tokens=T, attn_impl=args.impl, gate_bank=bank)
     q = torch.randn(B, T, Hq, d, device=dev, generator=g).to(torch.bfloat16)
     k = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
     v = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
