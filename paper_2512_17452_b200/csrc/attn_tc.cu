@@ -58,6 +58,22 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// 2^x on the FMA/ALU pipes (offloads the MUFU, which otherwise paces the
+// softmax): Cody-Waite split x = n + f, f in [-1/2, 1/2] via the 1.5*2^23
+// rounding trick, cubic near-minimax for 2^f (max rel. error 7.5e-5, far
+// below the bf16 rounding of P), exponent add for 2^n.  x <= -126 -> 0.
+__device__ __forceinline__ float ex2_emu(float x) {
+    const float xc = fmaxf(x, -126.f);
+    const float t = xc + 12582912.f;
+    const float f = xc - (t - 12582912.f);
+    float p = fmaf(f, 0.05517161f, 0.24261111f);
+    p = fmaf(p, f, 0.69326097f);
+    p = fmaf(p, f, 0.99992806f);
+    const int n = __float_as_int(t) - 0x4B400000;
+    const float r = __int_as_float(__float_as_int(p) + (n << 23));
+    return x < -126.f ? 0.f : r;
+}
+
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_saddr, int kk) {
     // K-major SW128 operand, K step kk (16 bf16 = 32 bytes); sub-tile per 64 K
     return tc::smem_desc_sw128(tile_saddr + (uint32_t)(kk >> 2) * SUB_BYTES + (uint32_t)(kk & 3) * 32u, 16, 1024);
@@ -320,7 +336,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             auto expo = [&](const uint32_t(&x)[32], uint32_t(&dst)[32], int off) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                    const float e0 = ex2(__uint_as_float(x[2 * e]) - mu), e1 = ex2(__uint_as_float(x[2 * e + 1]) - mu);
+                    // every 4th pair on the FMA pipe, the rest on the MUFU
+                    const float x0 = __uint_as_float(x[2 * e]) - mu, x1 = __uint_as_float(x[2 * e + 1]) - mu;
+                    const float e0 = (e & 3) == 3 ? ex2_emu(x0) : ex2(x0);
+                    const float e1 = (e & 3) == 3 ? ex2_emu(x1) : ex2(x1);
                     ls += e0 + e1;
                     dst[off + e] = tc::pack_bf16x2(e0, e1);
                 }
