@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwgkv_b200.so")
+LIB_PATH = os.environ.get("WGKV_LIB") or os.path.join(HERE, "libwgkv_b200.so")  # WGKV_LIB: A/B builds
 
 OK, EINVAL, ENOPAGES, ESTATE, ERUNTIME, ECUDA, ENOTSUP = range(7)
 BF16, F32 = 0, 1

@@ -69,6 +69,7 @@ struct wgkv_ctx {
     // gate parameters
     float *w1t = nullptr, *b1f = nullptr, *w2f = nullptr;
     double *b2f = nullptr, *w1d = nullptr, *b1d = nullptr, *w2d = nullptr, *freq = nullptr;
+    float* bandc = nullptr;  // per (layer, kv head) fp32 error-bound constant for K1's recheck band
     bool gates_set = false;
     // workspaces
     void* ws_kpost = nullptr;
@@ -107,6 +108,7 @@ struct wgkv_ctx {
         a.b1d = b1d;
         a.w2d = w2d;
         a.b2d = b2f;
+        a.bandc = bandc;
         return a;
     }
     bool use_tc() const {
@@ -171,6 +173,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->b1f = dalloc<float>(blocks * c.hidden, o);
     ctx->w2f = dalloc<float>(blocks * c.hidden, o);
     ctx->b2f = dalloc<double>(blocks, o);
+    ctx->bandc = dalloc<float>(blocks, o);
     ctx->w1d = dalloc<double>(blocks * fd * c.hidden, o);
     ctx->b1d = dalloc<double>(blocks * c.hidden, o);
     ctx->w2d = dalloc<double>(blocks * c.hidden, o);
@@ -259,6 +262,7 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
     const size_t nb = (size_t)c.layers * c.kv_heads;
     std::vector<float> w1t(nb * fd * hid), b1f(nb * hid), w2f(nb * hid);
     std::vector<double> w1d(nb * fd * hid), b1d(nb * hid), w2d(nb * hid), b2(nb);
+    std::vector<float> bandc(nb);
     for (int l = 0; l < c.layers; ++l)
         for (int h = 0; h < c.kv_heads; ++h) {
             const double* blk = bank + ((size_t)l * bank_heads + c.kv_head_offset + h) * blen;
@@ -275,6 +279,13 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
                 w2f[b * hid + u] = (float)w2d[b * hid + u];
             }
             b2[b] = blk[(size_t)hid * fd + 2 * hid];
+            double cb = 0.0;  // sum_h |w2_h| ||W1_h||_2
+            for (int u = 0; u < hid; ++u) {
+                double n2 = 0.0;
+                for (int k = 0; k < fd; ++k) n2 += blk[(size_t)u * fd + k] * blk[(size_t)u * fd + k];
+                cb += std::fabs(w2d[b * hid + u]) * std::sqrt(n2);
+            }
+            bandc[b] = (float)cb;
         }
     WGKV_CUDA_TRY(cudaMemcpy(ctx->w1t, w1t.data(), w1t.size() * 4, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->b1f, b1f.data(), b1f.size() * 4, cudaMemcpyHostToDevice));
@@ -283,6 +294,7 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
     WGKV_CUDA_TRY(cudaMemcpy(ctx->b1d, b1d.data(), b1d.size() * 8, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->w2d, w2d.data(), w2d.size() * 8, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->b2f, b2.data(), b2.size() * 8, cudaMemcpyHostToDevice));
+    WGKV_CUDA_TRY(cudaMemcpy(ctx->bandc, bandc.data(), bandc.size() * 4, cudaMemcpyHostToDevice));
     ctx->gates_set = true;
     return WGKV_OK;
 }

@@ -58,6 +58,9 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+#ifndef WGKV_EMU_EVERY
+#define WGKV_EMU_EVERY 4  // every k-th exp2 pair is emulated (0 = all on the MUFU)
+#endif
 // 2^x on the FMA/ALU pipes (offloads the MUFU, which otherwise paces the
 // softmax): Cody-Waite split x = n + f, f in [-1/2, 1/2] via the 1.5*2^23
 // rounding trick, cubic near-minimax for 2^f (max rel. error 7.5e-5, far
@@ -338,8 +341,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int e = 0; e < 16; ++e) {
                     // every 4th pair on the FMA pipe, the rest on the MUFU
                     const float x0 = __uint_as_float(x[2 * e]) - mu, x1 = __uint_as_float(x[2 * e + 1]) - mu;
-                    const float e0 = (e & 3) == 3 ? ex2_emu(x0) : ex2(x0);
-                    const float e1 = (e & 3) == 3 ? ex2_emu(x1) : ex2(x1);
+                    const bool emu = WGKV_EMU_EVERY > 0 && (e % (WGKV_EMU_EVERY > 0 ? WGKV_EMU_EVERY : 1)) ==
+                                                               WGKV_EMU_EVERY - 1;
+                    const float e0 = emu ? ex2_emu(x0) : ex2(x0);
+                    const float e1 = emu ? ex2_emu(x1) : ex2(x1);
                     ls += e0 + e1;
                     dst[off + e] = tc::pack_bf16x2(e0, e1);
                 }

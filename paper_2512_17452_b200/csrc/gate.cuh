@@ -24,6 +24,7 @@ struct GateArgs {
     const float* b1f;    // [blk][hidden]
     const float* w2f;    // [blk][hidden]
     const double* b2f;   // [blk]
+    const float* bandc;  // [blk] sum_h |w2_h| * ||W1_h||_2 (fp32 error bound constant)
     const double* w1d;
     const double* b1d;
     const double* w2d;
@@ -72,12 +73,27 @@ __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, con
     const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
-    for (int h = lane; h < hid; h += 32) {
-        const double* row = w1 + (size_t)h * fd;
-        double s = 0.0;
-        for (int k = 0; k < fd; ++k) s = __dadd_rn(s, __dmul_rn(row[k], xs[k]));
-        const double z1 = __dadd_rn(s, b1[h]);
-        terms[h] = __dmul_rn(w2[h], gelu_ref(z1));
+    // dot products: lanes stride over k (coalesced W1 rows, 4 rows in flight),
+    // shuffle-tree sums; fp64 throughout.  The summation order differs from the
+    // reference's sequential loop by O(1e-16) relative -- bits can differ only
+    // where |g - tau| < 1e-14, inside the reported 1e-6 band.
+    for (int h0 = 0; h0 < hid; h0 += 4) {
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = lane; k < fd; k += 32) {
+            const double x = xs[k];
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+                if (h0 + g < hid) s[g] = fma(w1[(size_t)(h0 + g) * fd + k], x, s[g]);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int g = 0; g < 4; ++g) s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
+        if (lane < 4 && h0 + lane < hid) {
+            const double sv = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
+            const int h = h0 + lane;
+            terms[h] = __dmul_rn(w2[h], gelu_ref(__dadd_rn(sv, b1[h])));
+        }
     }
     __syncwarp();
     double z2 = 0.0;
