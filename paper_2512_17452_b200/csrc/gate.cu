@@ -190,7 +190,7 @@ __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, flo
         __syncwarp();
         feature_fp64_warp(kf, d, a.pos0 + t, a.freq, xs);
         const int blk = a.layer * a.bank_heads + a.head_offset + h;
-        const double g = gate_fp64_warp(a.gd(), blk, xs, d, terms);
+        const double g = d == 128 ? gate_fp64_warp<256>(a.gd(), blk, xs, d, terms) : gate_fp64_warp(a.gd(), blk, xs, d, terms);
         if (lane == 0) {
             g_out[gi] = (float)g;
             bits_out[gi] = g >= a.tau ? 1 : 0;
@@ -216,9 +216,9 @@ int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, 
     cudaMemsetAsync(cand_cnt, 0, sizeof(int), st);
     dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
     gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, cand_cnt);
-    const int nw = 4;
+    const int nw = 8;
     const size_t rsm = sizeof(double) * nw * (2 * a.d + a.hidden) + sizeof(float) * nw * a.d;
-    gate_recheck_kernel<T><<<kNumSMs * 2, 32 * nw, rsm, st>>>(a, k_pre, g, bits, cand, cand_cnt, near_idx, near_cap,
+    gate_recheck_kernel<T><<<kNumSMs * 4, 32 * nw, rsm, st>>>(a, k_pre, g, bits, cand, cand_cnt, near_idx, near_cap,
                                                               near_cnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }

@@ -67,9 +67,10 @@ __device__ __forceinline__ void feature_fp64_warp(const float* kpre, int d, long
 // z2 = b2 + sum_h w2[h] * gelu(W1[h].x + b1[h]) (gating.cpp:158-171) by one
 // warp: lanes own hidden units, each dot is sequential in k; the z2 sum is
 // sequential in h on lane 0.  terms: smem scratch [hidden].
+template <int FD = 0>  // FD = 2d when known at compile time (fully unrolled loads)
 __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, const double* xs, int d, double* terms) {
     const int lane = threadIdx.x & 31;
-    const int fd = 2 * d, hid = gd.hidden;
+    const int fd = FD > 0 ? FD : 2 * d, hid = gd.hidden;
     const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
@@ -79,7 +80,9 @@ __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, con
     // where |g - tau| < 1e-14, inside the reported 1e-6 band.
     for (int h0 = 0; h0 < hid; h0 += 4) {
         double s[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = lane; k < fd; k += 32) {
+#pragma unroll
+        for (int j = 0; j < fd / 32; ++j) {  // fd % 32 == 0 (d % 32 == 0 is enforced)
+            const int k = lane + 32 * j;
             const double x = xs[k];
 #pragma unroll
             for (int g = 0; g < 4; ++g)
