@@ -58,6 +58,23 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+#ifndef WGKV_PACK_ALU
+#define WGKV_PACK_ALU 1
+#endif
+#ifndef WGKV_EXP_BF16X2
+#define WGKV_EXP_BF16X2 0
+#endif
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
+    uint32_t y;
+    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+// fp32 pair -> bf16x2 on the ALU pipe (two IADD + one PRMT) instead of F2FP,
+// which shares the XU pipe with MUFU.EX2 and made the softmax XU-bound.
+// Round-half-up on the (finite, non-negative) P values.
+__device__ __forceinline__ uint32_t pack_bf16x2_alu(float lo, float hi) {
+    return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
+}
 #ifndef WGKV_EMU_EVERY
 #define WGKV_EMU_EVERY 0  // every k-th exp2 pair is emulated (0 = all on the MUFU; measured
                           // best on B200: 1/8 -> -5 %, 1/4 -> -9 %, 1/2 -> -13 % K3 throughput)
@@ -340,14 +357,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             auto expo = [&](const uint32_t(&x)[32], uint32_t(&dst)[32], int off) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                    // every 4th pair on the FMA pipe, the rest on the MUFU
                     const float x0 = __uint_as_float(x[2 * e]) - mu, x1 = __uint_as_float(x[2 * e + 1]) - mu;
+#if WGKV_EXP_BF16X2
+                    // one packed XU op yields both P values in MMA format; the
+                    // row sum uses exactly the bf16 values the MMA consumes
+                    const uint32_t pp = ex2_bf16x2(tc::pack_bf16x2(x0, x1));
+                    ls += __uint_as_float(pp << 16) + __uint_as_float(pp & 0xffff0000u);
+                    dst[off + e] = pp;
+                    continue;
+#endif
+                    // every k-th pair on the FMA pipe, the rest on the MUFU
                     const bool emu = WGKV_EMU_EVERY > 0 && (e % (WGKV_EMU_EVERY > 0 ? WGKV_EMU_EVERY : 1)) ==
                                                                WGKV_EMU_EVERY - 1;
                     const float e0 = emu ? ex2_emu(x0) : ex2(x0);
                     const float e1 = emu ? ex2_emu(x1) : ex2(x1);
                     ls += e0 + e1;
-                    dst[off + e] = tc::pack_bf16x2(e0, e1);
+                    dst[off + e] = WGKV_PACK_ALU ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
                 }
             };
             expo(s0, pa, 0);
