@@ -172,10 +172,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     tc::tma_load_3d(sm + OFF_Q + t * TILE_BYTES + hh * SUB_BYTES, &tq, &bar->q_full, hh * 64, p0 + t,
                                     (int)(s * T + i0));
         }
+        // Global page ids of vertical blocks: lane i holds page i of a block; the
+        // next block's ids are loaded (in flight) before waiting on this one's
+        // slot, so the page-table reads never serialise the TMA issue.
+        const int ppb = 128 / ps;  // pages per 128-key block (<= 16)
+        const int last_page = C > 0 ? (C - 1) / ps : 0;
+        const int32_t* gpt = a.pv.gpt + hidx * a.pv.n_gp;
+        auto page_ids = [&](int jb) -> int {
+            return (jb < nv && lane < ppb) ? gpt[min(jb * ppb + lane, last_page)] : 0;
+        };
+        int next_ids = page_ids(0);
         for (int j = 0; j < nblk; ++j) {
             const int st = j & 1;
+            const int cur_ids = next_ids;
+            if (j + 1 < nblk) next_ids = page_ids(j + 1);
             if (j >= NSTAGE) tc::mbar_wait(&bar->kv_empty[st], ((j - NSTAGE) >> 1) & 1);
             const bool band = j >= nv;
+            int pg[16];
+#pragma unroll
+            for (int pi = 0; pi < 16; ++pi) pg[pi] = __shfl_sync(0xffffffffu, cur_ids, pi);
             const long kb0 = band ? s_lo + 128L * (j - nv) : 0;
             const bool masked = band && !(kb0 + 127 <= i0 && i0 + 127 - kb0 < W);
             if (masked) {
@@ -191,11 +206,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 uint8_t* vdst = kdst + TILE_BYTES;
                 tc::mbar_arrive_expect_tx(&bar->kv_full[st], STAGE_BYTES);
                 if (!band) {
-                    const int e0 = 128 * j, last = (C - 1) / ps;
-                    const int32_t* gpt = a.pv.gpt + hidx * a.pv.n_gp;
-                    for (int pi = 0; pi < 128 / ps; ++pi) {
-                        const int lp = min(e0 / ps + pi, last);
-                        const int page = gpt[lp];
+#pragma unroll
+                    for (int pi = 0; pi < 16; ++pi) {
+                        if (pi >= ppb) break;
+                        const int page = pg[pi];
                         for (int hh = 0; hh < 2; ++hh) {
                             const uint32_t o = hh * SUB_BYTES + pi * ps * 128;
                             tc::tma_load_3d(kdst + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page);
