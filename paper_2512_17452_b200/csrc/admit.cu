@@ -200,7 +200,8 @@ template <typename E>
 __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0, long W,
                                                              const E* __restrict__ k_pre, const E* __restrict__ v,
                                                              const float* __restrict__ forced_g,
-                                                             float* __restrict__ g_out, int32_t* __restrict__ events) {
+                                                             float* __restrict__ g_out, int32_t* __restrict__ events,
+                                                             int* __restrict__ work_counter) {
     extern __shared__ double dsh[];
     const int s = blockIdx.x / pv.kv_heads, h = blockIdx.x % pv.kv_heads;
     const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
@@ -210,36 +211,23 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
     float* kpost = reinterpret_cast<float*>(scratch + 2 * ga.hidden + 32);  // [d]
     __shared__ HeadState st;
     __shared__ int vpage, vslot, gpage, gslot, npage, nslot, event;
-    __shared__ float gval;
     if (tid == 0) st = pv.state[hidx];
     __syncthreads();
     const long pos = st.tokens_seen;
     const size_t in = ((size_t)s * pv.kv_heads + h) * d;
-    // RoPE (fp32 for the stored key, fp64 for the gate feature)
+    // RoPE of the stored key (fp32); the fp64 gate feature is built after the
+    // dependent-launch trigger below
     for (int i = tid; i < d / 2; i += blockDim.x) {
         const float x0 = to_f(k_pre[in + 2 * i]), x1 = to_f(k_pre[in + 2 * i + 1]);
         float c, sn;
         rope_cs(ga.freq, i, pos, c, sn);
         kpost[2 * i] = x0 * c - x1 * sn;
         kpost[2 * i + 1] = x0 * sn + x1 * c;
-        const double angle = (double)pos * ga.freq[i];
-        const double cd = cos(angle), sd = sin(angle);
-        xs[2 * i] = x0;
-        xs[2 * i + 1] = x1;
-        xs[d + 2 * i] = (double)x0 * cd - (double)x1 * sd;
-        xs[d + 2 * i + 1] = (double)x0 * sd + (double)x1 * cd;
     }
-    __syncthreads();
-    double g;
-    if (forced_g) {
-        g = forced_g[(size_t)s * pv.kv_heads + h];
-    } else {
-        g = gate_fp64_block(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch);
-    }
-    const uint8_t bit = g >= ga.tau ? 1 : 0;
-    // ---- routing decision (thread 0) ----------------------------------------
+    // ---- routing decision (thread 0).  Lazy promotion inspects the VICTIM's
+    // stored bit (written W steps ago), never the new token's gate -- so the new
+    // token's gate is off the critical path of this step's attention.
     if (tid == 0) {
-        gval = (float)g;
         event = 0;
         vpage = -1;
         gpage = -1;
@@ -298,36 +286,63 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
         }
     }
     __syncthreads();
-    // write the new token into the ring slot
+    // write the new token's K/V into the ring slot
     if (npage >= 0) {
         E* kd = pool + (size_t)npage * pv.page_elems() + (size_t)nslot * d;
         for (int e = tid; e < d; e += blockDim.x) {
             kd[e] = from_f<E>(kpost[e]);
             kd[e + (size_t)ps * d] = v[in + e];
         }
-        if (tid == 0) {
-            const size_t b = (size_t)npage * ps + nslot;
-            pv.gate[b] = gval;
-            pv.pos[b] = (int32_t)pos;
-            pv.adm[b] = bit;
-        }
+        if (tid == 0) pv.pos[(size_t)npage * ps + nslot] = (int32_t)pos;
     }
     if (tid == 0) {
-        st.local_ptr = (int)((st.local_ptr + 1) % W);
-        st.tokens_seen += 1;
-        pv.state[hidx] = st;
-        if (g_out) g_out[(size_t)s * pv.kv_heads + h] = gval;
+        HeadState nst = st;
+        nst.local_ptr = (int)((st.local_ptr + 1) % W);
+        nst.tokens_seen += 1;
+        pv.state[hidx] = nst;
         if (events) events[(size_t)s * pv.kv_heads + h] = event;
+        if (work_counter && blockIdx.x == 0) *work_counter = 0;  // K5's work-stealing counter
+    }
+    // everything K5 reads (pages, tables, state) is written: let the attention
+    // kernel (launched as a programmatic dependent) start now
+    __threadfence();
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    // ---- the new token's gate (gate_forward, gating.cpp:158-171), fp64 -------
+    double g;
+    if (forced_g) {
+        g = forced_g[(size_t)s * pv.kv_heads + h];
+    } else {
+        for (int i = tid; i < d / 2; i += blockDim.x) {
+            const double x0 = to_f(k_pre[in + 2 * i]), x1 = to_f(k_pre[in + 2 * i + 1]);
+            const double angle = (double)pos * ga.freq[i];
+            const double cd = cos(angle), sd = sin(angle);
+            xs[2 * i] = x0;
+            xs[2 * i + 1] = x1;
+            xs[d + 2 * i] = x0 * cd - x1 * sd;
+            xs[d + 2 * i + 1] = x0 * sd + x1 * cd;
+        }
+        __syncthreads();
+        g = gate_fp64_block(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch);
+    }
+    if (tid == 0) {
+        if (npage >= 0) {
+            const size_t b = (size_t)npage * ps + nslot;
+            pv.gate[b] = (float)g;
+            pv.adm[b] = g >= ga.tau ? 1 : 0;
+        }
+        if (g_out) g_out[(size_t)s * pv.kv_heads + h] = (float)g;
     }
 }
 
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
                          const E* k_pre, const E* v, const float* forced_g, float* g_out, int32_t* events,
-                         cudaStream_t st) {
+                         int* work_counter, cudaStream_t st) {
     const size_t smem = sizeof(double) * (2 * pv.head_dim + 2 * ga.hidden + 32) + sizeof(float) * pv.head_dim;
     decode_append_kernel<E><<<nseq * pv.kv_heads, 256, smem, st>>>(pv, ga, layer, seq0, W, k_pre, v, forced_g, g_out,
-                                                                   events);
+                                                                   events, work_counter);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -335,7 +350,7 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     template int launch_admit_prefill<E>(const PoolView&, int, int, int, long, long, const E*, const E*,          \
                                          const float*, const uint8_t*, int32_t*, cudaStream_t);                   \
     template int launch_decode_append<E>(const PoolView&, const GateArgs&, int, int, int, long, const E*, const E*, \
-                                         const float*, float*, int32_t*, cudaStream_t);
+                                         const float*, float*, int32_t*, int*, cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)
 #undef INST

@@ -12,6 +12,6 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
                          const E* k_pre, const E* v, const float* forced_g, float* g_out, int32_t* events,
-                         cudaStream_t st);
+                         int* work_counter, cudaStream_t st);
 
 }  // namespace wgkv

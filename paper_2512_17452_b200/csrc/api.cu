@@ -441,8 +441,8 @@ static int decode_check(wgkv_ctx* ctx, int layer, int seq0, int nseq) {
     return WGKV_OK;
 }
 
-int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
-                        const float* forced_g, float* g_out, int32_t* events_out) {
+static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
+                              const float* forced_g, float* g_out, int32_t* events_out, int* work_counter) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
@@ -454,16 +454,21 @@ int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void
     if (ctx->cfg.dtype == WGKV_BF16)
         st = launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
                                                  (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g,
-                                                 g_out, events_out, ctx->stream);
+                                                 g_out, events_out, work_counter, ctx->stream);
     else
         st = launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
-                                         (const float*)v, forced_g, g_out, events_out, ctx->stream);
+                                         (const float*)v, forced_g, g_out, events_out, work_counter, ctx->stream);
     if (st) return fail(st, "decode append kernel failed");
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
     return WGKV_OK;
 }
 
-int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out) {
+static bool fast_decode(const wgkv_config& c) {
+    return c.dtype == WGKV_BF16 && c.head_dim == 128 && c.page_size == 16 && c.q_heads / c.kv_heads <= 16 &&
+           c.attn_impl != WGKV_ATTN_SIMT;
+}
+
+static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out, bool fused) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
@@ -489,11 +494,9 @@ int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q
     a.n_pairs = nseq * c.kv_heads;
     a.nchunks = nullptr;
     if (c.topk_budget > 0) return fail(WGKV_ENOTSUP, "topk decode not built in this revision");
-    const bool fast = c.dtype == WGKV_BF16 && c.head_dim == 128 && c.page_size == 16 &&
-                      c.q_heads / c.kv_heads <= 16 && c.attn_impl != WGKV_ATTN_SIMT;
-    if (fast)
+    if (fast_decode(c))
         st = launch_decode_attn_mma(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part, ctx->ws_nchunks,
-                                    (__nv_bfloat16*)out, ctx->stream);
+                                    (__nv_bfloat16*)out, ctx->stream, fused);
     else if (c.dtype == WGKV_BF16)
         st = launch_decode_attn_simt<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part,
                                                     (__nv_bfloat16*)out, ctx->stream);
@@ -503,11 +506,26 @@ int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q
     return WGKV_OK;
 }
 
+int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
+                        const float* forced_g, float* g_out, int32_t* events_out) {
+    return decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, nullptr);
+}
+
+int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out) {
+    return decode_attn_impl(ctx, layer, seq0, nseq, q, out, false);
+}
+
+// K4 -> K5 -> combine chained with programmatic dependent launch: K4 publishes
+// the ring write and triggers, then computes the new token's gate while K5
+// streams the cache (the gate is only read W steps later, at promotion time).
 int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, const void* k_pre, const void* v,
                       const float* forced_g, void* out, float* g_out, int32_t* events_out) {
-    int st = wgkv_decode_step_kv(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out);
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    const bool fused = fast_decode(ctx->cfg) && ctx->cfg.topk_budget == 0;
+    int* counter = fused ? ctx->ws_nchunks + (size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads : nullptr;
+    int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, counter);
     if (st) return st;
-    return wgkv_decode_attn(ctx, layer, seq0, nseq, q, out);
+    return decode_attn_impl(ctx, layer, seq0, nseq, q, out, fused);
 }
 
 int wgkv_cache_state(wgkv_ctx* ctx, int layer, int seq, int kv_head, int64_t* lens) {

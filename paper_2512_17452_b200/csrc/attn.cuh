@@ -24,8 +24,10 @@ struct DecArgs {
     const int* nchunks;   // per (seq, kv head) chunk count written on device, or null (use n_chunks)
 };
 
+// counter_reset_by_append: K4 ran just before on the stream and zeroed the
+// work counter; K5 is then launched as its programmatic dependent (PDL)
 int launch_decode_attn_mma(const DecArgs& a, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
-                           __nv_bfloat16* out, cudaStream_t st);
+                           __nv_bfloat16* out, cudaStream_t st, bool counter_reset_by_append);
 
 template <typename T>
 int launch_vs_prefill_simt(const VsArgs& a, int nseq, const T* q, const T* k_post, const T* v, T* out,

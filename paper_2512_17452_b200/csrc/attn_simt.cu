@@ -322,6 +322,7 @@ __global__ void decode_combine_kernel(DecArgs a, const float* __restrict__ part,
     const size_t pstride = (size_t)gs * (d + 2);
     const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
     __shared__ float M, invL;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // partials of the attention kernel (PDL)
     const int nch = a.nchunks ? a.nchunks[bh] : a.n_chunks;
     if (threadIdx.x == 0) {
         float mx = -INFINITY;
@@ -357,7 +358,17 @@ int launch_decode_attn_simt(const DecArgs& a, int nseq, const E* q, float* part,
 }
 
 int launch_decode_combine_bf16(const DecArgs& a, int nseq, const float* part, __nv_bfloat16* out, cudaStream_t st) {
-    decode_combine_kernel<__nv_bfloat16><<<nseq * a.q_heads, 128, 0, st>>>(a, part, out);
+    // programmatic dependent of the attention kernel: launch latency overlaps its tail
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nseq * a.q_heads);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, decode_combine_kernel<__nv_bfloat16>, a, part, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 

@@ -67,6 +67,9 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
     const int gs = a.q_heads / a.pv.kv_heads;
     const int npairs = a.n_pairs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // launched as a programmatic dependent of K4: wait for its trigger (pages,
+    // tables and ring state of this step are then visible)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint8_t* ring = sm;                                                                    // [DW][DNS][8 KB]
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm + DW * DNS * PAGE_B);          // [16][QROW]
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + DW * DNS * PAGE_B + 16 * QROW * 2);  // [DW][DNS]
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
 }
 
 int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
-                           __nv_bfloat16* out, cudaStream_t st) {
+                           __nv_bfloat16* out, cudaStream_t st, bool counter_reset_by_append) {
     DecArgs a = a0;
     const int gs = a.q_heads / a.pv.kv_heads;
     if (a.pv.head_dim != 128 || a.pv.page_size != 16 || gs > 16) return WGKV_ENOTSUP;
@@ -309,9 +312,21 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         smem_set = smem;
     }
-    int* counter = nchunks + a.n_pairs;  // one int past the per-pair chunk counts
-    cudaMemsetAsync(counter, 0, sizeof(int), st);
-    decode_attn_mma_kernel<<<2 * kNumSMs, DW * 32, smem, st>>>(tp, a, q, part, nchunks, counter);
+    // work-stealing counter: one int past the per-(seq, kv head) chunk counts;
+    // zeroed by K4 when it precedes us (PDL), else by a memset here
+    int* counter = nchunks + (size_t)a.pv.max_seqs * a.pv.kv_heads;
+    if (!counter_reset_by_append) cudaMemsetAsync(counter, 0, sizeof(int), st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * kNumSMs);
+    cfg.blockDim = dim3(DW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = counter_reset_by_append ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, decode_attn_mma_kernel, tp, a, q, part, nchunks, counter);
     a.nchunks = nchunks;
     extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
     return launch_decode_combine_bf16(a, nseq, part, out, st);

@@ -33,7 +33,7 @@ def main():
 
     bank = np.zeros((1, Hkv, d * 2 * d + 2 * d + 1))
     bank[..., : d * 2 * d] = 0.02 * np.random.default_rng(0).standard_normal((1, Hkv, d * 2 * d))
-    s = W.Session(1, Hq, Hkv, d, d, 1024, rope_base=5e5, max_seqs=B, max_tokens=T + args.iters + 8,
+    s = W.Session(1, Hq, Hkv, d, d, 1024, rope_base=5e5, max_seqs=B, max_tokens=T + 3 * args.iters + 8,
                   max_prefill_tokens=T, attn_impl=args.impl, gate_bank=bank)
     q = torch.randn(B, T, Hq, d, device=dev, generator=g).to(torch.bfloat16)
     k = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
@@ -65,14 +65,19 @@ def main():
     for _ in range(args.iters // 2):
         check(lib.wgkv_decode_step_kv(h, 0, 0, B, P(kd), P(vd), None, None, None))
     ev[3].record()
+    for _ in range(args.iters // 2):
+        check(lib.wgkv_decode_layer(h, 0, 0, B, P(qd), P(kd), P(vd), None, P(out), None, None))
+    ev[4].record()
     torch.cuda.synchronize()
+    t_layer = ev[3].elapsed_time(ev[4]) / (args.iters // 2) * 1e3
     t_attn = ev[0].elapsed_time(ev[1]) / args.iters * 1e3
     t_app_forced = ev[1].elapsed_time(ev[2]) / (args.iters // 2) * 1e3
     t_app_gate = ev[2].elapsed_time(ev[3]) / (args.iters // 2) * 1e3
     s.sync()
     print(json.dumps({"T": T, "batch": B, "resident_entries": st["resident_entries"],
                       "k5_attn_us": t_attn, "k5_GBps": res_bytes / t_attn / 1e3,
-                      "k4_append_forced_us": t_app_forced, "k4_append_fp64_gate_us": t_app_gate}))
+                      "k4_append_forced_us": t_app_forced, "k4_append_fp64_gate_us": t_app_gate,
+                      "decode_layer_us": t_layer, "decode_layer_GBps": res_bytes / t_layer / 1e3}))
 
 
 if __name__ == "__main__":
