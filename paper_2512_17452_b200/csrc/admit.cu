@@ -197,11 +197,20 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 // K4: decode append.  One CTA (256 threads) per (seq, kv head).
 // ---------------------------------------------------------------------------
 template <typename E>
+__device__ __forceinline__ void gate_section(const PoolView& pv, const GateArgs& ga, int layer, int s, int h, long pos,
+                                             size_t in, int npage, int nslot, const E* __restrict__ k_pre,
+                                             const float* __restrict__ forced_g, float* __restrict__ g_out,
+                                             double* xs, double* scratch);
+
+// mode 0: append + gate; mode 1: append only (slot recorded for mode 2 =
+// decode_gate_kernel on a side stream).
+template <typename E>
 __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0, long W,
                                                              const E* __restrict__ k_pre, const E* __restrict__ v,
                                                              const float* __restrict__ forced_g,
                                                              float* __restrict__ g_out, int32_t* __restrict__ events,
-                                                             int* __restrict__ work_counter) {
+                                                             int* __restrict__ work_counter, int mode,
+                                                             int* __restrict__ slot_rec) {
     extern __shared__ double dsh[];
     const int s = blockIdx.x / pv.kv_heads, h = blockIdx.x % pv.kv_heads;
     const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
@@ -308,8 +317,41 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
     __threadfence();
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (mode == 1 && !forced_g) {  // the gate runs as mode 2 on a side stream
+        if (tid == 0) slot_rec[(size_t)s * pv.kv_heads + h] = npage >= 0 ? npage * ps + nslot : -1;
+        return;
+    }
+    gate_section(pv, ga, layer, s, h, pos, in, npage, nslot, k_pre, forced_g, g_out, xs, scratch);
+}
 
-    // ---- the new token's gate (gate_forward, gating.cpp:158-171), fp64 -------
+// Mode 2 of K4: the new token's gate only, for the slot mode 1 recorded.  Runs
+// concurrently with K5 (nothing reads the new slot's bit until it is the ring
+// victim W steps later).
+template <typename E>
+__global__ void __launch_bounds__(256) decode_gate_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
+                                                           const E* __restrict__ k_pre, float* __restrict__ g_out,
+                                                           const int* __restrict__ slot_rec) {
+    extern __shared__ double dsh[];
+    const int s = blockIdx.x / pv.kv_heads, h = blockIdx.x % pv.kv_heads;
+    const int d = pv.head_dim, ps = pv.page_size;
+    double* xs = dsh;
+    double* scratch = xs + 2 * d;
+    const long hidx = pv.head_index(layer, seq0 + s, h);
+    const long pos = pv.state[hidx].tokens_seen - 1;
+    const int rec = slot_rec[(size_t)s * pv.kv_heads + h];
+    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
+    gate_section(pv, ga, layer, s, h, pos, in, rec >= 0 ? rec / ps : -1, rec >= 0 ? rec % ps : 0, k_pre,
+                 (const float*)nullptr, g_out, xs, scratch);
+}
+
+// the new token's gate (gate_forward, gating.cpp:158-171), fp64, written into
+// its ring slot's metadata (whole CTA)
+template <typename E>
+__device__ __forceinline__ void gate_section(const PoolView& pv, const GateArgs& ga, int layer, int s, int h, long pos,
+                                             size_t in, int npage, int nslot, const E* __restrict__ k_pre,
+                                             const float* __restrict__ forced_g, float* __restrict__ g_out,
+                                             double* xs, double* scratch) {
+    const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
     double g;
     if (forced_g) {
         g = forced_g[(size_t)s * pv.kv_heads + h];
@@ -339,10 +381,18 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
                          const E* k_pre, const E* v, const float* forced_g, float* g_out, int32_t* events,
-                         int* work_counter, cudaStream_t st) {
+                         int* work_counter, int* slot_rec, cudaStream_t st, cudaStream_t side,
+                         cudaEvent_t ev_fork, cudaEvent_t ev_join) {
     const size_t smem = sizeof(double) * (2 * pv.head_dim + 2 * ga.hidden + 32) + sizeof(float) * pv.head_dim;
+    const bool split = side != nullptr && forced_g == nullptr;
     decode_append_kernel<E><<<nseq * pv.kv_heads, 256, smem, st>>>(pv, ga, layer, seq0, W, k_pre, v, forced_g, g_out,
-                                                                   events, work_counter);
+                                                                   events, work_counter, split ? 1 : 0, slot_rec);
+    if (split) {  // fork: the gate on the side stream, joined by the caller with ev_join
+        cudaEventRecord(ev_fork, st);
+        cudaStreamWaitEvent(side, ev_fork, 0);
+        decode_gate_kernel<E><<<nseq * pv.kv_heads, 256, smem, side>>>(pv, ga, layer, seq0, k_pre, g_out, slot_rec);
+        cudaEventRecord(ev_join, side);
+    }
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -350,7 +400,8 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     template int launch_admit_prefill<E>(const PoolView&, int, int, int, long, long, const E*, const E*,          \
                                          const float*, const uint8_t*, int32_t*, cudaStream_t);                   \
     template int launch_decode_append<E>(const PoolView&, const GateArgs&, int, int, int, long, const E*, const E*, \
-                                         const float*, float*, int32_t*, int*, cudaStream_t);
+                                         const float*, float*, int32_t*, int*, int*, cudaStream_t, cudaStream_t,  \
+                                         cudaEvent_t, cudaEvent_t);
 INST(float)
 INST(__nv_bfloat16)
 #undef INST

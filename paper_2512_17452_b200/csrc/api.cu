@@ -81,6 +81,9 @@ struct wgkv_ctx {
     int64_t* ws_near = nullptr;
     float* ws_part = nullptr;
     int* ws_nchunks = nullptr;
+    int* ws_slot = nullptr;  // [S*H] new-token ring slot recorded by K4 for the side-stream gate
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int max_chunks = 64;
     long near_cap = 0;
     // host mirrors for lifecycle checks and grid sizing
@@ -191,6 +194,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     const int gs = c.q_heads / c.kv_heads;
     ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
     ctx->ws_nchunks = dalloc<int>((size_t)S * H + 1, o);  // + work-stealing counter
+    ctx->ws_slot = dalloc<int>((size_t)S * H, o);
     for (void* p : o)
         if (!p) {
             for (void* q : o) cudaFree(q);
@@ -216,6 +220,9 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
         delete ctx;
         return fail(WGKV_ECUDA, "wgkv_ctx_create: init failed");
     }
+    cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
     ctx->prefilled.assign((size_t)L * S, 0);
     ctx->tokens.assign((size_t)L * S, 0);
     *out = ctx;
@@ -227,6 +234,9 @@ int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     cudaSetDevice(ctx->cfg.device);
     cudaDeviceSynchronize();
     for (void* p : ctx->owned) cudaFree(p);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     delete ctx;
     return WGKV_OK;
 }
@@ -442,7 +452,8 @@ static int decode_check(wgkv_ctx* ctx, int layer, int seq0, int nseq) {
 }
 
 static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
-                              const float* forced_g, float* g_out, int32_t* events_out, int* work_counter) {
+                              const float* forced_g, float* g_out, int32_t* events_out, int* work_counter,
+                              bool split_gate) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
@@ -454,10 +465,12 @@ static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, cons
     if (ctx->cfg.dtype == WGKV_BF16)
         st = launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
                                                  (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g,
-                                                 g_out, events_out, work_counter, ctx->stream);
+                                                 g_out, events_out, work_counter, ctx->ws_slot, ctx->stream,
+                                                 split_gate ? ctx->side : nullptr, ctx->ev_fork, ctx->ev_join);
     else
         st = launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
-                                         (const float*)v, forced_g, g_out, events_out, work_counter, ctx->stream);
+                                         (const float*)v, forced_g, g_out, events_out, work_counter, ctx->ws_slot,
+                                         ctx->stream, split_gate ? ctx->side : nullptr, ctx->ev_fork, ctx->ev_join);
     if (st) return fail(st, "decode append kernel failed");
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
     return WGKV_OK;
@@ -508,7 +521,7 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
 
 int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
                         const float* forced_g, float* g_out, int32_t* events_out) {
-    return decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, nullptr);
+    return decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, nullptr, false);
 }
 
 int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out) {
@@ -523,9 +536,13 @@ int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* 
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     const bool fused = fast_decode(ctx->cfg) && ctx->cfg.topk_budget == 0;
     int* counter = fused ? ctx->ws_nchunks + (size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads : nullptr;
-    int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, counter);
+    // the new token's gate forks onto the side stream and runs alongside K5
+    const bool split = !forced_g;
+    int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, counter, split);
     if (st) return st;
-    return decode_attn_impl(ctx, layer, seq0, nseq, q, out, fused);
+    st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, fused);
+    if (split) cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);  // join (capture-safe)
+    return st;
 }
 
 int wgkv_cache_state(wgkv_ctx* ctx, int layer, int seq, int kv_head, int64_t* lens) {
