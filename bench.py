@@ -458,7 +458,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="issue decode kernels eagerly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-T", type=int, default=8192)
+    ap.add_argument("--cpu-sample-T", type=int, default=16384)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
