@@ -82,6 +82,9 @@ struct wgkv_ctx {
     float* ws_part = nullptr;
     int* ws_nchunks = nullptr;
     int* ws_slot = nullptr;  // [S*H] new-token ring slot recorded by K4 for the side-stream gate
+    float* ws_score = nullptr;  // K6: [S][Hq][n_gp] page scores
+    int32_t* ws_sel = nullptr;  // K6: [S][Hq][n_gp] selected logical pages
+    int32_t* ws_nsel = nullptr; // K6: [S][Hq]
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int max_chunks = 64;
@@ -195,6 +198,11 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
     ctx->ws_nchunks = dalloc<int>((size_t)S * H + 1, o);  // + work-stealing counter
     ctx->ws_slot = dalloc<int>((size_t)S * H, o);
+    if (c.topk_budget > 0) {
+        ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
+        ctx->ws_sel = dalloc<int32_t>((size_t)S * c.q_heads * n_gp, o);
+        ctx->ws_nsel = dalloc<int32_t>((size_t)S * c.q_heads, o);
+    }
     for (void* p : o)
         if (!p) {
             for (void* q : o) cudaFree(q);
@@ -506,7 +514,17 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
     a.freq = ctx->freq;
     a.n_pairs = nseq * c.kv_heads;
     a.nchunks = nullptr;
-    if (c.topk_budget > 0) return fail(WGKV_ENOTSUP, "topk decode not built in this revision");
+    if (c.topk_budget > 0) {  // wgkv_plus_topk (engine.cpp:320-324)
+        if (c.dtype == WGKV_BF16)
+            st = launch_topk_decode<__nv_bfloat16>(a, nseq, c.topk_budget, (const __nv_bfloat16*)q, ctx->ws_score,
+                                                   ctx->ws_sel, ctx->ws_nsel, ctx->ws_part, (__nv_bfloat16*)out,
+                                                   ctx->stream);
+        else
+            st = launch_topk_decode<float>(a, nseq, c.topk_budget, (const float*)q, ctx->ws_score, ctx->ws_sel,
+                                           ctx->ws_nsel, ctx->ws_part, (float*)out, ctx->stream);
+        if (st) return fail(st, std::string("topk decode: ") + cudaGetErrorString(cudaGetLastError()));
+        return WGKV_OK;
+    }
     if (fast_decode(c))
         st = launch_decode_attn_mma(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part, ctx->ws_nchunks,
                                     (__nv_bfloat16*)out, ctx->stream, fused);

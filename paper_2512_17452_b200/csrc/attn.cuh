@@ -24,6 +24,12 @@ struct DecArgs {
     const int* nchunks;   // per (seq, kv head) chunk count written on device, or null (use n_chunks)
 };
 
+// K6: select_topk_pages + per-q-head attention over the selection (topk.cu).
+// scores/sel: [nseq][q_heads][n_gp]; nsel: [nseq][q_heads]
+template <typename E>
+int launch_topk_decode(const DecArgs& a, int nseq, long budget, const E* q, float* scores, int32_t* sel,
+                       int32_t* nsel, float* part, E* out, cudaStream_t st);
+
 // counter_reset_by_append: K4 ran just before on the stream and zeroed the
 // work counter; K5 is then launched as its programmatic dependent (PDL)
 int launch_decode_attn_mma(const DecArgs& a, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,

@@ -74,12 +74,10 @@ def test_gate_bits_bit_exact(W, orc, w_std, b2):
 def _run_golden(W, path, dtype):
     z = np.load(path)
     L, hq, hkv, d, hid, n, steps, Wn, ps, topk = (int(x) for x in z["cfg"])
-    if topk:
-        pytest.skip("top-k decode lands with K6")
     dt = torch.bfloat16 if dtype == "bf16" else torch.float32
     s = W.Session(L, hq, hkv, d, hid, Wn, tau=float(z["tau"]), rope_base=float(z["base"]), page_size=ps,
                   max_tokens=n + steps, dtype=W.BF16 if dtype == "bf16" else W.F32, gate_bank=z["bank"],
-                  attn_impl=W.ATTN_SIMT)
+                  attn_impl=W.ATTN_SIMT, topk_budget=topk)
     q, k, v = (z[x] for x in ("q", "k", "v"))
     tol = TOL[dtype]
     for l in range(L):
@@ -237,3 +235,31 @@ def test_tc_matches_simt_bitwise_bits_close_outputs(W, orc):
         outs.append(s.prefill_layer(0, q, k, v).float().cpu().numpy())
         s.sync()
     assert rel_err(outs[1], outs[0]) < 1e-2
+
+
+# ---------------------------------------------------- K6 select_topk_pages --
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("budget", [1, 3, 1000])
+def test_topk_decode_vs_oracle(W, orc, dtype, budget):
+    """wgkv_plus_topk decode (engine.cpp:320-324): per q head, max-dot page
+    scores, top-`budget` pages (ties to older), attention over them + Local."""
+    d, hq, hkv, T, steps, Wn = 128, 8, 2, 600, 12, 64
+    bank = orc.gate_random_init(1, hkv, d, d, 41, 0.1, -1.5)
+    q = bf16_np(orc.gaussian(42, (T + steps) * hq * d).reshape(1, T + steps, hq, d))
+    k = bf16_np(orc.gaussian(43, (T + steps) * hkv * d).reshape(1, T + steps, hkv, d))
+    v = bf16_np(orc.gaussian(44, (T + steps) * hkv * d).reshape(1, T + steps, hkv, d))
+    # plant a loud key every 40 tokens so the best pages are well separated
+    for t in range(0, T, 40):
+        k[0, t] *= 3.0
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    s = W.Session(1, hq, hkv, d, d, Wn, max_tokens=T + steps, dtype=W.BF16 if dtype == "bf16" else W.F32,
+                  gate_bank=bank, topk_budget=budget)
+    s.prefill_layer(0, to_dev(q[:, :T], dt), to_dev(k[:, :T], dt), to_dev(v[:, :T], dt))
+    r = O.Session(orc, 1, hq, hkv, d, d, Wn, gate_bank=bank, max_tokens=T + steps, topk_budget=budget)
+    r.prefill_layer(0, q[0, :T], k[0, :T], v[0, :T])
+    for t in range(T, T + steps):
+        o = s.decode_layer(0, to_dev(q[:, t], dt), to_dev(k[:, t], dt), to_dev(v[:, t], dt))
+        ro, _, _, _ = r.decode_layer(0, q[0, t], k[0, t], v[0, t])
+        o = o.float().cpu().numpy()[0]
+        for p in range(hq):
+            assert rel_err(o[p], ro[p]) < TOL[dtype], (t, p)
