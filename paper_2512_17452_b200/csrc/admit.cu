@@ -310,7 +310,10 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
         nst.tokens_seen += 1;
         pv.state[hidx] = nst;
         if (events) events[(size_t)s * pv.kv_heads + h] = event;
-        if (work_counter && blockIdx.x == 0) *work_counter = 0;  // K5's work-stealing counter
+        if (work_counter) {  // K5's work-stealing counter and this (seq, head)'s chunk-merge counter
+            if (blockIdx.x == 0) work_counter[0] = 0;
+            work_counter[1 + blockIdx.x] = 0;
+        }
     }
     // everything K5 reads (pages, tables, state) is written: let the attention
     // kernel (launched as a programmatic dependent) start now

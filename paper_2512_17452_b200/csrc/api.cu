@@ -196,7 +196,8 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->ws_near = dalloc<int64_t>((size_t)ctx->near_cap, o);
     const int gs = c.q_heads / c.kv_heads;
     ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
-    ctx->ws_nchunks = dalloc<int>((size_t)S * H + 1, o);  // + work-stealing counter
+    // per-pair chunk counts | work-stealing counter | per-pair merge counters
+    ctx->ws_nchunks = dalloc<int>(2 * (size_t)S * H + 1, o);
     ctx->ws_slot = dalloc<int>((size_t)S * H, o);
     if (c.topk_budget > 0) {
         ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
