@@ -59,9 +59,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
                                                                       DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                       float* __restrict__ part,
                                                                       int* __restrict__ nchunks,
-                                                                      int* __restrict__ work_counter,
-                                                                      int* __restrict__ pair_done,
-                                                                      __nv_bfloat16* __restrict__ out) {
+                                                                      int* __restrict__ work_counter) {
     extern __shared__ uint8_t dsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     constexpr int d = 128;
@@ -289,35 +287,6 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
                 pout[g * (d + 2) + d + 1] = L;
             }
         }
-        // ---- the last chunk of this (seq, kv head) to finish merges all of its
-        // chunk partials (replaces a separate combine launch)
-        __shared__ int s_last;
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            const int nc_bh = item_base[bh + 1] - item_base[bh];
-            s_last = atomicAdd(&pair_done[bh], 1) == nc_bh - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            const int nc_bh = item_base[bh + 1] - item_base[bh];
-            const float* pb = part + (size_t)bh * a.max_chunks * pstride;
-            for (int e = tid; e < gs * d; e += blockDim.x) {
-                const int g = e / d, c = e % d;
-                float M = -INFINITY;
-                for (int ch = 0; ch < nc_bh; ++ch) M = fmaxf(M, pb[ch * pstride + g * (d + 2) + d]);
-                float acc = 0.f, L = 0.f;
-                for (int ch = 0; ch < nc_bh; ++ch) {
-                    const float* r = pb + ch * pstride + g * (d + 2);
-                    if (r[d] == -INFINITY) continue;
-                    const float f = __expf(r[d] - M);
-                    acc += f * r[c];
-                    L += f * r[d + 1];
-                }
-                out[((size_t)s * a.q_heads + h * gs + g) * d + c] = __float2bfloat16_rn(acc / L);
-            }
-        }
         __syncthreads();
     }
 }
@@ -357,11 +326,10 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = counter_reset_by_append ? 1 : 0;
-    // per-(seq, kv head) completion counters live after the work counter
-    int* pair_done = counter + 1;
-    if (!counter_reset_by_append) cudaMemsetAsync(pair_done, 0, sizeof(int) * a.n_pairs, st);
-    cudaLaunchKernelEx(&cfg, decode_attn_mma_kernel, tp, a, q, part, nchunks, counter, pair_done, out);
-    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+    cudaLaunchKernelEx(&cfg, decode_attn_mma_kernel, tp, a, q, part, nchunks, counter);
+    a.nchunks = nchunks;
+    extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
+    return launch_decode_combine_bf16(a, nseq, part, out, st);
 }
 
 }  // namespace wgkv
