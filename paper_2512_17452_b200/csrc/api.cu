@@ -70,6 +70,7 @@ struct wgkv_ctx {
     float *w1t = nullptr, *b1f = nullptr, *w2f = nullptr;
     double *b2f = nullptr, *w1d = nullptr, *b1d = nullptr, *w2d = nullptr, *freq = nullptr;
     float* bandc = nullptr;  // per (layer, kv head) fp32 error-bound constant for K1's recheck band
+    __nv_bfloat16* w1split = nullptr;  // [L*H][Wpre_hi, Wpost_hi, Wpre_lo, Wpost_lo][128][128] (K1 tcgen05)
     bool gates_set = false;
     // workspaces
     void* ws_kpost = nullptr;
@@ -181,6 +182,8 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->b2f = dalloc<double>(blocks, o);
     ctx->bandc = dalloc<float>(blocks, o);
     ctx->w1d = dalloc<double>(blocks * fd * c.hidden, o);
+    if (c.dtype == WGKV_BF16 && d == 128 && c.hidden == 128)  // K1 tensor-core operand: split-bf16 W1 tiles
+        ctx->w1split = dalloc<__nv_bfloat16>(blocks * 4 * 128 * 128, o);
     ctx->b1d = dalloc<double>(blocks * c.hidden, o);
     ctx->w2d = dalloc<double>(blocks * c.hidden, o);
     ctx->freq = dalloc<double>((size_t)d / 2, o);
@@ -314,6 +317,20 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
     WGKV_CUDA_TRY(cudaMemcpy(ctx->w2d, w2d.data(), w2d.size() * 8, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->b2f, b2.data(), b2.size() * 8, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->bandc, bandc.data(), bandc.size() * 4, cudaMemcpyHostToDevice));
+    if (ctx->w1split) {  // W1 = hi + lo in bf16, as four K-major [128 hidden][128 k] tiles per head
+        std::vector<__nv_bfloat16> ws(nb * 4 * 128 * 128);
+        for (size_t b = 0; b < nb; ++b)
+            for (int u = 0; u < 128; ++u)
+                for (int k = 0; k < 256; ++k) {
+                    const double w = w1d[(b * 128 + u) * 256 + k];
+                    const __nv_bfloat16 hi = __float2bfloat16_rn((float)w);
+                    const __nv_bfloat16 lo = __float2bfloat16_rn((float)(w - (double)__bfloat162float(hi)));
+                    const size_t seg = k < 128 ? 0 : 1;  // 0: k_pre columns, 1: k_post columns
+                    ws[((b * 4 + seg) * 128 + u) * 128 + (k & 127)] = hi;
+                    ws[((b * 4 + 2 + seg) * 128 + u) * 128 + (k & 127)] = lo;
+                }
+        WGKV_CUDA_TRY(cudaMemcpy(ctx->w1split, ws.data(), ws.size() * 2, cudaMemcpyHostToDevice));
+    }
     ctx->gates_set = true;
     return WGKV_OK;
 }
@@ -364,12 +381,15 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
         // effective_gate override (engine.cpp:126-151): RoPE only, g = forced, bit = g >= tau
         st = launch_forced_gate(a, nseq, k_pre, k_post_out, forced_g, g_out, bits_out, ctx->esz, ctx->stream);
     } else if (ctx->cfg.dtype == WGKV_BF16) {
+        const bool tc = ctx->cfg.attn_impl != WGKV_ATTN_SIMT && ctx->w1split;
         st = launch_gate_prefill<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)k_pre, (__nv_bfloat16*)k_post_out,
                                                 g_out, bits_out, ctx->ws_cand, ctx->ws_cnt, nidx, ncap,
-                                                ctx->ws_cnt + 1, ctx->stream);
+                                                ctx->ws_cnt + 1, tc ? ctx->w1split : nullptr,
+                                                (long)ctx->cfg.layers * ctx->cfg.kv_heads * 4, ctx->stream);
     } else {
         st = launch_gate_prefill<float>(a, nseq, (const float*)k_pre, (float*)k_post_out, g_out, bits_out,
-                                        ctx->ws_cand, ctx->ws_cnt, nidx, ncap, ctx->ws_cnt + 1, ctx->stream);
+                                        ctx->ws_cand, ctx->ws_cnt, nidx, ncap, ctx->ws_cnt + 1, nullptr, 0,
+                                        ctx->stream);
     }
     if (st) return fail(st, std::string("gate kernels: ") + cudaGetErrorString(cudaGetLastError()));
     if (near_count) {

@@ -206,16 +206,27 @@ __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, flo
 template <typename T>
 int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, float* g, uint8_t* bits,
                         int64_t* cand, int* cand_cnt, int64_t* near_idx, int near_cap, int* near_cnt,
-                        cudaStream_t st) {
-    const size_t smem = sizeof(float) * ((size_t)2 * a.d * GT_XS + 2 * GT_KC * GT_HID + 2 * GT_TOK);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(gate_prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+                        const __nv_bfloat16* w1split, long n_wtiles, cudaStream_t st) {
     cudaMemsetAsync(cand_cnt, 0, sizeof(int), st);
-    dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
-    gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, cand_cnt);
+    bool done = false;
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        // tensor-core path (d = hidden = 128, split-bf16 W1 prepared by wgkv_gate_set)
+        if (w1split && a.d == 128 && a.hidden == 128) {
+            const int r = launch_gate_tc(a, nseq, k_pre, k_post, g, bits, cand, cand_cnt, w1split, n_wtiles, st);
+            if (r != WGKV_OK) return r;
+            done = true;
+        }
+    }
+    if (!done) {
+        const size_t smem = sizeof(float) * ((size_t)2 * a.d * GT_XS + 2 * GT_KC * GT_HID + 2 * GT_TOK);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(gate_prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set = true;
+        }
+        dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
+        gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, cand_cnt);
+    }
     const int nw = 8;
     const size_t rsm = sizeof(double) * nw * (2 * a.d + a.hidden) + sizeof(float) * nw * a.d;
     gate_recheck_kernel<T><<<kNumSMs * 4, 32 * nw, rsm, st>>>(a, k_pre, g, bits, cand, cand_cnt, near_idx, near_cap,
@@ -262,8 +273,9 @@ int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_p
 }
 
 template int launch_gate_prefill<float>(const GateArgs&, int, const float*, float*, float*, uint8_t*, int64_t*, int*,
-                                        int64_t*, int, int*, cudaStream_t);
+                                        int64_t*, int, int*, const __nv_bfloat16*, long, cudaStream_t);
 template int launch_gate_prefill<__nv_bfloat16>(const GateArgs&, int, const __nv_bfloat16*, __nv_bfloat16*, float*,
-                                                uint8_t*, int64_t*, int*, int64_t*, int, int*, cudaStream_t);
+                                                uint8_t*, int64_t*, int*, int64_t*, int, int*, const __nv_bfloat16*,
+                                                long, cudaStream_t);
 
 }  // namespace wgkv

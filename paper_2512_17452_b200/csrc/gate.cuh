@@ -166,6 +166,11 @@ int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_p
 template <typename T>
 int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, float* g, uint8_t* bits,
                         int64_t* cand, int* cand_cnt, int64_t* near_idx, int near_cap, int* near_cnt,
-                        cudaStream_t st);
+                        const __nv_bfloat16* w1split, long n_wtiles, cudaStream_t st);
+
+// tensor-core K1 (gate_tc.cu): w1split = [L*H][4][128][128] bf16 split W1 tiles
+int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv_bfloat16* k_post, float* g,
+                   uint8_t* bits, int64_t* cand, int* cand_cnt, const __nv_bfloat16* w1split, long n_wtiles,
+                   cudaStream_t st);
 
 }  // namespace wgkv

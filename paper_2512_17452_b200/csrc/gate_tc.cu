@@ -1,0 +1,214 @@
+// gate_tc.cu -- K1 on the 5th-gen tensor cores: z1 = W1 . [k_pre ; k_post]
+// as a tcgen05 GEMM (M = 128 tokens, N = 128 hidden, K = 2d = 256) with a
+// split-bf16 scheme that keeps ~fp32 accuracy:
+//     k_pre        is exact in bf16 (it is the bf16 input);
+//     k_post = hi + lo,  W1 = W_hi + W_lo   (bf16 pairs, |rest| <= 2^-17 rel.)
+//     z1 = Apre.(Wpre_hi + Wpre_lo) + Ahi.(Wpost_hi + Wpost_lo) + Alo.Wpost_hi
+// i.e. 5 K=128 segments accumulated in one fp32 TMEM tile.  The epilogue
+// (one TMEM lane = one token per thread) adds b1, applies the exact-erf GELU,
+// the w2 dot, sigmoid and threshold, and lists tokens inside a worst-case error
+// band for the fp64 recheck (gate.cu), so the final bits are the reference's
+// (gating.cpp:158-190) except reported |g - tau| < 1e-6 tokens.
+//
+// Persistent: 148 CTAs walk a flat list of (seq, kv head, 128-token tile)
+// ordered by head, reloading W1's split tiles only when the head changes.
+// Warps 0-3 build the A tiles (load k_pre, RoPE, split, write SW128 smem; also
+// write k_post to global) and run the epilogue; warp 4 owns TMEM, loads B by
+// TMA and issues the MMAs.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "gate.cuh"
+#include "tc.cuh"
+
+namespace wgkv {
+
+namespace {
+constexpr uint32_t GT_TILE = 128 * 128 * 2;  // one [128][128] bf16 operand tile (2 SW128 sub-tiles)
+constexpr uint32_t GT_SUB = GT_TILE / 2;
+constexpr uint32_t G_OFF_B = 0;               // 4 B tiles: Wpre_hi, Wpost_hi, Wpre_lo, Wpost_lo
+constexpr uint32_t G_OFF_A = 4 * GT_TILE;     // 3 A tiles: k_pre, k_post hi, k_post lo
+constexpr uint32_t G_OFF_BAR = G_OFF_A + 3 * GT_TILE;
+constexpr uint32_t G_SMEM = G_OFF_BAR + 2048 + 1024;
+constexpr int G_THREADS = 160;
+
+__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk) {
+    return tc::smem_desc_sw128(tile + (uint32_t)(kk >> 2) * GT_SUB + (uint32_t)(kk & 3) * 32u, 16, 1024);
+}
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+}  // namespace
+
+struct GateTcArgs {
+    GateArgs g;
+    int nseq;
+    long tiles_per_pair;
+    long total_tiles;
+};
+
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gate_tc_kernel(const __grid_constant__ CUtensorMap tw, GateTcArgs A, const __nv_bfloat16* __restrict__ k_pre,
+                   __nv_bfloat16* __restrict__ k_post, float* __restrict__ g_out, uint8_t* __restrict__ bits_out,
+                   int64_t* __restrict__ cand, int* __restrict__ cand_cnt) {
+    extern __shared__ uint8_t gsm_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = smem_u32(sm);
+    uint64_t* b_full = reinterpret_cast<uint64_t*>(sm + G_OFF_BAR);
+    uint64_t* a_ready = b_full + 1;
+    uint64_t* mma_done = b_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 3);
+    float* b1s = reinterpret_cast<float*>(b_full + 4);  // [128]
+    float* w2s = b1s + 128;                             // [128]
+    const GateArgs& a = A.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long t_begin = A.total_tiles * blockIdx.x / gridDim.x;
+    const long t_end = A.total_tiles * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) {
+        tc::mbar_init(b_full, 1);
+        tc::mbar_init(a_ready, 128);
+        tc::mbar_init(mma_done, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 4) tc::tmem_alloc(tmem_slot, 128);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const float u_eff = 5.0e-5f;  // per-product worst-case relative error of the split + fp32 accumulation
+    int cur_blk = -1, b_loads = 0;
+    for (long tile = t_begin; tile < t_end; ++tile) {
+        const int pair = (int)(tile / A.tiles_per_pair);
+        const long t0 = (tile % A.tiles_per_pair) * 128;
+        const int s = pair / a.kv_heads, h = pair % a.kv_heads;
+        const int blk = a.layer * a.kv_heads + h;
+        const int it = (int)(tile - t_begin);
+        if (blk != cur_blk) {  // (re)load W1's split tiles and b1/w2 for this head
+            __syncthreads();   // previous tile's MMA has completed (waited below) before B is overwritten
+            if (warp == 4 && lane == 0) {
+                tc::mbar_arrive_expect_tx(b_full, 4 * GT_TILE);
+                for (int q = 0; q < 4; ++q)
+                    for (int hh = 0; hh < 2; ++hh)
+                        tc::tma_load_3d(sm + G_OFF_B + q * GT_TILE + hh * GT_SUB, &tw, b_full, hh * 64, 0,
+                                        blk * 4 + q);
+            }
+            if (threadIdx.x < 128) {
+                b1s[threadIdx.x] = a.b1f[(size_t)blk * 128 + threadIdx.x];
+                w2s[threadIdx.x] = a.w2f[(size_t)blk * 128 + threadIdx.x];
+            }
+            tc::mbar_wait(b_full, b_loads & 1);
+            ++b_loads;
+            cur_blk = blk;
+            __syncthreads();
+        }
+        if (warp < 4) {
+            // ---- A tiles: one token row per thread ---------------------------------
+            const int r = threadIdx.x;
+            const long t = t0 + r;
+            float xx = 0.f;
+            const size_t off = (((size_t)s * a.T + min(t, a.T - 1)) * a.kv_heads + h) * 128;
+            const uint4* src = reinterpret_cast<const uint4*>(k_pre + off);
+            uint4* dpost = reinterpret_cast<uint4*>(k_post + off);
+#pragma unroll 2
+            for (int c = 0; c < 16; ++c) {  // 16-byte chunk c = dims 8c .. 8c+7
+                uint4 raw = t < a.T ? src[c] : make_uint4(0, 0, 0, 0);
+                const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float x0 = __uint_as_float(w[u] << 16), x1 = __uint_as_float(w[u] & 0xffff0000u);
+                    float cs, sn;
+                    rope_cs(a.freq, c * 4 + u, a.pos0 + t, cs, sn);
+                    const float y0 = x0 * cs - x1 * sn, y1 = x0 * sn + x1 * cs;
+                    xx = fmaf(x0, x0, fmaf(x1, x1, fmaf(y0, y0, fmaf(y1, y1, xx))));
+                    const uint16_t h0 = bf16_bits(y0), h1 = bf16_bits(y1);
+                    const float r0 = y0 - __uint_as_float((uint32_t)h0 << 16), r1 = y1 - __uint_as_float((uint32_t)h1 << 16);
+                    hi[u] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+                    lo[u] = (uint32_t)bf16_bits(r0) | ((uint32_t)bf16_bits(r1) << 16);
+                }
+                const uint32_t so = (uint32_t)(c >> 3) * GT_SUB + tc::sw128_off(r, c & 7);
+                *reinterpret_cast<uint4*>(sm + G_OFF_A + so) = raw;
+                *reinterpret_cast<uint4*>(sm + G_OFF_A + GT_TILE + so) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(sm + G_OFF_A + 2 * GT_TILE + so) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                if (t < a.T) dpost[c] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            }
+            tc::fence_proxy_async_smem();
+            tc::mbar_arrive(a_ready);
+            // ---- epilogue ----------------------------------------------------------
+            tc::mbar_wait(mma_done, it & 1);
+            tc::fence_after_sync();
+            const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+            float part = 0.f, apart = 0.f;
+#pragma unroll 1
+            for (int cc = 0; cc < 4; ++cc) {
+                uint32_t z[32];
+                tc::tmem_ld32(trow + 32 * cc, z);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const int hh = 32 * cc + e;
+                    const float z1 = __uint_as_float(z[e]) + b1s[hh];
+                    const float ge = 0.5f * z1 * (1.f + erff(z1 * 0.70710678118654752f));
+                    part = fmaf(w2s[hh], ge, part);
+                    apart += fabsf(w2s[hh] * ge);
+                }
+            }
+            tc::fence_before_sync();
+            if (t < a.T) {
+                const float z2 = (float)a.b2f[blk] + part;
+                const size_t gi = ((size_t)s * a.kv_heads + h) * a.T + t;
+                g_out[gi] = 1.f / (1.f + __expf(-z2));
+                bits_out[gi] = z2 >= a.ztau ? 1 : 0;
+                const float band = 4.f * (1.13f * 257.f * u_eff * sqrtf(xx) * a.bandc[blk] +
+                                          134.f * 5.9604645e-8f * (apart + fabsf((float)a.b2f[blk]) + fabsf(a.ztau)));
+                if (fabsf(z2 - a.ztau) <= band) cand[atomicAdd(cand_cnt, 1)] = (int64_t)gi;
+            }
+        } else if (lane == 0) {
+            // ---- MMA: 5 segments x 8 K-steps into one fp32 tile ----------------------
+            tc::mbar_wait(a_ready, it & 1);
+            tc::fence_after_sync();
+            constexpr uint32_t idG = tc::idesc_bf16(128, 128, false, false);
+            const uint32_t Apre = sbase + G_OFF_A, Ahi = Apre + GT_TILE, Alo = Apre + 2 * GT_TILE;
+            const uint32_t Bph = sbase + G_OFF_B, Bqh = Bph + GT_TILE, Bpl = Bph + 2 * GT_TILE, Bql = Bph + 3 * GT_TILE;
+            const uint32_t segA[5] = {Apre, Ahi, Apre, Ahi, Alo};
+            const uint32_t segB[5] = {Bph, Bqh, Bpl, Bql, Bqh};
+#pragma unroll
+            for (int sg = 0; sg < 5; ++sg)
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    tc::mma_ss(tmem, kdesc(segA[sg], kk), kdesc(segB[sg], kk), idG, (sg | kk) ? 1u : 0u);
+            tc::mma_commit(mma_done);
+        }
+        __syncwarp();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 4) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc(tmem, 128);
+    }
+}
+
+int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv_bfloat16* k_post, float* g,
+                   uint8_t* bits, int64_t* cand, int* cand_cnt, const __nv_bfloat16* w1split, long n_wtiles,
+                   cudaStream_t st) {
+    if (a.d != 128 || a.hidden != 128) return WGKV_ENOTSUP;
+    CUtensorMap tw;  // [L*H*4][128 hidden][128 k] split W1 tiles
+    if (make_tmap_3d_bf16(&tw, w1split, 128, 128, (uint64_t)n_wtiles, 256, 128 * 256, 64, 128, 1)) return WGKV_ECUDA;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gate_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+        attr = true;
+    }
+    GateTcArgs A;
+    A.g = a;
+    A.nseq = nseq;
+    A.tiles_per_pair = (a.T + 127) / 128;
+    A.total_tiles = A.tiles_per_pair * nseq * a.kv_heads;
+    const int grid = (int)std::min<long>(kNumSMs, A.total_tiles);
+    gate_tc_kernel<<<grid, G_THREADS, G_SMEM, st>>>(tw, A, k_pre, k_post, g, bits, cand, cand_cnt);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+}  // namespace wgkv
