@@ -201,21 +201,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) {
-                uint8_t* kdst = sm + OFF_KV + st * STAGE_BYTES;
-                uint8_t* vdst = kdst + TILE_BYTES;
-                tc::mbar_arrive_expect_tx(&bar->kv_full[st], STAGE_BYTES);
-                if (!band) {
+            uint8_t* kdst = sm + OFF_KV + st * STAGE_BYTES;
+            uint8_t* vdst = kdst + TILE_BYTES;
+            if (lane == 0) tc::mbar_arrive_expect_tx(&bar->kv_full[st], STAGE_BYTES);
+            __syncwarp();
+            if (!band) {
+                // lane-parallel issue: copy i = (page i/4, K|V, dim half); up to 4 * 16 copies
+                for (int i = lane; i < 4 * ppb; i += 32) {
+                    const int pi = i >> 2, kv = (i >> 1) & 1, hh = i & 1;
+                    int page = 0;
 #pragma unroll
-                    for (int pi = 0; pi < 16; ++pi) {
-                        if (pi >= ppb) break;
-                        const int page = pg[pi];
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const uint32_t o = hh * SUB_BYTES + pi * ps * 128;
-                            tc::tma_load_3d(kdst + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page);
-                            tc::tma_load_3d(vdst + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page + 1);
-                        }
-                    }
+                    for (int q = 0; q < 16; ++q)
+                        if (q == pi) page = pg[q];
+                    const uint32_t o = hh * SUB_BYTES + pi * ps * 128;
+                    tc::tma_load_3d((kv ? vdst : kdst) + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page + kv);
+                }
+            }
+            if (lane == 0) {
+                if (!band) {
                 } else {
                     for (int hh = 0; hh < 2; ++hh) {
                         tc::tma_load_3d(kdst + hh * SUB_BYTES, &tk, &bar->kv_full[st], hh * 64, h, (int)(s * T + kb0));
