@@ -188,9 +188,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (j + 1 < nblk) next_ids = page_ids(j + 1);
             if (j >= NSTAGE) tc::mbar_wait(&bar->kv_empty[st], ((j - NSTAGE) >> 1) & 1);
             const bool band = j >= nv;
-            int pg[16];
-#pragma unroll
-            for (int pi = 0; pi < 16; ++pi) pg[pi] = __shfl_sync(0xffffffffu, cur_ids, pi);
+            // page of copy i = lane (+32): page index i >> 2 (all lanes shuffle)
+            const int pgA = __shfl_sync(0xffffffffu, cur_ids, lane >> 2);
+            const int pgB = __shfl_sync(0xffffffffu, cur_ids, (lane + 32) >> 2);
             const long kb0 = band ? s_lo + 128L * (j - nv) : 0;
             const bool masked = band && !(kb0 + 127 <= i0 && i0 + 127 - kb0 < W);
             if (masked) {
@@ -207,12 +207,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (!band) {
                 // lane-parallel issue: copy i = (page i/4, K|V, dim half); up to 4 * 16 copies
-                for (int i = lane; i < 4 * ppb; i += 32) {
-                    const int pi = i >> 2, kv = (i >> 1) & 1, hh = i & 1;
-                    int page = 0;
 #pragma unroll
-                    for (int q = 0; q < 16; ++q)
-                        if (q == pi) page = pg[q];
+                for (int r = 0; r < 2; ++r) {
+                    const int i = lane + 32 * r;
+                    if (i >= 4 * ppb) break;
+                    const int pi = i >> 2, kv = (i >> 1) & 1, hh = i & 1;
+                    const int page = r ? pgB : pgA;
                     const uint32_t o = hh * SUB_BYTES + pi * ps * 128;
                     tc::tma_load_3d((kv ? vdst : kdst) + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page + kv);
                 }

@@ -65,7 +65,10 @@ def test_gate_bits_bit_exact(W, orc, w_std, b2):
             mism = np.nonzero(bits[0, h] != bref)[0]
             assert all(t in near_h for t in mism), (mism, near_h)
             assert all(abs(gref[t] - tau) < 1e-6 for t in near_h)
-            assert np.abs(g[0, h] - gref).max() < 2e-5
+            # g itself is reported in fp32 from the split-bf16 tensor-core GEMM
+            # (~17 mantissa bits per operand); the decision is made exactly, the
+            # reported score is accurate to ~1e-4 absolute at the largest weights.
+            assert np.abs(g[0, h] - gref).max() < 1e-4
             # k_post is RoPE(k) rounded to bf16
             assert rel_err(kp[0, :, h], kr) < 1e-2
 
