@@ -339,6 +339,7 @@ def run_gpu(args, cfg):
     per = []
     with ClockSampler(local) as clk:
         barrier()
+        torch.cuda.profiler.start()  # `ncu --profile-from-start off` captures the timed region only
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
             e, k3 = one_step(True)
@@ -347,6 +348,7 @@ def run_gpu(args, cfg):
             per.append((e, k3))
         barrier()
         t_wall = time.perf_counter() - t_wall0
+        torch.cuda.profiler.stop()
     sess.sync()
     pre_ms = [e[0].elapsed_time(e[1]) for e, _ in per]
     dec_ms = [e[1].elapsed_time(e[2]) for e, _ in per]

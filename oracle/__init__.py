@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+import sys
 
 import numpy as np
 
@@ -41,8 +42,8 @@ _u64p = C.POINTER(C.c_uint64)
 def build(force: bool = False) -> None:
     """Compile liboracle.so (and _ref when /root/reference is present)."""
     if force or not os.path.exists(ORACLE_SO):
-        subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
-    subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True, stdout=sys.stderr)
+    subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True, stdout=sys.stderr)
 
 
 def _f64(a) -> np.ndarray:
