@@ -372,17 +372,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 m = mn;
             }
             const float mu = (m == -INFINITY) ? 0.f : m;
-            float lsv[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent partial sums
+            // packed f32x2 arithmetic (FADD2) halves the subtract and row-sum
+            // instruction count; 4 independent float2 partial sums
+            float2 lsv[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+            const float2 nmu = make_float2(-mu, -mu);
             uint32_t pa[32], pb[32];
             auto expo = [&](const uint32_t(&x)[32], uint32_t(&dst)[32], int off) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
-                    const float x0 = __uint_as_float(x[2 * e]) - mu, x1 = __uint_as_float(x[2 * e + 1]) - mu;
+                    const float2 xd = __fadd2_rn(make_float2(__uint_as_float(x[2 * e]), __uint_as_float(x[2 * e + 1])), nmu);
+                    const float x0 = xd.x, x1 = xd.y;
 #if WGKV_EXP_BF16X2
                     // one packed XU op yields both P values in MMA format; the
                     // row sum uses exactly the bf16 values the MMA consumes
                     const uint32_t pp = ex2_bf16x2(tc::pack_bf16x2(x0, x1));
-                    lsv[e & 3] += __uint_as_float(pp << 16) + __uint_as_float(pp & 0xffff0000u);
+                    lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u)));
                     dst[off + e] = pp;
                     continue;
 #endif
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                                                WGKV_EMU_EVERY - 1;
                     const float e0 = emu ? ex2_emu(x0) : ex2(x0);
                     const float e1 = emu ? ex2_emu(x1) : ex2(x1);
-                    lsv[e & 3] += e0 + e1;
+                    lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(e0, e1));
                     dst[off + e] = WGKV_PACK_ALU ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
                 }
             };
@@ -399,7 +403,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             expo(s1, pa, 16);
             expo(s2, pb, 0);
             expo(s3, pb, 16);
-            l += (lsv[0] + lsv[1]) + (lsv[2] + lsv[3]);
+            {
+                const float2 a01 = __fadd2_rn(lsv[0], lsv[1]), a23 = __fadd2_rn(lsv[2], lsv[3]);
+                const float2 t = __fadd2_rn(a01, a23);
+                l += t.x + t.y;
+            }
             tc::tmem_st32(trow + colS, pa);
             tc::tmem_st32(trow + colS + 32, pb);
             // O_t is complete up to PV(j-1) (s_full(j) was committed after it);
