@@ -25,3 +25,10 @@ oracle:
 
 clean:
 	rm -rf build $(PKG)/libwgkv_b200.so
+
+# A/B experiment build: make variant NAME=x DEFS="-DFOO=1" -> build/var/libwgkv_x.so
+# (load with WGKV_LIB=build/var/libwgkv_x.so; not a product artefact)
+variant: $(OBJ)
+	@mkdir -p build/var/$(NAME)
+	$(NVCC) $(NVFLAGS) $(DEFS) -I$(PKG)/csrc -c $(or $(SRCF),$(PKG)/csrc/attn_tc.cu) -o build/var/$(NAME)/attn_tc.o 2> build/var/$(NAME)/ptxas.log || (cat build/var/$(NAME)/ptxas.log; false)
+	$(NVCC) $(ARCH) -shared -o build/var/libwgkv_$(NAME).so $(filter-out build/attn_tc.o,$(OBJ)) build/var/$(NAME)/attn_tc.o -Xcompiler -fPIC

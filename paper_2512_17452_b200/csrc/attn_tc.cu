@@ -39,15 +39,19 @@ constexpr uint32_t OFF_Q = 0;
 constexpr uint32_t OFF_KV = NT * TILE_BYTES;
 constexpr uint32_t STAGE_BYTES = 2 * TILE_BYTES;      // K then V
 constexpr uint32_t OFF_BAR = OFF_KV + NSTAGE * STAGE_BYTES;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 512 + 1024;  // + barriers/meta + alignment slack
-constexpr int NTHREADS = 320;  // 3 full warpgroups (setmaxnreg is per warpgroup)
+constexpr int NSPLIT = 2;                   // softmax warpgroups per tile (column halves)
+constexpr int HC = 128 / NSPLIT;            // S columns per softmax thread
+constexpr int NSOFT = NT * NSPLIT * 4;      // softmax warps
+constexpr int WARP_TMA = NSOFT, WARP_MMA = NSOFT + 1;
+constexpr uint32_t OFF_X = OFF_BAR + 512;   // [NT][NSPLIT][128] f32 row-max / row-sum exchange
+constexpr uint32_t SMEM_BYTES = OFF_X + NT * NSPLIT * 128 * 4 + 1024;  // + alignment slack
+constexpr int NTHREADS = (NSOFT + 2) * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct Bars {
     uint64_t q_full, q_ready;
-    uint64_t kv_full[NSTAGE], kv_empty[NSTAGE];
+    uint64_t k_full[NSTAGE], k_empty[NSTAGE], v_full[NSTAGE], v_empty[NSTAGE];
     uint64_t s_full[NT], p_full[NT], o_final[NT];
-    uint32_t mask[NSTAGE][4];
     uint32_t tmem;
     int C;
 };
@@ -135,19 +139,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         C = min(C, a.pv.state[hidx].global_len);  // 0 after a failed page claim
         bar->C = C;
         tc::mbar_init(&bar->q_full, 1);
-        tc::mbar_init(&bar->q_ready, NT * 128);
+        tc::mbar_init(&bar->q_ready, NSOFT * 32);
         for (int i = 0; i < NSTAGE; ++i) {
-            tc::mbar_init(&bar->kv_full[i], 1);
-            tc::mbar_init(&bar->kv_empty[i], 1);
+            tc::mbar_init(&bar->k_full[i], 1);
+            tc::mbar_init(&bar->k_empty[i], 1);
+            tc::mbar_init(&bar->v_full[i], 1);
+            tc::mbar_init(&bar->v_empty[i], 1);
         }
         for (int t = 0; t < NT; ++t) {
             tc::mbar_init(&bar->s_full[t], 1);
-            tc::mbar_init(&bar->p_full[t], 128);
+            tc::mbar_init(&bar->p_full[t], NSPLIT * 128);
             tc::mbar_init(&bar->o_final[t], 1);
         }
         tc::fence_barrier_init();
     }
-    if (warp == 9) tc::tmem_alloc(&bar->tmem, 512);
+    if (warp == WARP_MMA) tc::tmem_alloc(&bar->tmem, 512);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int nblk = nv + nb;
     const int ps = a.pv.page_size;
 
-    if (warp == 8) {
+    if (warp == WARP_TMA) {
         // ================================ TMA producer ===========================
         if (lane == 0) {
             tc::tma_prefetch(&tq);
@@ -182,52 +188,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             return (jb < nv && lane < ppb) ? gpt[min(jb * ppb + lane, last_page)] : 0;
         };
         int next_ids = page_ids(0);
+        // K and V of a block have separate full/empty barriers: K(j) is free
+        // once both tiles' S(j) are done, long before PV(j) releases V(j), so
+        // the K refill gets a whole extra MMA round of slack.
         for (int j = 0; j < nblk; ++j) {
             const int st = j & 1;
             const int cur_ids = next_ids;
             if (j + 1 < nblk) next_ids = page_ids(j + 1);
-            if (j >= NSTAGE) tc::mbar_wait(&bar->kv_empty[st], ((j - NSTAGE) >> 1) & 1);
             const bool band = j >= nv;
-            // page of copy i = lane (+32): page index i >> 2 (all lanes shuffle)
-            const int pgA = __shfl_sync(0xffffffffu, cur_ids, lane >> 2);
-            const int pgB = __shfl_sync(0xffffffffu, cur_ids, (lane + 32) >> 2);
             const long kb0 = band ? s_lo + 128L * (j - nv) : 0;
-            const bool masked = band && !(kb0 + 127 <= i0 && i0 + 127 - kb0 < W);
-            if (masked) {
-                for (int w = 0; w < 4; ++w) {
-                    const long key = kb0 + 32 * w + lane;
-                    const unsigned m = __ballot_sync(0xffffffffu, key < T && bits[key] != 0);
-                    if (lane == 0) bar->mask[st][w] = m;
-                }
-            }
-            __syncwarp();
-            uint8_t* kdst = sm + OFF_KV + st * STAGE_BYTES;
-            uint8_t* vdst = kdst + TILE_BYTES;
-            if (lane == 0) tc::mbar_arrive_expect_tx(&bar->kv_full[st], STAGE_BYTES);
-            __syncwarp();
-            if (!band) {
-                // lane-parallel issue: copy i = (page i/4, K|V, dim half); up to 4 * 16 copies
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int i = lane + 32 * r;
-                    if (i >= 4 * ppb) break;
-                    const int pi = i >> 2, kv = (i >> 1) & 1, hh = i & 1;
-                    const int page = r ? pgB : pgA;
-                    const uint32_t o = hh * SUB_BYTES + pi * ps * 128;
-                    tc::tma_load_3d((kv ? vdst : kdst) + o, &tpool, &bar->kv_full[st], hh * 64, 0, 2 * page + kv);
-                }
-            }
-            if (lane == 0) {
+            // vertical copy `lane` = (page lane/2, dim half lane%2), 2*ppb <= 32
+            const int pg = __shfl_sync(0xffffffffu, cur_ids, lane >> 1);
+            for (int kv = 0; kv < 2; ++kv) {
+                uint64_t* full = kv ? &bar->v_full[st] : &bar->k_full[st];
+                if (j >= NSTAGE) tc::mbar_wait(kv ? &bar->v_empty[st] : &bar->k_empty[st], ((j - NSTAGE) >> 1) & 1);
+                uint8_t* dst = sm + OFF_KV + st * STAGE_BYTES + kv * TILE_BYTES;
+                if (lane == 0) tc::mbar_arrive_expect_tx(full, TILE_BYTES);
+                __syncwarp();
                 if (!band) {
-                } else {
-                    for (int hh = 0; hh < 2; ++hh) {
-                        tc::tma_load_3d(kdst + hh * SUB_BYTES, &tk, &bar->kv_full[st], hh * 64, h, (int)(s * T + kb0));
-                        tc::tma_load_3d(vdst + hh * SUB_BYTES, &tv, &bar->kv_full[st], hh * 64, h, (int)(s * T + kb0));
-                    }
+                    if (lane < 2 * ppb)
+                        tc::tma_load_3d(dst + (lane & 1) * SUB_BYTES + (lane >> 1) * ps * 128, &tpool, full,
+                                        (lane & 1) * 64, 0, 2 * pg + kv);
+                } else if (lane < 2) {
+                    tc::tma_load_3d(dst + lane * SUB_BYTES, kv ? &tv : &tk, full, lane * 64, h, (int)(s * T + kb0));
                 }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == WARP_MMA) {
         // ================================ MMA issuer =============================
         if (lane == 0) {
             constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
@@ -248,58 +235,69 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                (acc || kk > 0) ? 1u : 0u);
             };
             tc::mbar_wait(&bar->q_ready, 0);
-            tc::mbar_wait(&bar->kv_full[0], 0);
+            tc::mbar_wait(&bar->k_full[0], 0);
             tc::fence_after_sync();
             for (int t = 0; t < NT; ++t) {
                 issue_S(t, 0);
                 tc::mma_commit(&bar->s_full[t]);
             }
+            tc::mma_commit(&bar->k_empty[0]);
             for (int j = 0; j < nblk; ++j) {
                 const int st = j & 1;
                 for (int t = 0; t < NT; ++t) {
                     tc::mbar_wait(&bar->p_full[t], j & 1);
+                    if (t == 0) tc::mbar_wait(&bar->v_full[st], (j >> 1) & 1);
                     tc::fence_after_sync();
                     issue_PV(t, st, j > 0);
                     if (j == nblk - 1) tc::mma_commit(&bar->o_final[t]);
-                    if (t == NT - 1) tc::mma_commit(&bar->kv_empty[st]);
+                    if (t == NT - 1) tc::mma_commit(&bar->v_empty[st]);
                     if (j + 1 < nblk) {
+                        const int sn = (j + 1) & 1;
                         if (t == 0) {
-                            tc::mbar_wait(&bar->kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                            tc::mbar_wait(&bar->k_full[sn], ((j + 1) >> 1) & 1);
                             tc::fence_after_sync();
                         }
-                        issue_S(t, (j + 1) & 1);
+                        issue_S(t, sn);
                         tc::mma_commit(&bar->s_full[t]);
+                        if (t == NT - 1) tc::mma_commit(&bar->k_empty[sn]);
                     }
                 }
             }
         }
         __syncwarp();
-    } else if (warp < 8) {
+    } else {
         // ================================ softmax ================================
-        const int t = warp >> 2;
-        const int r = (warp & 3) * 32 + lane;  // row inside the tile == TMEM lane
+        // warp = (tile t, column half c, lane quarter wq): rows r of tile t,
+        // S/P/O columns [HC*c, HC*c + HC).  The two halves of a row exchange
+        // their row max through smem (named barrier per row quarter).
+        const int t = warp >> 3, c = (warp >> 2) & 1, wq = warp & 3;
+        const int r = wq * 32 + lane;  // row inside the tile == TMEM lane
         const long i = i0 + r;
-        const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint32_t colO = 256 * t, colS = 256 * t + 128;
-        // RoPE(q) in place (engine.cpp:229), pre-scaled by log2(e)/sqrt(d)
+        const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
+        const uint32_t colO = 256 * t + HC * c, colS = 256 * t + 128;
+        const uint32_t barid = 1 + t * 4 + wq;
+        float* xm = reinterpret_cast<float*>(sm + OFF_X) + t * NSPLIT * 128;
+        auto pair_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(NSPLIT * 32) : "memory"); };
+        // RoPE(q) in place (engine.cpp:229), pre-scaled by log2(e)/sqrt(d); half c
+        // rotates the d-columns of SW128 sub-tile c
         tc::mbar_wait(&bar->q_full, 0);
         {
             const float qs = rsqrtf(128.f) * LOG2E;
             uint8_t* qt = sm + OFF_Q + t * TILE_BYTES;
-            for (int hh = 0; hh < 2; ++hh)
-                for (int c = 0; c < 8; ++c) {
-                    uint4* p = reinterpret_cast<uint4*>(qt + hh * SUB_BYTES + tc::sw128_off(r, c));
-                    uint4 v = *p;
-                    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            const int hh = c;
+            for (int cc = 0; cc < 8; ++cc) {
+                uint4* p = reinterpret_cast<uint4*>(qt + hh * SUB_BYTES + tc::sw128_off(r, cc));
+                uint4 v = *p;
+                uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float x0 = __uint_as_float(w[u] << 16), x1 = __uint_as_float(w[u] & 0xffff0000u);
-                        float cs, sn;
-                        rope_cs_fast(a.freq, hh * 32 + c * 4 + u, i, cs, sn);
-                        w[u] = tc::pack_bf16x2((x0 * cs - x1 * sn) * qs, (x0 * sn + x1 * cs) * qs);
-                    }
-                    *p = make_uint4(w[0], w[1], w[2], w[3]);
+                for (int u = 0; u < 4; ++u) {
+                    const float x0 = __uint_as_float(w[u] << 16), x1 = __uint_as_float(w[u] & 0xffff0000u);
+                    float cs, sn;
+                    rope_cs_fast(a.freq, hh * 32 + cc * 4 + u, i, cs, sn);
+                    w[u] = tc::pack_bf16x2((x0 * cs - x1 * sn) * qs, (x0 * sn + x1 * cs) * qs);
                 }
+                *p = make_uint4(w[0], w[1], w[2], w[3]);
+            }
         }
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&bar->q_ready);
@@ -308,12 +306,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int j = 0; j < nblk; ++j) {
             tc::mbar_wait(&bar->s_full[t], j & 1);
             tc::fence_after_sync();
-            // S row -> registers (four named 32-column chunks keep it in registers)
-            uint32_t s0[32], s1[32], s2[32], s3[32];
-            tc::tmem_ld32(trow + colS, s0);
-            tc::tmem_ld32(trow + colS + 32, s1);
-            tc::tmem_ld32(trow + colS + 64, s2);
-            tc::tmem_ld32(trow + colS + 96, s3);
+#ifdef WGKV_DBG_NO_SOFTMAX  // diagnostic: MMA/TMA pipeline speed with the softmax removed
+            tc::fence_before_sync();
+            tc::mbar_arrive(&bar->p_full[t]);
+            continue;
+#endif
+            uint32_t s0[32], s1[32];
+            tc::tmem_ld32(trow + colS + HC * c, s0);
+            tc::tmem_ld32(trow + colS + HC * c + 32, s1);
             tc::tmem_ld_wait();
             const uint32_t NEG_INF = 0xff800000u;
             // ---- masks -------------------------------------------------------
@@ -325,32 +325,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         for (int e = 0; e < 32; ++e)
                             if (base + e >= vc) x[e] = NEG_INF;
                     };
-                    cut(s0, 0);
-                    cut(s1, 32);
-                    cut(s2, 64);
-                    cut(s3, 96);
+                    cut(s0, HC * c);
+                    cut(s1, HC * c + 32);
                 }
             } else {
                 const long kb0 = s_lo + 128L * (j - nv);
                 if (!(kb0 + 127 <= i0 && i0 + 127 - kb0 < W)) {
-                    tc::mbar_wait(&bar->kv_full[j & 1], (j >> 1) & 1);
-                    const long dd = i - kb0;  // key c is causal iff c <= dd; in-window iff dd - c < W
+                    // admitted-key masks of this tile's 64 columns (edge tiles only)
+                    const long kc = kb0 + 64 * c + lane;
+                    const uint32_t mk0 = __ballot_sync(0xffffffffu, kc < T && bits[kc] != 0);
+                    const uint32_t mk1 = __ballot_sync(0xffffffffu, kc + 32 < T && bits[kc + 32] != 0);
+                    const long dd = i - kb0;  // key col is causal iff col <= dd; in-window iff dd - col < W
                     auto cut = [&](uint32_t(&x)[32], int w) {
-                        const uint32_t mw = bar->mask[j & 1][w];
+                        const uint32_t mw = (w & 1) ? mk1 : mk0;
 #pragma unroll
                         for (int e = 0; e < 32; ++e) {
-                            const long c = 32 * w + e;
-                            const bool ok = c <= dd && ((dd - c) < W || ((mw >> e) & 1u));
+                            const long col = 32 * w + e;
+                            const bool ok = col <= dd && ((dd - col) < W || ((mw >> e) & 1u));
                             if (!ok) x[e] = NEG_INF;
                         }
                     };
-                    cut(s0, 0);
-                    cut(s1, 1);
-                    cut(s2, 2);
-                    cut(s3, 3);
+                    cut(s0, 2 * c);
+                    cut(s1, 2 * c + 1);
                 }
             }
-            // row max: 8 independent partial maxima keep the dependency chain short
             float pm[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
             auto rmax = [&](const uint32_t(&x)[32]) {
 #pragma unroll
@@ -358,11 +356,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             };
             rmax(s0);
             rmax(s1);
-            rmax(s2);
-            rmax(s3);
-            const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                                   fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+            float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+            // both halves hold their S in registers past this barrier, so the
+            // P stores below may overwrite any S column
+            xm[c * 128 + r] = mx;
+            pair_sync();
+            mx = fmaxf(mx, xm[(c ^ 1) * 128 + r]);
             // ---- lazy rescale: only when the max grows by more than 2^8 -----
+            // (both halves see the same m and mx, so they take the same branch)
             const bool rescale = __any_sync(0xffffffffu, mx > m + 8.f);
             float alpha = 1.f;
             if (rescale) {
@@ -376,69 +378,66 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // instruction count; 4 independent float2 partial sums
             float2 lsv[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
             const float2 nmu = make_float2(-mu, -mu);
-            uint32_t pa[32], pb[32];
-            auto expo = [&](const uint32_t(&x)[32], uint32_t(&dst)[32], int off) {
+            uint32_t pa[32];
+            auto expo = [&](const uint32_t(&x)[32], int off) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const float2 xd = __fadd2_rn(make_float2(__uint_as_float(x[2 * e]), __uint_as_float(x[2 * e + 1])), nmu);
-                    const float x0 = xd.x, x1 = xd.y;
-#if WGKV_EXP_BF16X2
-                    // one packed XU op yields both P values in MMA format; the
-                    // row sum uses exactly the bf16 values the MMA consumes
-                    const uint32_t pp = ex2_bf16x2(tc::pack_bf16x2(x0, x1));
-                    lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u)));
-                    dst[off + e] = pp;
-                    continue;
-#endif
                     // every k-th pair on the FMA pipe, the rest on the MUFU
                     const bool emu = WGKV_EMU_EVERY > 0 && (e % (WGKV_EMU_EVERY > 0 ? WGKV_EMU_EVERY : 1)) ==
                                                                WGKV_EMU_EVERY - 1;
-                    const float e0 = emu ? ex2_emu(x0) : ex2(x0);
-                    const float e1 = emu ? ex2_emu(x1) : ex2(x1);
+                    const float e0 = emu ? ex2_emu(xd.x) : ex2(xd.x);
+                    const float e1 = emu ? ex2_emu(xd.y) : ex2(xd.y);
                     lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(e0, e1));
-                    dst[off + e] = WGKV_PACK_ALU ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
+                    pa[off + e] = WGKV_PACK_ALU ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
                 }
             };
-            expo(s0, pa, 0);
-            expo(s1, pa, 16);
-            expo(s2, pb, 0);
-            expo(s3, pb, 16);
+            expo(s0, 0);
+            expo(s1, 16);
             {
                 const float2 a01 = __fadd2_rn(lsv[0], lsv[1]), a23 = __fadd2_rn(lsv[2], lsv[3]);
-                const float2 t = __fadd2_rn(a01, a23);
-                l += t.x + t.y;
+                const float2 tt = __fadd2_rn(a01, a23);
+                l += tt.x + tt.y;
             }
-            tc::tmem_st32(trow + colS, pa);
-            tc::tmem_st32(trow + colS + 32, pb);
+            // P (bf16x2) of keys [HC*c, HC*c + HC) -> packed columns [HC/2*c, ...)
+            tc::tmem_st32(trow + colS + (HC / 2) * c, pa);
             // O_t is complete up to PV(j-1) (s_full(j) was committed after it);
             // PV(j) waits for p_full below, so the rescale lands in between
             if (rescale && j > 0) {
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
+                for (int k = 0; k < HC / 32; ++k) {
                     uint32_t o[32];
-                    tc::tmem_ld32(trow + colO + 32 * c, o);
+                    tc::tmem_ld32(trow + colO + 32 * k, o);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tc::tmem_st32(trow + colO + 32 * c, o);
+                    for (int e = 0; e < 32; e += 2) {
+                        const float2 v = __fmul2_rn(make_float2(__uint_as_float(o[e]), __uint_as_float(o[e + 1])),
+                                                    make_float2(alpha, alpha));
+                        o[e] = __float_as_uint(v.x);
+                        o[e + 1] = __float_as_uint(v.y);
+                    }
+                    tc::tmem_st32(trow + colO + 32 * k, o);
                 }
             }
             tc::tmem_st_wait();
             tc::fence_before_sync();
             tc::mbar_arrive(&bar->p_full[t]);
         }
-        // ---- epilogue: O / l -> bf16 ------------------------------------------
+        // ---- epilogue: O / l -> bf16 (row sum = both halves) -------------------
         tc::mbar_wait(&bar->o_final[t], 0);
         tc::fence_after_sync();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* orow = out + (((size_t)s * T + i) * Hq + p0 + t) * 128;
+        xm[c * 128 + r] = l;
+        pair_sync();
+        const float lt = l + xm[(c ^ 1) * 128 + r];
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        __nv_bfloat16* orow = out + (((size_t)s * T + i) * Hq + p0 + t) * 128 + HC * c;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int k = 0; k < HC / 32; ++k) {
             uint32_t o[32];
-            tc::tmem_ld32(trow + colO + 32 * c, o);
+            tc::tmem_ld32(trow + colO + 32 * k, o);
             tc::tmem_ld_wait();
             if (i < T) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+                uint4* dst = reinterpret_cast<uint4*>(orow + 32 * k);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4)
                     dst[q4] = make_uint4(tc::pack_bf16x2(__uint_as_float(o[8 * q4]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
@@ -450,7 +449,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == WARP_MMA) {
         tc::fence_after_sync();
         tc::tmem_dealloc(tmem, 512);
     }
