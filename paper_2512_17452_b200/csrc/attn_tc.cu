@@ -9,17 +9,24 @@
 //              place from the pages K2 filled, one TMA per page half)
 //   band     : keys [i0-W+1, i0+127] of k_post / v (TMA tiles), with per
 //              element masks only on the <= 2 edge tiles
-// (SURVEY.md App. A.9).  Warp roles, 384 threads, 1 CTA / SM:
-//   warps 0-3 / 4-7 : softmax for tile 0 / 1 (one TMEM lane = one row each):
-//                     RoPE(q) in smem, then per key tile tcgen05.ld S, mask,
-//                     online softmax (lazy rescale, threshold 2^8), P as bf16
-//                     written back into TMEM over S, O rescale in TMEM
-//   warp 8          : TMA producer (Q once, K/V double-buffered ring)
-//   warp 9          : TMEM allocator + single-thread MMA issuer (warps 10-11 idle;
-//                     warpgroup 2 runs at 40 registers, the softmax ones at 232):
-//                     S_t = Q_t K^T (SS, K-major x K-major, M=N=128, K=128)
-//                     O_t += P_t V  (TS: P from TMEM, V MN-major from smem)
+// (SURVEY.md App. A.9).  Warp roles, 19 warps (608 threads), 1 CTA / SM:
+//   warps 0-15 : softmax; warp = (tile t, column half c, lane quarter wq)
+//                owns rows 32wq..32wq+31 (its TMEM lane quarter) and S/P/O
+//                columns [64c, 64c+64) of tile t: RoPE(q) in smem, then per key
+//                block tcgen05.ld S, mask, row max exchanged with the other
+//                half through smem (named barrier), online softmax (lazy
+//                rescale, threshold 2^8; 1/4 of the exp2 on the FMA pipe, bf16
+//                packing on the ALU so the MUFU only does exp2), P as bf16x2
+//                written back into TMEM over S, O rescale in TMEM
+//   warp 16/17 : TMA producers for K / V (Q once), 2-stage ring each with its
+//                own full/empty barriers
+//   warp 18    : TMEM allocator + single-thread MMA issuer, tiles in turn:
+//                S_t = Q_t K^T (SS, K-major x K-major, M=N=128, K=128)
+//                O_t += P_t V  (TS: P from TMEM, V MN-major from smem)
 // TMEM: tile t owns O_t = cols [256t, 256t+128) and S_t/P_t = [256t+128, 256t+256).
+// Measured alternatives (profiles/r1_k3_notes.md): one head per CTA with a
+// double-buffered S (smem/TMA-bound, -20 %), one MMA issuer per tile (the
+// two softmax groups fall into phase and contend for the MUFU, -16 %).
 #include <cuda.h>
 
 #include <cstdio>
@@ -42,10 +49,10 @@ constexpr uint32_t OFF_BAR = OFF_KV + NSTAGE * STAGE_BYTES;
 constexpr int NSPLIT = 2;                   // softmax warpgroups per tile (column halves)
 constexpr int HC = 128 / NSPLIT;            // S columns per softmax thread
 constexpr int NSOFT = NT * NSPLIT * 4;      // softmax warps
-constexpr int WARP_TMA = NSOFT, WARP_MMA = NSOFT + 1;
+constexpr int WARP_TMA = NSOFT, WARP_MMA = NSOFT + 2;  // K producer, V producer, MMA issuer
 constexpr uint32_t OFF_X = OFF_BAR + 512;   // [NT][NSPLIT][128] f32 row-max / row-sum exchange
 constexpr uint32_t SMEM_BYTES = OFF_X + NT * NSPLIT * 128 * 4 + 1024;  // + alignment slack
-constexpr int NTHREADS = (NSOFT + 2) * 32;
+constexpr int NTHREADS = (NSOFT + 3) * 32;
 constexpr float LOG2E = 1.4426950408889634f;
 
 struct Bars {
@@ -63,40 +70,36 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 #ifndef WGKV_PACK_ALU
-#define WGKV_PACK_ALU 0  // measured: PRMT packing is 2 % slower than F2FP on B200
+#define WGKV_PACK_ALU 1  // F2FP shares the MUFU pipe on B200 (tools/ubench_mufu.cu); PRMT packing: -3.5 % K3 time
 #endif
-#ifndef WGKV_EXP_BF16X2
-#define WGKV_EXP_BF16X2 0
-#endif
-__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
-    uint32_t y;
-    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
-}
 // fp32 pair -> bf16x2 on the ALU pipe (two IADD + one PRMT) instead of F2FP,
-// which shares the XU pipe with MUFU.EX2 and made the softmax XU-bound.
+// which competes with MUFU.EX2 for the same pipe on B200.
 // Round-half-up on the (finite, non-negative) P values.
 __device__ __forceinline__ uint32_t pack_bf16x2_alu(float lo, float hi) {
     return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
 }
-#ifndef WGKV_EMU_EVERY
-#define WGKV_EMU_EVERY 0  // every k-th exp2 pair is emulated (0 = all on the MUFU; measured
-                          // best on B200: 1/8 -> -5 %, 1/4 -> -9 %, 1/2 -> -13 % K3 throughput)
+#ifndef WGKV_EMU_MASK
+#define WGKV_EMU_MASK 0x8888  // bit e set: exp2 pair e of each 32-column chunk runs on the FMA pipe
+                              // (measured with packing on the ALU: 1/4 -> -0.7 %, 5/16 +1 %, 1/2 +7 %)
 #endif
-// 2^x on the FMA/ALU pipes (offloads the MUFU, which otherwise paces the
-// softmax): Cody-Waite split x = n + f, f in [-1/2, 1/2] via the 1.5*2^23
-// rounding trick, cubic near-minimax for 2^f (max rel. error 7.5e-5, far
-// below the bf16 rounding of P), exponent add for 2^n.  x <= -126 -> 0.
-__device__ __forceinline__ float ex2_emu(float x) {
-    const float xc = fmaxf(x, -126.f);
-    const float t = xc + 12582912.f;
-    const float f = xc - (t - 12582912.f);
-    float p = fmaf(f, 0.05517161f, 0.24261111f);
-    p = fmaf(p, f, 0.69326097f);
-    p = fmaf(p, f, 0.99992806f);
-    const int n = __float_as_int(t) - 0x4B400000;
-    const float r = __int_as_float(__float_as_int(p) + (n << 23));
-    return x < -126.f ? 0.f : r;
+// 2^x for a pair on the FMA/ALU pipes (offloads the MUFU, which otherwise
+// paces the softmax), packed f32x2 arithmetic: Cody-Waite split x = n + f with
+// f in [-1/2, 1/2] via the 1.5*2^23 rounding trick, cubic near-minimax for
+// 2^f (max rel. error 7.5e-5, far below the bf16 rounding of P), exponent
+// add for 2^n.  x is clamped at -127.5, where the exponent field goes negative
+// and the integer max returns exactly +0 (so masked -inf keys give P = 0).
+__device__ __forceinline__ float2 ex2_emu2(float x0, float x1) {
+    const float2 xc = make_float2(fmaxf(x0, -127.5f), fmaxf(x1, -127.5f));
+    const float2 big = make_float2(12582912.f, 12582912.f);
+    const float2 t = __fadd2_rn(xc, big);
+    const float2 tb = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(tb, make_float2(-1.f, -1.f), xc);
+    float2 p = __ffma2_rn(f, make_float2(0.05517161f, 0.05517161f), make_float2(0.24261111f, 0.24261111f));
+    p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+    p = __ffma2_rn(p, f, make_float2(0.99992806f, 0.99992806f));
+    const int r0 = max(__float_as_int(p.x) + (__float_as_int(t.x) << 23), 0);
+    const int r1 = max(__float_as_int(p.y) + (__float_as_int(t.y) << 23), 0);
+    return make_float2(__int_as_float(r0), __int_as_float(r1));
 }
 
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_saddr, int kk) {
@@ -106,6 +109,17 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_saddr, int kk) {
 
 }  // namespace
 
+#ifdef WGKV_TRACE  // diagnostic build only: per-block event clocks of CTA (0,0,0)
+__device__ unsigned long long g_k3_trace[4][4096][8];
+#define K3_TR(who, j, ev)                                                                          \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 4096) g_k3_trace[who][j][ev] = clock64(); \
+    } while (0)
+#else
+#define K3_TR(who, j, ev) \
+    do {                  \
+    } while (0)
+#endif
 __global__ void __launch_bounds__(NTHREADS, 1)
     vs_prefill_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                          const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tpool, VsArgs a,
@@ -165,9 +179,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int nblk = nv + nb;
     const int ps = a.pv.page_size;
 
-    if (warp == WARP_TMA) {
-        // ================================ TMA producer ===========================
-        if (lane == 0) {
+    if (warp == WARP_TMA || warp == WARP_TMA + 1) {
+        // ============================ TMA producers ===========================
+        // one warp for K, one for V: each runs ahead by the ring depth on its
+        // own (one in-order producer holds K(j+1) behind the release of
+        // V(j+1-NSTAGE), which comes a whole PV later)
+        const int kv = warp - WARP_TMA;
+        if (lane == 0 && kv == 0) {
             tc::tma_prefetch(&tq);
             tc::tma_prefetch(&tk);
             tc::tma_prefetch(&tv);
@@ -199,9 +217,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const long kb0 = band ? s_lo + 128L * (j - nv) : 0;
             // vertical copy `lane` = (page lane/2, dim half lane%2), 2*ppb <= 32
             const int pg = __shfl_sync(0xffffffffu, cur_ids, lane >> 1);
-            for (int kv = 0; kv < 2; ++kv) {
+            {
                 uint64_t* full = kv ? &bar->v_full[st] : &bar->k_full[st];
                 if (j >= NSTAGE) tc::mbar_wait(kv ? &bar->v_empty[st] : &bar->k_empty[st], ((j - NSTAGE) >> 1) & 1);
+                if (lane == 0) K3_TR(3, j, kv);
                 uint8_t* dst = sm + OFF_KV + st * STAGE_BYTES + kv * TILE_BYTES;
                 if (lane == 0) tc::mbar_arrive_expect_tx(full, TILE_BYTES);
                 __syncwarp();
@@ -246,7 +265,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int st = j & 1;
                 for (int t = 0; t < NT; ++t) {
                     tc::mbar_wait(&bar->p_full[t], j & 1);
+                    K3_TR(2, j, 3 * t);
                     if (t == 0) tc::mbar_wait(&bar->v_full[st], (j >> 1) & 1);
+                    K3_TR(2, j, 3 * t + 1);
                     tc::fence_after_sync();
                     issue_PV(t, st, j > 0);
                     if (j == nblk - 1) tc::mma_commit(&bar->o_final[t]);
@@ -259,6 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                         issue_S(t, sn);
                         tc::mma_commit(&bar->s_full[t]);
+                        K3_TR(2, j, 3 * t + 2);
                         if (t == NT - 1) tc::mma_commit(&bar->k_empty[sn]);
                     }
                 }
@@ -306,6 +328,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int j = 0; j < nblk; ++j) {
             tc::mbar_wait(&bar->s_full[t], j & 1);
             tc::fence_after_sync();
+            if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 0);
 #ifdef WGKV_DBG_NO_SOFTMAX  // diagnostic: MMA/TMA pipeline speed with the softmax removed
             tc::fence_before_sync();
             tc::mbar_arrive(&bar->p_full[t]);
@@ -360,9 +383,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                              fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
             // both halves hold their S in registers past this barrier, so the
             // P stores below may overwrite any S column
+            if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 1);
             xm[c * 128 + r] = mx;
             pair_sync();
             mx = fmaxf(mx, xm[(c ^ 1) * 128 + r]);
+            if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 2);
             // ---- lazy rescale: only when the max grows by more than 2^8 -----
             // (both halves see the same m and mx, so they take the same branch)
             const bool rescale = __any_sync(0xffffffffu, mx > m + 8.f);
@@ -383,11 +408,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     const float2 xd = __fadd2_rn(make_float2(__uint_as_float(x[2 * e]), __uint_as_float(x[2 * e + 1])), nmu);
-                    // every k-th pair on the FMA pipe, the rest on the MUFU
-                    const bool emu = WGKV_EMU_EVERY > 0 && (e % (WGKV_EMU_EVERY > 0 ? WGKV_EMU_EVERY : 1)) ==
-                                                               WGKV_EMU_EVERY - 1;
-                    const float e0 = emu ? ex2_emu(xd.x) : ex2(xd.x);
-                    const float e1 = emu ? ex2_emu(xd.y) : ex2(xd.y);
+                    // selected pairs on the FMA pipe, the rest on the MUFU
+                    float e0, e1;
+                    if ((WGKV_EMU_MASK >> e) & 1) {
+                        const float2 ee = ex2_emu2(xd.x, xd.y);
+                        e0 = ee.x;
+                        e1 = ee.y;
+                    } else {
+                        e0 = ex2(xd.x);
+                        e1 = ex2(xd.y);
+                    }
                     lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(e0, e1));
                     pa[off + e] = WGKV_PACK_ALU ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
                 }
@@ -399,6 +429,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float2 tt = __fadd2_rn(a01, a23);
                 l += tt.x + tt.y;
             }
+            if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 3);
             // P (bf16x2) of keys [HC*c, HC*c + HC) -> packed columns [HC/2*c, ...)
             tc::tmem_st32(trow + colS + (HC / 2) * c, pa);
             // O_t is complete up to PV(j-1) (s_full(j) was committed after it);
@@ -422,6 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::tmem_st_wait();
             tc::fence_before_sync();
             tc::mbar_arrive(&bar->p_full[t]);
+            if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 4);
         }
         // ---- epilogue: O / l -> bf16 (row sum = both halves) -------------------
         tc::mbar_wait(&bar->o_final[t], 0);
@@ -481,6 +513,12 @@ int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t 
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? WGKV_OK : WGKV_ECUDA;
 }
+
+#ifdef WGKV_TRACE
+extern "C" int wgkv_dbg_k3_trace(void* host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, g_k3_trace, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int launch_vs_prefill_tc(const VsArgs& a, int nseq, const __nv_bfloat16* q, const __nv_bfloat16* k_post,
                          const __nv_bfloat16* v, __nv_bfloat16* out, cudaStream_t st) {

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--batch", type=int, default=4)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--window", type=int, default=1024)
+    ap.add_argument("--trace", default="", help="diagnostic K3 build (-DWGKV_TRACE): dump CTA (0,0,0) event clocks")
     args = ap.parse_args()
     B, T, Hq, Hkv, d, Wn = args.batch, args.T, 32, 8, 128, args.window
     dev = torch.device("cuda", 0)
@@ -67,6 +68,11 @@ def main():
             tk3 += ev[2].elapsed_time(ev[3]) / args.reps
         st = s.stats(0, B)
         s.release(0, B)
+    if args.trace:
+        buf = np.zeros((4, 4096, 8), np.uint64)
+        fn = lib.wgkv_dbg_k3_trace1 if os.environ.get("WGKV_TRACE_V1") else lib.wgkv_dbg_k3_trace
+        check(fn(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes)))
+        np.save(args.trace, buf)
     ii = torch.arange(T, device=dev)
     band = torch.clamp(ii + 1, max=Wn).sum()
     pairs = int((band + torch.cumsum(bits[..., : T - Wn].long(), -1).sum(-1)).sum().item()) * (Hq // Hkv)
