@@ -313,36 +313,56 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
     }
 }
 
-// merge chunk partials of one (seq, q head): out = sum e^(m_c-M) o_c / sum e^(m_c-M) l_c
+// merge chunk partials of one (seq, q head): out = sum e^(m_c-M) o_c / sum e^(m_c-M) l_c.
+// Warp 0 loads every chunk's (m, l) at once and reduces them with shuffles;
+// the weights go through smem, then each thread sums one output column with
+// independent loads (no serial load chains: this kernel is latency-bound).
 template <typename E>
 __global__ void decode_combine_kernel(DecArgs a, const float* __restrict__ part, E* __restrict__ out) {
+    constexpr int MAXC = 64;  // >= DecArgs::max_chunks (api.cu)
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
     const int sp = blockIdx.x, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
     const int bh = s * a.pv.kv_heads + h;
     const size_t pstride = (size_t)gs * (d + 2);
     const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
-    __shared__ float M, invL;
+    __shared__ float w[MAXC];
+    __shared__ float invL;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // partials of the attention kernel (PDL)
-    const int nch = a.nchunks ? a.nchunks[bh] : a.n_chunks;
-    if (threadIdx.x == 0) {
-        float mx = -INFINITY;
-        for (int c = 0; c < nch; ++c) mx = fmaxf(mx, base[(size_t)c * pstride + d]);
-        float L = 0.f;
-        for (int c = 0; c < nch; ++c) {
-            const float mc = base[(size_t)c * pstride + d];
-            if (mc != -INFINITY) L += __expf(mc - mx) * base[(size_t)c * pstride + d + 1];
+    const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, MAXC);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        float mc[2], lc[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int c = lane + 32 * k;
+            mc[k] = c < nch ? base[(size_t)c * pstride + d] : -INFINITY;
+            lc[k] = c < nch ? base[(size_t)c * pstride + d + 1] : 0.f;
         }
-        M = mx;
-        invL = 1.f / L;
+        float M = fmaxf(mc[0], mc[1]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        float L = 0.f;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int c = lane + 32 * k;
+            const float wc = mc[k] == -INFINITY ? 0.f : __expf(mc[k] - M);
+            if (c < MAXC) w[c] = wc;
+            L += wc * lc[k];
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        if (lane == 0) invL = 1.f / L;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < d; e += blockDim.x) {
-        float acc = 0.f;
-        for (int c = 0; c < nch; ++c) {
-            const float mc = base[(size_t)c * pstride + d];
-            if (mc != -INFINITY) acc += __expf(mc - M) * base[(size_t)c * pstride + e];
+        float acc0 = 0.f, acc1 = 0.f;
+        int c = 0;
+        for (; c + 1 < nch; c += 2) {
+            acc0 += w[c] * base[(size_t)c * pstride + e];
+            acc1 += w[c + 1] * base[(size_t)(c + 1) * pstride + e];
         }
-        out[((size_t)s * a.q_heads + p) * d + e] = from_f<E>(acc * invL);
+        if (c < nch) acc0 += w[c] * base[(size_t)c * pstride + e];
+        out[((size_t)s * a.q_heads + p) * d + e] = from_f<E>((acc0 + acc1) * invL);
     }
 }
 
