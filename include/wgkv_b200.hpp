@@ -15,8 +15,11 @@
 // (SURVEY.md §5).  All tensors are device pointers (see wgkv_b200.h).
 #pragma once
 
+#include <cmath>
+#include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "wgkv_b200.h"
 
@@ -93,6 +96,79 @@ public:
 private:
     wgkv_ctx* ctx_ = nullptr;
 };
+
+
+// ---------------------------------------------------------------------------
+// PolicyConfig / ForcedAdmission (engine.hpp:17-40) and Session::effective_gate
+// (engine.cpp:126-151): the policy override of the MLP gate.  The device path
+// takes it as the optional forced_g buffer of wgkv_gate_score /
+// wgkv_prefill_layer / wgkv_decode_step_kv / wgkv_decode_layer (nullptr = the
+// MLP decides); policy_gates() fills that buffer on the host.
+// ---------------------------------------------------------------------------
+enum class PolicyKind { full, wgkv, local_sink, static_heads, wgkv_plus_topk };
+
+struct ForcedAdmission {
+    enum class Mode { none, stride, recent_fraction };
+    Mode mode = Mode::none;
+    long keep_every = 4;     // stride: admit positions with pos % keep_every == phase
+    long phase = 0;
+    double fraction = 0.25;  // recent_fraction: admit the newest fraction of pre-window prompt positions
+};
+
+struct Policy {
+    PolicyKind kind = PolicyKind::wgkv;
+    long window = 256;
+    long sink = 128;
+    std::vector<uint8_t> retrieval_bitmap;  // static_heads: layers * kv_heads entries
+    long topk_budget = 0;                   // wgkv_plus_topk (wgkv_config::topk_budget)
+    ForcedAdmission forced;
+};
+
+// true when the gate MLP decides (engine.cpp:203): pass forced_g = nullptr
+inline bool uses_mlp_gates(const Policy& p) {
+    return (p.kind == PolicyKind::wgkv || p.kind == PolicyKind::wgkv_plus_topk) &&
+           p.forced.mode == ForcedAdmission::Mode::none;
+}
+
+// effective gate of (layer, global kv head, position) when the MLP does not decide
+inline double effective_gate(const Policy& p, int layer, int head, int kv_heads, long position, long prompt_len) {
+    switch (p.kind) {
+        case PolicyKind::full: return 1.0;
+        case PolicyKind::local_sink: return position < p.sink ? 1.0 : 0.0;
+        case PolicyKind::static_heads:
+            return p.retrieval_bitmap.at(static_cast<size_t>(layer) * kv_heads + head) ? 1.0 : 0.0;
+        case PolicyKind::wgkv:
+        case PolicyKind::wgkv_plus_topk:
+            switch (p.forced.mode) {
+                case ForcedAdmission::Mode::none: break;
+                case ForcedAdmission::Mode::stride:
+                    return position % p.forced.keep_every == p.forced.phase ? 1.0 : 0.0;
+                case ForcedAdmission::Mode::recent_fraction: {
+                    const long pre_window = prompt_len - p.window > 0 ? prompt_len - p.window : 0;
+                    const long cutoff = pre_window - static_cast<long>(std::llround(p.forced.fraction * pre_window));
+                    return position >= cutoff ? 1.0 : 0.0;
+                }
+            }
+    }
+    throw std::logic_error("effective_gate: the gate MLP decides under this policy");
+}
+
+// forced_g for positions [pos0, pos0 + T) of nseq sequences and the local kv
+// heads [kv_head_offset, kv_head_offset + kv_heads_local) of kv_heads_total:
+// out = [nseq][kv_heads_local][T] (copy it to the device).  Returns false
+// (and leaves out empty) when the MLP decides.
+inline bool policy_gates(const Policy& p, int layer, int kv_head_offset, int kv_heads_local, int kv_heads_total,
+                         int nseq, long pos0, long T, long prompt_len, std::vector<float>& out) {
+    out.clear();
+    if (uses_mlp_gates(p)) return false;
+    out.resize(static_cast<size_t>(nseq) * kv_heads_local * T);
+    for (int s = 0; s < nseq; ++s)
+        for (int h = 0; h < kv_heads_local; ++h)
+            for (long t = 0; t < T; ++t)
+                out[(static_cast<size_t>(s) * kv_heads_local + h) * T + t] = static_cast<float>(
+                    effective_gate(p, layer, kv_head_offset + h, kv_heads_total, pos0 + t, prompt_len));
+    return true;
+}
 
 }  // namespace b200
 }  // namespace wgkv

@@ -251,9 +251,23 @@ class Ref(_Base):
         L.wr_session_select_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_long, _lp, _lp]
         L.wr_gate_save.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.wr_thread_budget.restype = C.c_int
+        L.wr_policy_trace.argtypes = [C.c_int, C.c_long, C.c_long, _u8p, C.c_int, C.c_long, C.c_long, C.c_double,
+                                      C.c_int, C.c_int, C.c_long, C.c_int, _dp]
 
     def thread_budget(self) -> int:
         return int(self.lib.wr_thread_budget())
+
+    def policy_trace(self, kind: int, window: int, sink: int, bitmap, fmode: int, keep_every: int, phase: int,
+                     fraction: float, L: int, H: int, T: int, n_decode: int) -> np.ndarray:
+        """GateTrace gates [L][H][T+n_decode] of a real wgkv::Session under the policy."""
+        out = np.zeros((L, H, T + n_decode))
+        bm = None if bitmap is None else np.ascontiguousarray(bitmap, np.uint8)
+        st = self.lib.wr_policy_trace(kind, window, sink, None if bm is None else bm.ctypes.data_as(_u8p), fmode,
+                                      keep_every, phase, fraction, L, H, T, n_decode,
+                                      out.ctypes.data_as(_dp))
+        if st:
+            raise RuntimeError(f"wr_policy_trace status {st}")
+        return out
 
 
 # ---------------------------------------------------------------------------

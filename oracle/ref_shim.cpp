@@ -410,4 +410,48 @@ int wr_session_select_topk(void* sp, int layer, int h, const double* q, long bud
     }
 }
 
+// Session::effective_gate as the reference applies it (engine.cpp:126-151):
+// a real wgkv::Session over ToyModel::random with the given policy runs
+// prefill(T tokens) + n_decode decode steps; the GateTrace it records
+// (engine.cpp:214-217, 305) is copied out as out_g[L][H][T + n_decode].
+// kind: 0 full, 1 wgkv, 2 local_sink, 3 static_heads, 4 wgkv_plus_topk
+// (PolicyKind order, engine.hpp:17); fmode: 0 none, 1 stride, 2 recent_fraction.
+int wr_policy_trace(int kind, long window, long sink, const uint8_t* bitmap, int fmode, long keep_every, long phase,
+                    double fraction, int L, int H, long T, int n_decode, double* out_g) {
+    try {
+        ModelConfig mc;
+        mc.layers = L;
+        mc.q_heads = H;
+        mc.kv_heads = H;
+        mc.head_dim = 8;
+        mc.mlp_hidden = 16;
+        mc.vocab = 32;
+        const ToyModel model = ToyModel::random(mc, 7);
+        const GateBank gates = GateBank::random_init(L, H, mc.head_dim, mc.head_dim, 11, 0.5, 0.0);
+        PolicyConfig pc;
+        pc.kind = static_cast<PolicyKind>(kind);
+        pc.window = window;
+        pc.sink = sink;
+        if (bitmap) pc.retrieval_bitmap.assign(bitmap, bitmap + static_cast<size_t>(L) * H);
+        pc.forced.mode = static_cast<ForcedAdmission::Mode>(fmode);
+        pc.forced.keep_every = keep_every;
+        pc.forced.phase = phase;
+        pc.forced.fraction = fraction;
+        Session sess(model, gates, pc, T + n_decode);
+        std::vector<int> tokens(static_cast<size_t>(T));
+        for (long t = 0; t < T; ++t) tokens[static_cast<size_t>(t)] = static_cast<int>((t * 7 + 3) % mc.vocab);
+        sess.prefill(tokens);
+        for (int n = 0; n < n_decode; ++n) sess.decode_step((n * 5 + 1) % mc.vocab);
+        const GateTrace& tr = sess.trace();
+        for (int l = 0; l < L; ++l)
+            for (int h = 0; h < H; ++h)
+                for (long t = 0; t < T + n_decode; ++t)
+                    out_g[(static_cast<size_t>(l) * H + h) * (T + n_decode) + t] =
+                        tr.gates[static_cast<size_t>(l)][static_cast<size_t>(h)][static_cast<size_t>(t)];
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
 }  // extern "C"

@@ -197,6 +197,42 @@ def test_forced_full_is_dense_causal(W, orc):
         assert rel_err(out[0, :, p], ref) < 1e-5
 
 
+@pytest.mark.parametrize("kind", ["local_sink", "stride", "recent_fraction"])
+def test_policy_sessions_vs_oracle(W, orc, kind):
+    """Policy overrides (engine.cpp:126-151) through forced gates: prefill +
+    lazy-promotion decode equal the oracle session fed the same gates."""
+    from paper_2512_17452_b200 import policy as P
+    d, hq, hkv, T, steps, Wn = 128, 4, 2, 400, 70, 64
+    pol = {"local_sink": P.Policy(kind="local_sink", window=Wn, sink=37),
+           "stride": P.Policy(kind="wgkv", window=Wn, forced=P.ForcedAdmission("stride", keep_every=3, phase=2)),
+           "recent_fraction": P.Policy(kind="wgkv", window=Wn,
+                                       forced=P.ForcedAdmission("recent_fraction", fraction=0.4))}[kind]
+    q = bf16_np(orc.gaussian(11, (T + steps) * hq * d).reshape(1, T + steps, hq, d))
+    k = bf16_np(orc.gaussian(12, (T + steps) * hkv * d).reshape(1, T + steps, hkv, d))
+    v = bf16_np(orc.gaussian(13, (T + steps) * hkv * d).reshape(1, T + steps, hkv, d))
+    s = W.Session(1, hq, hkv, d, d, Wn, max_tokens=T + steps, dtype=W.BF16)
+    r = O.Session(orc, 1, hq, hkv, d, d, Wn, max_tokens=T + steps)
+    fg = P.policy_gates(pol, 0, 0, hkv, hkv, 1, 0, T, T)
+    out = s.prefill_layer(0, to_dev(q[:, :T], torch.bfloat16), to_dev(k[:, :T], torch.bfloat16),
+                          to_dev(v[:, :T], torch.bfloat16), forced_gates=torch.from_numpy(fg.copy()).cuda())
+    ro, _, rb, _ = r.prefill_layer(0, q[0, :T], k[0, :T], v[0, :T], forced_gates=fg[0])
+    o = out.float().cpu().numpy()[0]
+    for p in range(hq):
+        assert rel_err(o[:, p], ro[:, p]) < TOL["bf16"]
+    for t in range(T, T + steps):
+        fg = P.policy_gates(pol, 0, 0, hkv, hkv, 1, t, 1, T)
+        o, _, ev = s.decode_layer(0, to_dev(q[:, t], torch.bfloat16), to_dev(k[:, t], torch.bfloat16),
+                                  to_dev(v[:, t], torch.bfloat16),
+                                  forced_gates=torch.from_numpy(fg.reshape(1, hkv).copy()).cuda(), want_events=True)
+        ro, _, rev, _ = r.decode_layer(0, q[0, t], k[0, t], v[0, t], forced_gates=fg.reshape(hkv))
+        assert np.array_equal(ev.cpu().numpy()[0], rev)
+        o = o.float().cpu().numpy()[0]
+        for p in range(hq):
+            assert rel_err(o[p], ro[p]) < TOL["bf16"]
+    for h in range(hkv):
+        assert np.array_equal(s.gather(0, 0, h)["global_pos"], r.gather(0, h)["global_pos"])
+
+
 # -------------------------------------------------------------- error paths --
 def test_lifecycle_and_pool_errors(W, orc):
     d = 128
