@@ -25,8 +25,11 @@ def main():
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--admit", type=float, default=0.25)
     ap.add_argument("--impl", type=int, default=0, help="attn_impl (0 auto, 1 simt)")
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--topk", type=int, default=0, help="topk_budget (Global pages per q head; 0 = all)")
     args = ap.parse_args()
-    B, T, Hq, Hkv, d = args.batch, args.T, 32, 8, 128
+    B, T, Hq, Hkv, d = args.batch, args.T, args.hq, args.hkv, 128
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     import numpy as np
@@ -34,7 +37,7 @@ def main():
     bank = np.zeros((1, Hkv, d * 2 * d + 2 * d + 1))
     bank[..., : d * 2 * d] = 0.02 * np.random.default_rng(0).standard_normal((1, Hkv, d * 2 * d))
     s = W.Session(1, Hq, Hkv, d, d, 1024, rope_base=5e5, max_seqs=B, max_tokens=T + 3 * args.iters + 8,
-                  max_prefill_tokens=T, attn_impl=args.impl, gate_bank=bank)
+                  max_prefill_tokens=T, attn_impl=args.impl, gate_bank=bank, topk_budget=args.topk)
     q = torch.randn(B, T, Hq, d, device=dev, generator=g).to(torch.bfloat16)
     k = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
     v = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
@@ -51,6 +54,11 @@ def main():
     lib, h = s.lib, s.h
     st = s.stats(0, B)
     res_bytes = st["resident_entries"] * 2 * d * 2
+    if args.topk:  # K6 reads: every Global K once per group (scoring) + selected K/V per q head + Local K/V
+        n_loc = min(T, 1024)
+        n_glob = (st["resident_entries"] / (B * Hkv)) - n_loc
+        sel = min(args.topk * 16, n_glob)
+        res_bytes = B * Hkv * (n_glob * d * 2 + (Hq // Hkv) * (sel + n_loc) * 2 * d * 2)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     for _ in range(5):
         check(lib.wgkv_decode_attn(h, 0, 0, B, P(qd), P(out)))
@@ -74,7 +82,8 @@ def main():
     t_app_forced = ev[1].elapsed_time(ev[2]) / (args.iters // 2) * 1e3
     t_app_gate = ev[2].elapsed_time(ev[3]) / (args.iters // 2) * 1e3
     s.sync()
-    print(json.dumps({"T": T, "batch": B, "resident_entries": st["resident_entries"],
+    print(json.dumps({"T": T, "batch": B, "hq": Hq, "hkv": Hkv, "topk": args.topk,
+                      "resident_entries": st["resident_entries"],
                       "k5_attn_us": t_attn, "k5_GBps": res_bytes / t_attn / 1e3,
                       "k4_append_forced_us": t_app_forced, "k4_append_fp64_gate_us": t_app_gate,
                       "decode_layer_us": t_layer, "decode_layer_GBps": res_bytes / t_layer / 1e3}))
