@@ -86,9 +86,12 @@ struct wgkv_ctx {
     float* ws_score = nullptr;  // K6: [S][Hq][n_gp] page scores
     int32_t* ws_sel = nullptr;  // K6: [S][Hq][n_gp] selected logical pages
     int32_t* ws_nsel = nullptr; // K6: [S][Hq]
+    unsigned long long* ws_thr = nullptr;  // K6: [S][Hq] selection thresholds
+    uint8_t* ws_umask = nullptr;           // K6: [S][H][n_gp] union q-head masks
+    int* ws_ucnt = nullptr;                // K6: [S][H][ceil(n_gp/1024)] union block counts
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    int max_chunks = 64;
+    int max_chunks = kMaxChunks;
     long near_cap = 0;
     // host mirrors for lifecycle checks and grid sizing
     std::vector<uint8_t> prefilled;  // [L][S]
@@ -206,6 +209,9 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
         ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
         ctx->ws_sel = dalloc<int32_t>((size_t)S * c.q_heads * n_gp, o);
         ctx->ws_nsel = dalloc<int32_t>((size_t)S * c.q_heads, o);
+        ctx->ws_thr = dalloc<unsigned long long>((size_t)S * c.q_heads, o);
+        ctx->ws_umask = dalloc<uint8_t>((size_t)S * H * n_gp, o);
+        ctx->ws_ucnt = dalloc<int>((size_t)S * H * ((n_gp + 1023) / 1024), o);
     }
     for (void* p : o)
         if (!p) {
@@ -538,11 +544,14 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
     if (c.topk_budget > 0) {  // wgkv_plus_topk (engine.cpp:320-324)
         if (c.dtype == WGKV_BF16)
             st = launch_topk_decode<__nv_bfloat16>(a, nseq, c.topk_budget, (const __nv_bfloat16*)q, ctx->ws_score,
-                                                   ctx->ws_sel, ctx->ws_nsel, ctx->ws_part, (__nv_bfloat16*)out,
-                                                   ctx->stream);
+                                                   ctx->ws_sel, ctx->ws_nsel, ctx->ws_thr, ctx->ws_umask,
+                                                   ctx->ws_ucnt, ctx->ws_part,
+                                                   ctx->ws_nchunks, (__nv_bfloat16*)out, ctx->stream);
         else
             st = launch_topk_decode<float>(a, nseq, c.topk_budget, (const float*)q, ctx->ws_score, ctx->ws_sel,
-                                           ctx->ws_nsel, ctx->ws_part, (float*)out, ctx->stream);
+                                           ctx->ws_nsel, ctx->ws_thr, ctx->ws_umask, ctx->ws_ucnt, ctx->ws_part,
+                                           ctx->ws_nchunks, (float*)out,
+                                           ctx->stream);
         if (st) return fail(st, std::string("topk decode: ") + cudaGetErrorString(cudaGetLastError()));
         return WGKV_OK;
     }

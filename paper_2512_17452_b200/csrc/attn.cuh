@@ -13,6 +13,10 @@ struct VsArgs {
     const int32_t* chunk_off;  // [nseq][kv_heads][nchunk+1] admitted-before-chunk (K2)
 };
 
+// partial-buffer chunks per (seq, kv head): enough for a single kv head to
+// spread over every SM (1M-token contexts with 8-way head sharding)
+constexpr int kMaxChunks = 512;
+
 struct DecArgs {
     PoolView pv;
     int layer, seq0, q_heads;
@@ -22,13 +26,19 @@ struct DecArgs {
     const double* freq;
     int n_pairs;          // nseq * kv_heads (persistent kernel)
     const int* nchunks;   // per (seq, kv head) chunk count written on device, or null (use n_chunks)
+    // K6 union selection (bf16 top-k): per (seq, kv head) [n_gp] entries
+    // logical page | q-head mask << 24, and their count; null = all pages
+    const int32_t* sel;
+    const int32_t* nsel;
 };
 
 // K6: select_topk_pages + per-q-head attention over the selection (topk.cu).
-// scores/sel: [nseq][q_heads][n_gp]; nsel: [nseq][q_heads]
+// scores/sel: [nseq][q_heads][n_gp]; nsel, thr: [nseq][q_heads];
+// umask [nseq][kv_heads][n_gp], ucnt [nseq][kv_heads][ceil(n_gp/1024)]
 template <typename E>
 int launch_topk_decode(const DecArgs& a, int nseq, long budget, const E* q, float* scores, int32_t* sel,
-                       int32_t* nsel, float* part, E* out, cudaStream_t st);
+                       int32_t* nsel, unsigned long long* thr, uint8_t* umask, int* ucnt, float* part, int* nchunks,
+                       E* out, cudaStream_t st);
 
 // counter_reset_by_append: K4 ran just before on the stream and zeroed the
 // work counter; K5 is then launched as its programmatic dependent (PDL)

@@ -314,55 +314,82 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
 }
 
 // merge chunk partials of one (seq, q head): out = sum e^(m_c-M) o_c / sum e^(m_c-M) l_c.
-// Warp 0 loads every chunk's (m, l) at once and reduces them with shuffles;
-// the weights go through smem, then each thread sums one output column with
-// independent loads (no serial load chains: this kernel is latency-bound).
+// The block reduces every chunk's (m, l) and publishes the weights through
+// smem; then the 8 warps each sum every 8th chunk row with coalesced
+// float2 loads (independent across chunks: this kernel is latency-bound) and
+// the warp sums are reduced in smem.
 template <typename E>
-__global__ void decode_combine_kernel(DecArgs a, const float* __restrict__ part, E* __restrict__ out) {
-    constexpr int MAXC = 64;  // >= DecArgs::max_chunks (api.cu)
+__global__ void __launch_bounds__(256) decode_combine_kernel(DecArgs a, const float* __restrict__ part,
+                                                             E* __restrict__ out) {
+    constexpr int MAXC = kMaxChunks;
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
     const int sp = blockIdx.x, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
     const int bh = s * a.pv.kv_heads + h;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t pstride = (size_t)gs * (d + 2);
     const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
     __shared__ float w[MAXC];
+    __shared__ float red[8][256];
     __shared__ float invL;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // partials of the attention kernel (PDL)
     const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, MAXC);
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        float mc[2], lc[2];
+    __shared__ float wred[8];
+    // (m, l) of every chunk: block max, then weights and block sum of l
+    float M = -INFINITY;
+    for (int c = tid; c < nch; c += blockDim.x) M = fmaxf(M, base[(size_t)c * pstride + d]);
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int c = lane + 32 * k;
-            mc[k] = c < nch ? base[(size_t)c * pstride + d] : -INFINITY;
-            lc[k] = c < nch ? base[(size_t)c * pstride + d + 1] : 0.f;
-        }
-        float M = fmaxf(mc[0], mc[1]);
+    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (lane == 0) wred[warp] = M;
+    __syncthreads();
+    M = wred[0];
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        float L = 0.f;
+    for (int k = 1; k < 8; ++k) M = fmaxf(M, wred[k]);
+    float L = 0.f;
+    for (int c = tid; c < nch; c += blockDim.x) {
+        const float mc = base[(size_t)c * pstride + d];
+        const float wc = mc == -INFINITY ? 0.f : __expf(mc - M);
+        w[c] = wc;
+        L += wc * base[(size_t)c * pstride + d + 1];
+    }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int c = lane + 32 * k;
-            const float wc = mc[k] == -INFINITY ? 0.f : __expf(mc[k] - M);
-            if (c < MAXC) w[c] = wc;
-            L += wc * lc[k];
-        }
+    for (int o = 16; o >= 1; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    __syncthreads();  // every wred[] read of M is done
+    if (lane == 0) wred[warp] = L;
+    __syncthreads();
+    if (tid == 0) {
+        float t = 0.f;
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-        if (lane == 0) invL = 1.f / L;
+        for (int k = 0; k < 8; ++k) t += wred[k];
+        invL = 1.f / t;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < d; e += blockDim.x) {
-        float acc0 = 0.f, acc1 = 0.f;
-        int c = 0;
-        for (; c + 1 < nch; c += 2) {
-            acc0 += w[c] * base[(size_t)c * pstride + e];
-            acc1 += w[c + 1] * base[(size_t)(c + 1) * pstride + e];
+    float2 acc[4];  // columns 2*lane + 64*j (d <= 256)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int c = warp; c < nch; c += 8) {
+        const float wc = w[c];
+        const float* r = base + (size_t)c * pstride;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (2 * lane + 64 * j < d) {
+                const float2 x = *reinterpret_cast<const float2*>(r + 2 * lane + 64 * j);
+                acc[j].x = fmaf(wc, x.x, acc[j].x);
+                acc[j].y = fmaf(wc, x.y, acc[j].y);
+            }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (2 * lane + 64 * j < d) {
+            red[warp][2 * lane + 64 * j] = acc[j].x;
+            red[warp][2 * lane + 64 * j + 1] = acc[j].y;
         }
-        if (c < nch) acc0 += w[c] * base[(size_t)c * pstride + e];
-        out[((size_t)s * a.q_heads + p) * d + e] = from_f<E>((acc0 + acc1) * invL);
+    __syncthreads();
+    for (int e = tid; e < d; e += blockDim.x) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += red[k][e];
+        out[((size_t)s * a.q_heads + p) * d + e] = from_f<E>(t * invL);
     }
 }
 
@@ -373,7 +400,7 @@ int launch_decode_attn_simt(const DecArgs& a, int nseq, const E* q, float* part,
     const size_t smem = sizeof(float) * ((size_t)gs * d + (size_t)4 * gs * (d + 2));
     cudaFuncSetAttribute(decode_attn_simt_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     decode_attn_simt_kernel<E><<<dim3(a.n_chunks, nseq * a.pv.kv_heads), 128, smem, st>>>(a, q, part);
-    decode_combine_kernel<E><<<nseq * a.q_heads, 128, 0, st>>>(a, part, out);
+    decode_combine_kernel<E><<<nseq * a.q_heads, 256, 0, st>>>(a, part, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -381,7 +408,7 @@ int launch_decode_combine_bf16(const DecArgs& a, int nseq, const float* part, __
     // programmatic dependent of the attention kernel: launch latency overlaps its tail
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nseq * a.q_heads);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(256);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -55,6 +55,10 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, uint32_t row, uint32_t ch
 
 }  // namespace
 
+// TOPK: the Global part of each (seq, kv head) is K6's union selection
+// (a.sel / a.nsel: logical page | q-head mask << 24) instead of every page;
+// rows (q heads) that did not select a page get -inf logits for it.
+template <bool TOPK>
 __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __grid_constant__ CUtensorMap tpool,
                                                                       DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                       float* __restrict__ part,
@@ -84,7 +88,8 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         int npmax = 0;
         for (int p = 0; p < npairs; ++p) {
             const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
-            const int np = (st.global_len + ps - 1) / ps + (st.local_len + ps - 1) / ps;
+            const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
+            const int np = ngv + (st.local_len + ps - 1) / ps;
             total += np;
             npmax = max(npmax, np);
         }
@@ -97,7 +102,8 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         int acc = 0;
         for (int p = 0; p < npairs; ++p) {
             const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
-            const int np = (st.global_len + ps - 1) / ps + (st.local_len + ps - 1) / ps;
+            const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
+            const int np = ngv + (st.local_len + ps - 1) / ps;
             item_base[p] = acc;
             const int nc = max(1, (np + cp - 1) / cp);
             acc += nc;
@@ -128,41 +134,51 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
         const HeadState st = a.pv.state[hidx];
         const long pos = st.tokens_seen - 1;
-        const int ng = (st.global_len + ps - 1) / ps;
+        const int ngp = (st.global_len + ps - 1) / ps;
+        const int ng = TOPK ? a.nsel[bh] : ngp;  // virtual Global pages
         const int NP = ng + (st.local_len + ps - 1) / ps;
+        // TOPK: the partial last Global page can only be the last union entry
+        const int32_t* usel = TOPK ? a.sel + (size_t)bh * a.pv.n_gp : nullptr;
+        const bool last_sel = TOPK && ng > 0 && (usel[ng - 1] & 0xFFFFFF) == ngp - 1;
         const int vp0 = chunk * cp, vp1 = min(NP, vp0 + cp);
         const size_t pstride = (size_t)gs * (d + 2);
         float* pout = part + ((size_t)bh * a.max_chunks + chunk) * pstride;
 
-        // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d); rows >= gs are zero
-        for (int e = tid; e < 16 * (d / 2); e += blockDim.x) {
-            const int r = e / (d / 2), i = e % (d / 2);
-            float y0 = 0.f, y1 = 0.f;
-            if (r < gs) {
-                const size_t off = ((size_t)s * a.q_heads + h * gs + r) * d + 2 * i;
-                const float x0 = __bfloat162float(q[off]), x1 = __bfloat162float(q[off + 1]);
-                float c, sn;
-                rope_cs(a.freq, i, pos, c, sn);
-                y0 = (x0 * c - x1 * sn) * qs;
-                y1 = (x0 * sn + x1 * c) * qs;
-            }
-            Qs[r * QROW + 2 * i] = __float2bfloat16_rn(y0);
-            Qs[r * QROW + 2 * i + 1] = __float2bfloat16_rn(y1);
-        }
         // stage this item's physical page ids (coalesced) so the TMA issue
         // never waits on a dependent global load
-        for (int v = vp0 + tid; v < vp1; v += blockDim.x)
-            pids[v - vp0] = v < ng ? a.pv.gpt[hidx * a.pv.n_gp + v] : a.pv.lpt[hidx * a.pv.n_lp + (v - ng)];
+        for (int v = vp0 + tid; v < vp1; v += blockDim.x) {
+            if (TOPK) {  // page id | q-head mask << 24 (local pages: every head)
+                int pg;
+                uint32_t mk;
+                if (v < ng) {
+                    const uint32_t e = (uint32_t)usel[v];
+                    pg = a.pv.gpt[hidx * a.pv.n_gp + (e & 0xFFFFFFu)];
+                    mk = e >> 24;
+                } else {
+                    pg = a.pv.lpt[hidx * a.pv.n_lp + (v - ng)];
+                    mk = 0xFFu;
+                }
+                if (pg < 0) pg = mk = 0;  // failed allocation (latched ENOPAGES): masked
+                pids[v - vp0] = (int)((uint32_t)pg | (mk << 24));
+            } else {
+                pids[v - vp0] = v < ng ? a.pv.gpt[hidx * a.pv.n_gp + v] : a.pv.lpt[hidx * a.pv.n_lp + (v - ng)];
+            }
+        }
         __syncthreads();
 
         const int nmine = vp1 > vp0 ? (vp1 - vp0 - warp + DW - 1) / DW : 0;  // pages vp0+warp, +DW, ...
         auto page_of = [&](int vp, int& valid) -> int {
-            valid = vp < ng ? min(ps, st.global_len - vp * ps) : min(ps, st.local_len - (vp - ng) * ps);
+            if (TOPK)
+                valid = vp < ng ? ((vp == ng - 1 && last_sel) ? st.global_len - (ngp - 1) * ps : ps)
+                                : min(ps, st.local_len - (vp - ng) * ps);
+            else
+                valid = vp < ng ? min(ps, st.global_len - vp * ps) : min(ps, st.local_len - (vp - ng) * ps);
             return pids[vp - vp0];
         };
         auto issue = [&](int k) {  // k-th page of this warp (ring slot (kq + k) % DNS)
             int valid;
             int page = page_of(vp0 + warp + k * DW, valid);
+            if (TOPK) page &= 0xFFFFFF;
             if (page < 0) page = 0;  // failed allocation (latched ENOPAGES): stream a harmless page
             const uint32_t slot = (kq + k) % DNS;
             uint8_t* dst = ring + (warp * DNS + slot) * PAGE_B;
@@ -177,6 +193,23 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
             tc::fence_proxy_async_smem();
             for (int k = 0; k < min(DNS, nmine); ++k) issue(k);
         }
+        // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d); rows >= gs are zero
+        // (computed while the first pages of the item are in flight)
+        for (int e = tid; e < 16 * (d / 2); e += blockDim.x) {
+            const int r = e / (d / 2), i = e % (d / 2);
+            float y0 = 0.f, y1 = 0.f;
+            if (r < gs) {
+                const size_t off = ((size_t)s * a.q_heads + h * gs + r) * d + 2 * i;
+                const float x0 = __bfloat162float(q[off]), x1 = __bfloat162float(q[off + 1]);
+                float c, sn;
+                rope_cs(a.freq, i, pos, c, sn);
+                y0 = (x0 * c - x1 * sn) * qs;
+                y1 = (x0 * sn + x1 * c) * qs;
+            }
+            Qs[r * QROW + 2 * i] = __float2bfloat16_rn(y0);
+            Qs[r * QROW + 2 * i + 1] = __float2bfloat16_rn(y1);
+        }
+        __syncthreads();
         // Q A-fragments: 8 k-steps of 16 dims (rows 0..15, only < gs nonzero)
         uint32_t qa[8][4];
         {
@@ -193,7 +226,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         const int t0 = (lane & 3) * 2;
         for (int k = 0; k < nmine; ++k) {
             int valid;
-            page_of(vp0 + warp + k * DW, valid);
+            const int pidv = page_of(vp0 + warp + k * DW, valid);
             const uint32_t slot = (kq + k) % DNS;
             tc::mbar_wait(&full[warp * DNS + slot], ((kq + k) / DNS) & 1);
             const uint32_t kb = wring + slot * PAGE_B, vb = kb + 4096;
@@ -217,13 +250,16 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
                     for (int e = 0; e < 2; ++e)
                         if (nt * 8 + t0 + e >= valid) sc[nt][e] = -INFINITY;
             }
+            if (TOPK && !(((uint32_t)pidv >> (24 + (lane >> 2))) & 1u))  // row lane/4 did not select this page
+                sc[0][0] = sc[0][1] = sc[1][0] = sc[1][1] = -INFINITY;
             float mx = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
             const float mn = fmaxf(m, mx);
             const float alpha = (m == -INFINITY) ? 0.f : ex2f(m - mn);
-            const float p00 = ex2f(sc[0][0] - mn), p01 = ex2f(sc[0][1] - mn);
-            const float p10 = ex2f(sc[1][0] - mn), p11 = ex2f(sc[1][1] - mn);
+            const float mb = (TOPK && mn == -INFINITY) ? 0.f : mn;  // row with nothing selected yet
+            const float p00 = ex2f(sc[0][0] - mb), p01 = ex2f(sc[0][1] - mb);
+            const float p10 = ex2f(sc[1][0] - mb), p11 = ex2f(sc[1][1] - mb);
             float ls = p00 + p01 + p10 + p11;
             ls += __shfl_xor_sync(0xffffffffu, ls, 1);
             ls += __shfl_xor_sync(0xffffffffu, ls, 2);
@@ -296,21 +332,27 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     DecArgs a = a0;
     const int gs = a.q_heads / a.pv.kv_heads;
     if (a.pv.head_dim != 128 || a.pv.page_size != 16 || gs > 16) return WGKV_ENOTSUP;
+    // cached per pool (a new context may reuse a freed pool's address with
+    // another capacity, so the key includes it)
     static CUtensorMap tp;
     static const void* tp_base = nullptr;
-    if (tp_base != a.pv.data) {
+    static long tp_cap = -1;
+    if (tp_base != a.pv.data || tp_cap != a.pv.capacity) {
         if (make_tmap_3d_bf16(&tp, a.pv.data, 128, 16, 2 * (uint64_t)a.pv.capacity, 256, 16 * 256, 64, 16, 1))
             return WGKV_ECUDA;
         tp_base = a.pv.data;
+        tp_cap = a.pv.capacity;
     }
     a.n_pairs = nseq * a.pv.kv_heads;
     const size_t smem =
         1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
     if (smem > 113 * 1024) return WGKV_ENOTSUP;
-    static size_t smem_set = 0;  // host-side only; keeps graph capture free of attribute calls
-    if (smem > smem_set) {
-        cudaFuncSetAttribute(decode_attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        smem_set = smem;
+    const bool topk = a.sel != nullptr;
+    auto kern = topk ? decode_attn_mma_kernel<true> : decode_attn_mma_kernel<false>;
+    static size_t smem_set[2] = {0, 0};  // host-side only; keeps graph capture free of attribute calls
+    if (smem > smem_set[topk]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_set[topk] = smem;
     }
     // work-stealing counter: one int past the per-(seq, kv head) chunk counts;
     // zeroed by K4 when it precedes us (PDL), else by a memset here
@@ -326,7 +368,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = counter_reset_by_append ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, decode_attn_mma_kernel, tp, a, q, part, nchunks, counter);
+    cudaLaunchKernelEx(&cfg, kern, tp, a, q, part, nchunks, counter);
     a.nchunks = nchunks;
     extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
     return launch_decode_combine_bf16(a, nseq, part, out, st);

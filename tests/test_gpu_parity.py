@@ -319,3 +319,33 @@ def test_topk_decode_vs_oracle(W, orc, dtype, budget):
             assert gap < 3e-2, (t, p, gap)
             near_ties += 1
     assert near_ties <= checks // 4, (near_ties, checks)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("T", [20000, 70000])
+def test_topk_all_ties_take_oldest(W, dtype, T):
+    """Every page scores exactly 0 (k = 0), so select_topk_pages' tie rule
+    (engine.cpp:36-84: stable sort, older page first) must pick logical pages
+    0..budget-1; the logits are then all 0 and each q head's output is the mean
+    of V over the selected tokens + the Local ring.  At T = 70000 the Global
+    cache holds > 4096 pages in one score bin, which exercises the
+    all-pages refinement of the threshold kernel."""
+    hq, hkv, d, Wn, budget = 4, 1, 128, 1024, 100
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    s = W.Session(1, hq, hkv, d, d, Wn, max_tokens=T + 1, dtype=W.BF16 if dtype == "bf16" else W.F32,
+                  topk_budget=budget, rope_base=5e5)
+    q = torch.randn(1, T + 1, hq, d, device="cuda", generator=g).to(dt)
+    k = torch.zeros(1, T + 1, hkv, d, device="cuda", dtype=dt)
+    v = torch.randn(1, T + 1, hkv, d, device="cuda", generator=g).to(dt)
+    ones = torch.ones(1, hkv, T, device="cuda")
+    s.prefill_layer(0, q[:, :T], k[:, :T], v[:, :T], forced_gates=ones)
+    out = s.decode_layer(0, q[:, T], k[:, T], v[:, T], forced_gates=torch.ones(1, hkv, device="cuda"))
+    s.sync()
+    # Global = tokens 0..T-W (T-W promoted by this step), Local = T-W+1..T
+    vv = v[0, :, 0].double().cpu().numpy()
+    sel = np.concatenate([vv[: budget * 16], vv[T - Wn + 1: T + 1]])
+    ref = sel.mean(axis=0)
+    o = out.double().cpu().numpy()[0]
+    for p in range(hq):
+        assert rel_err(o[p], ref) < TOL[dtype], p
