@@ -70,6 +70,7 @@ struct wgkv_ctx {
     float *w1t = nullptr, *b1f = nullptr, *w2f = nullptr;
     double *b2f = nullptr, *w1d = nullptr, *b1d = nullptr, *w2d = nullptr, *freq = nullptr;
     float* bandc = nullptr;  // per (layer, kv head) fp32 error-bound constant for K1's recheck band
+    float4* bw = nullptr;    // [blk][hidden/2] {b1[2j], b1[2j+1], w2[2j], w2[2j+1]} (K1 tc epilogue)
     __nv_bfloat16* w1split = nullptr;  // [L*H][Wpre_hi, Wpost_hi, Wpre_lo, Wpost_lo][128][128] (K1 tcgen05)
     bool gates_set = false;
     // workspaces
@@ -78,7 +79,9 @@ struct wgkv_ctx {
     uint8_t* ws_bits = nullptr;
     int32_t* ws_chunk = nullptr;
     int64_t* ws_cand = nullptr;
-    int* ws_cnt = nullptr;  // [0] candidates, [1] near count
+    int* ws_cnt = nullptr;  // [1] near count
+    int* ws_pcnt = nullptr;      // [S][H] recheck-list lengths (K1)
+    float2* ws_rope = nullptr;   // [max_prefill_tokens][d/2] cos/sin table (K1)
     int64_t* ws_near = nullptr;
     float* ws_part = nullptr;
     int* ws_nchunks = nullptr;
@@ -119,6 +122,7 @@ struct wgkv_ctx {
         a.w2d = w2d;
         a.b2d = b2f;
         a.bandc = bandc;
+        a.bw = bw;
         return a;
     }
     bool use_tc() const {
@@ -184,6 +188,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->w2f = dalloc<float>(blocks * c.hidden, o);
     ctx->b2f = dalloc<double>(blocks, o);
     ctx->bandc = dalloc<float>(blocks, o);
+    ctx->bw = dalloc<float4>(blocks * ((c.hidden + 1) / 2), o);
     ctx->w1d = dalloc<double>(blocks * fd * c.hidden, o);
     if (c.dtype == WGKV_BF16 && d == 128 && c.hidden == 128)  // K1 tensor-core operand: split-bf16 W1 tiles
         ctx->w1split = dalloc<__nv_bfloat16>(blocks * 4 * 128 * 128, o);
@@ -198,6 +203,8 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->ws_chunk = dalloc<int32_t>((size_t)S * H * ((Tm + 127) / 128 + 1), o);
     ctx->ws_cand = dalloc<int64_t>(toks, o);
     ctx->ws_cnt = dalloc<int>(4, o);
+    ctx->ws_pcnt = dalloc<int>((size_t)S * H, o);
+    ctx->ws_rope = dalloc<float2>((size_t)Tm * (d / 2), o);
     ctx->near_cap = 1 << 20;
     ctx->ws_near = dalloc<int64_t>((size_t)ctx->near_cap, o);
     const int gs = c.q_heads / c.kv_heads;
@@ -323,6 +330,18 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
     WGKV_CUDA_TRY(cudaMemcpy(ctx->w2d, w2d.data(), w2d.size() * 8, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->b2f, b2.data(), b2.size() * 8, cudaMemcpyHostToDevice));
     WGKV_CUDA_TRY(cudaMemcpy(ctx->bandc, bandc.data(), bandc.size() * 4, cudaMemcpyHostToDevice));
+    {
+        const int hp = (hid + 1) / 2;
+        std::vector<float4> bw(nb * hp);
+        for (size_t b = 0; b < nb; ++b)
+            for (int j = 0; j < hp; ++j) {
+                const int u0 = 2 * j, u1 = std::min(2 * j + 1, hid - 1);
+                const float z = (2 * j + 1 < hid) ? 1.f : 0.f;
+                bw[b * hp + j] = make_float4(b1f[b * hid + u0], b1f[b * hid + u1] * z, w2f[b * hid + u0],
+                                             w2f[b * hid + u1] * z);
+            }
+        WGKV_CUDA_TRY(cudaMemcpy(ctx->bw, bw.data(), bw.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    }
     if (ctx->w1split) {  // W1 = hi + lo in bf16, as four K-major [128 hidden][128 k] tiles per head
         std::vector<__nv_bfloat16> ws(nb * 4 * 128 * 128);
         for (size_t b = 0; b < nb; ++b)
@@ -389,13 +408,14 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
     } else if (ctx->cfg.dtype == WGKV_BF16) {
         const bool tc = ctx->cfg.attn_impl != WGKV_ATTN_SIMT && ctx->w1split;
         st = launch_gate_prefill<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)k_pre, (__nv_bfloat16*)k_post_out,
-                                                g_out, bits_out, ctx->ws_cand, ctx->ws_cnt, nidx, ncap,
+                                                g_out, bits_out, (int32_t*)ctx->ws_cand, ctx->ws_pcnt, nidx, ncap,
                                                 ctx->ws_cnt + 1, tc ? ctx->w1split : nullptr,
-                                                (long)ctx->cfg.layers * ctx->cfg.kv_heads * 4, ctx->stream);
+                                                (long)ctx->cfg.layers * ctx->cfg.kv_heads * 4, ctx->ws_rope,
+                                                ctx->stream);
     } else {
         st = launch_gate_prefill<float>(a, nseq, (const float*)k_pre, (float*)k_post_out, g_out, bits_out,
-                                        ctx->ws_cand, ctx->ws_cnt, nidx, ncap, ctx->ws_cnt + 1, nullptr, 0,
-                                        ctx->stream);
+                                        (int32_t*)ctx->ws_cand, ctx->ws_pcnt, nidx, ncap, ctx->ws_cnt + 1, nullptr, 0,
+                                        ctx->ws_rope, ctx->stream);
     }
     if (st) return fail(st, std::string("gate kernels: ") + cudaGetErrorString(cudaGetLastError()));
     if (near_count) {
@@ -726,6 +746,19 @@ int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out) {
     WGKV_CUDA_TRY(cudaMemcpy(&top, ctx->pv.free_top, sizeof(top), cudaMemcpyDeviceToHost));
     out[0] = ctx->pv.capacity;
     out[1] = top;
+    return WGKV_OK;
+}
+
+// diagnostics (not part of the C-ABI contract): out[0] = tokens the last
+// wgkv_gate_score listed for the fp64 recheck, out[1] = reported near-tau tokens
+extern "C" int wgkv_dbg_gate_counts(wgkv_ctx* ctx, int* out) {
+    if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
+    WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    std::vector<int> pc((size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads);
+    WGKV_CUDA_TRY(cudaMemcpy(pc.data(), ctx->ws_pcnt, sizeof(int) * pc.size(), cudaMemcpyDeviceToHost));
+    out[0] = 0;
+    for (int v : pc) out[0] += v;
+    WGKV_CUDA_TRY(cudaMemcpy(out + 1, ctx->ws_cnt + 1, sizeof(int), cudaMemcpyDeviceToHost));
     return WGKV_OK;
 }
 

@@ -13,6 +13,8 @@
 //       and overwrites g/bit, so bits equal the reference's except where the
 //       fp64 score itself is within 1e-6 of tau (reported).
 // The fp64 routine is shared with decode (K4), where it is the only path.
+#include <algorithm>
+
 #include "gate.cuh"
 
 namespace wgkv {
@@ -28,7 +30,7 @@ constexpr int GT_XS = GT_TOK + 4;
 template <typename T>
 __global__ void __launch_bounds__(256, 2)
     gate_prefill_kernel(GateArgs a, const T* __restrict__ k_pre, T* __restrict__ k_post, float* __restrict__ g_out,
-                        uint8_t* __restrict__ bits_out, int64_t* __restrict__ cand, int* __restrict__ cand_cnt) {
+                        uint8_t* __restrict__ bits_out, int32_t* __restrict__ cand, int* __restrict__ pcnt) {
     extern __shared__ float4 smem_f4[];
     float* Xs = reinterpret_cast<float*>(smem_f4);     // [2d][GT_XS]   transposed feature
     float* Ws = Xs + 2 * a.d * GT_XS;                  // [2][GT_KC][GT_HID]
@@ -159,19 +161,20 @@ __global__ void __launch_bounds__(256, 2)
             const float u = 5.9604645e-8f;
             const float band = 4.f * (1.13f * (fd + 1) * u * sqrtf(xx) * a.bandc[blk] +
                                       (a.hidden + 6) * u * (sacc[tid] + fabsf((float)a.b2f[blk]) + fabsf(a.ztau)));
-            if (fabsf(z2 - a.ztau) <= band) {
-                const int slot = atomicAdd(cand_cnt, 1);
-                cand[slot] = (int64_t)gi;
+            if (fabsf(z2 - a.ztau) <= band) {  // per-(seq, kv head) candidate list
+                const int pair = s * a.kv_heads + h;
+                cand[(size_t)pair * a.T + atomicAdd(&pcnt[pair], 1)] = (int32_t)t;
             }
         }
     }
 }
 
 // One warp per candidate: exact fp64 gate, overwrite g/bit, report |g-tau|<1e-6.
+// Candidates are listed per (seq, kv head) pair (blockIdx.y): cand[pair*T + i] = t.
 template <typename T>
 __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, float* __restrict__ g_out,
-                                    uint8_t* __restrict__ bits_out, const int64_t* __restrict__ cand,
-                                    const int* __restrict__ cand_cnt, int64_t* __restrict__ near_idx, int near_cap,
+                                    uint8_t* __restrict__ bits_out, const int32_t* __restrict__ cand,
+                                    const int* __restrict__ pcnt, int64_t* __restrict__ near_idx, int near_cap,
                                     int* __restrict__ near_cnt) {
     extern __shared__ double dsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -179,12 +182,11 @@ __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, flo
     double* xs = dsm + (size_t)warp * (2 * d + a.hidden);
     double* terms = xs + 2 * d;
     float* kf = reinterpret_cast<float*>(dsm + (size_t)nw * (2 * d + a.hidden)) + warp * d;
-    const int n = *cand_cnt;
+    const int pair = blockIdx.y, s = pair / a.kv_heads, h = pair % a.kv_heads;
+    const int n = pcnt[pair];
     for (int c = blockIdx.x * nw + warp; c < n; c += gridDim.x * nw) {
-        const int64_t gi = cand[c];
-        const long t = gi % a.T;
-        const int h = (int)((gi / a.T) % a.kv_heads);
-        const int s = (int)(gi / ((int64_t)a.T * a.kv_heads));
+        const long t = cand[(size_t)pair * a.T + c];
+        const int64_t gi = ((int64_t)s * a.kv_heads + h) * a.T + t;
         const size_t off = (((size_t)s * a.T + t) * a.kv_heads + h) * d;
         for (int k = lane; k < d; k += 32) kf[k] = to_f(k_pre[off + k]);
         __syncwarp();
@@ -203,16 +205,161 @@ __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, flo
     }
 }
 
+// ---------------------------------------------------------------------------
+// fp64 recheck as a blocked GEMM (d = hidden = 128): one work item = up to 64
+// listed tokens of one (seq, kv head), so every W1 element fetched serves 64
+// tokens (the per-token warp form re-reads the head's 256 KB fp64 W1 from L2
+// for every token).  X = [k_pre ; RoPE_fp64(k_pre)] for the 64 tokens is built
+// in smem exactly as feature_fp64_warp does; z1 = W1 . x in fp64 (DFMA, k in
+// order); then, per token, the reference's order for the rest: terms
+// w2_h * gelu(z1_h + b1_h), z2 = b2 + sum_h terms (sequential), sigmoid, clamp
+// (gating.cpp:158-171).  Only the dot's rounding differs from the reference
+// (FMA), by O(1e-16) relative: bits can differ only where |g - tau| < 1e-14,
+// inside the reported 1e-6 band.
+// ---------------------------------------------------------------------------
+constexpr int RC_C = 64;   // tokens per work item
+constexpr int RC_KC = 32;  // k chunk of W1 staged per step
+constexpr int RC_TP = 129; // padded terms row (doubles)
+constexpr size_t RC_SMEM = sizeof(double) * (256 * RC_C + (size_t)RC_C * RC_TP) + 4 * RC_C + 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256, 1)
+    gate_recheck_gemm_kernel(GateArgs a, int npairs, const T* __restrict__ k_pre, float* __restrict__ g_out,
+                             uint8_t* __restrict__ bits_out, const int32_t* __restrict__ cand,
+                             const int* __restrict__ pcnt, int64_t* __restrict__ near_idx, int near_cap,
+                             int* __restrict__ near_cnt) {
+    extern __shared__ double rsm[];
+    double* X = rsm;                         // [256 k][RC_C]
+    double* Wt = X + 256 * RC_C;             // [RC_KC][128] W1 chunk (k-major); then terms [RC_C][RC_TP]
+    int* ts = reinterpret_cast<int*>(Wt + RC_C * RC_TP);  // [RC_C] token index t
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    constexpr int d = 128, fd = 256, hid = 128;
+    // items: pair-major chunks of RC_C listed tokens
+    int item = blockIdx.x;
+    int pair = 0, before = 0;
+    for (;; item += gridDim.x) {
+        // locate (pair, chunk) of this item (pairs are few; a linear walk)
+        int acc = 0, p = 0, nc = 0;
+        for (; p < npairs; ++p) {
+            nc = (pcnt[p] + RC_C - 1) / RC_C;
+            if (item < acc + nc) break;
+            acc += nc;
+        }
+        if (p >= npairs) break;
+        pair = p;
+        before = (item - acc) * RC_C;
+        const int n = min(RC_C, pcnt[pair] - before);
+        const int s = pair / a.kv_heads, h = pair % a.kv_heads;
+        const int blk = a.layer * a.bank_heads + a.head_offset + h;
+        __syncthreads();  // previous item done with X / Wt / ts
+        if (tid < RC_C) ts[tid] = tid < n ? cand[(size_t)pair * a.T + before + tid] : 0;
+        __syncthreads();
+        // ---- features (feature_fp64_warp's arithmetic) ---------------------
+        for (int e = tid; e < RC_C * (d / 2); e += blockDim.x) {
+            const int c = e % RC_C, i = e / RC_C;
+            double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+            if (c < n) {
+                const long t = ts[c];
+                const size_t off = (((size_t)s * a.T + t) * a.kv_heads + h) * d + 2 * i;
+                x0 = (double)to_f(k_pre[off]);
+                x1 = (double)to_f(k_pre[off + 1]);
+                const double angle = __dmul_rn((double)(a.pos0 + t), a.freq[i]);
+                const double cs = cos(angle), sn = sin(angle);
+                y0 = __dsub_rn(__dmul_rn(x0, cs), __dmul_rn(x1, sn));
+                y1 = __dadd_rn(__dmul_rn(x0, sn), __dmul_rn(x1, cs));
+            }
+            X[(2 * i) * RC_C + c] = x0;
+            X[(2 * i + 1) * RC_C + c] = x1;
+            X[(d + 2 * i) * RC_C + c] = y0;
+            X[(d + 2 * i + 1) * RC_C + c] = y1;
+        }
+        // ---- z1 = W1 . x: thread owns tokens 8ty..8ty+7, hidden tx + 32j ---
+        double acc8[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc8[i][j] = 0.0;
+        const double* w1 = a.w1d + (size_t)blk * hid * fd;
+        // register prefetch of the next W1 chunk: 8 double2 per thread
+        double2 pre[8];
+        auto fetch = [&](int kc) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int e = tid + 256 * q;  // 2048 double2 = [128 h][16 k-pairs]
+                const int hh = e & 127, kp = e >> 7;
+                pre[q] = *reinterpret_cast<const double2*>(w1 + (size_t)hh * fd + kc * RC_KC + 2 * kp);
+            }
+        };
+        fetch(0);
+        for (int kc = 0; kc < fd / RC_KC; ++kc) {
+            __syncthreads();  // previous chunk consumed (and, first time, X written)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int e = tid + 256 * q;
+                const int hh = e & 127, kp = e >> 7;
+                Wt[(2 * kp) * 128 + hh] = pre[q].x;
+                Wt[(2 * kp + 1) * 128 + hh] = pre[q].y;
+            }
+            __syncthreads();
+            if (kc + 1 < fd / RC_KC) fetch(kc + 1);
+#pragma unroll 4
+            for (int kk = 0; kk < RC_KC; ++kk) {
+                const double* xr = X + (size_t)(kc * RC_KC + kk) * RC_C + 8 * ty;
+                const double2 x01 = *reinterpret_cast<const double2*>(xr);
+                const double2 x23 = *reinterpret_cast<const double2*>(xr + 2);
+                const double2 x45 = *reinterpret_cast<const double2*>(xr + 4);
+                const double2 x67 = *reinterpret_cast<const double2*>(xr + 6);
+                const double xv[8] = {x01.x, x01.y, x23.x, x23.y, x45.x, x45.y, x67.x, x67.y};
+                double wv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) wv[j] = Wt[kk * 128 + tx + 32 * j];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc8[i][j] = fma(wv[j], xv[i], acc8[i][j]);
+            }
+        }
+        __syncthreads();  // Wt becomes the terms buffer
+        double* terms = Wt;
+        const double* b1 = a.b1d + (size_t)blk * hid;
+        const double* w2 = a.w2d + (size_t)blk * hid;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int hh = tx + 32 * j;
+            const double bb = b1[hh], ww = w2[hh];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                terms[(8 * ty + i) * RC_TP + hh] = __dmul_rn(ww, gelu_ref(__dadd_rn(acc8[i][j], bb)));
+        }
+        __syncthreads();
+        if (tid < n) {
+            double z2 = a.b2d[blk];
+            for (int hh = 0; hh < hid; ++hh) z2 = __dadd_rn(z2, terms[tid * RC_TP + hh]);
+            double g = sigmoid_ref(z2);
+            const double lo = 4.9406564584124654e-324, hi = 0.99999999999999988898;
+            g = g < lo ? lo : (g > hi ? hi : g);
+            const int64_t gi = ((int64_t)s * a.kv_heads + h) * a.T + ts[tid];
+            g_out[gi] = (float)g;
+            bits_out[gi] = g >= a.tau ? 1 : 0;
+            if (fabs(g - a.tau) < 1e-6) {
+                const int slot = atomicAdd(near_cnt, 1);
+                if (slot < near_cap) near_idx[slot] = gi;
+            }
+        }
+    }
+}
+
 template <typename T>
 int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, float* g, uint8_t* bits,
-                        int64_t* cand, int* cand_cnt, int64_t* near_idx, int near_cap, int* near_cnt,
-                        const __nv_bfloat16* w1split, long n_wtiles, cudaStream_t st) {
-    cudaMemsetAsync(cand_cnt, 0, sizeof(int), st);
+                        int32_t* cand, int* pcnt, int64_t* near_idx, int near_cap, int* near_cnt,
+                        const __nv_bfloat16* w1split, long n_wtiles, float2* rope_ws, cudaStream_t st) {
+    const int npairs = nseq * a.kv_heads;
+    cudaMemsetAsync(pcnt, 0, sizeof(int) * npairs, st);
     bool done = false;
     if constexpr (std::is_same<T, __nv_bfloat16>::value) {
         // tensor-core path (d = hidden = 128, split-bf16 W1 prepared by wgkv_gate_set)
         if (w1split && a.d == 128 && a.hidden == 128) {
-            const int r = launch_gate_tc(a, nseq, k_pre, k_post, g, bits, cand, cand_cnt, w1split, n_wtiles, st);
+            const int r = launch_gate_tc(a, nseq, k_pre, k_post, g, bits, cand, pcnt, w1split, n_wtiles, rope_ws, st);
             if (r != WGKV_OK) return r;
             done = true;
         }
@@ -225,12 +372,23 @@ int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, 
             attr_set = true;
         }
         dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
-        gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, cand_cnt);
+        gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, pcnt);
+    }
+    if (a.d == 128 && a.hidden == 128) {
+        static bool rc_attr = false;
+        if (!rc_attr) {
+            cudaFuncSetAttribute(gate_recheck_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)RC_SMEM);
+            rc_attr = true;
+        }
+        gate_recheck_gemm_kernel<T><<<kNumSMs, 256, RC_SMEM, st>>>(a, npairs, k_pre, g, bits, cand, pcnt, near_idx,
+                                                                   near_cap, near_cnt);
+        return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
     }
     const int nw = 8;
     const size_t rsm = sizeof(double) * nw * (2 * a.d + a.hidden) + sizeof(float) * nw * a.d;
-    gate_recheck_kernel<T><<<kNumSMs * 4, 32 * nw, rsm, st>>>(a, k_pre, g, bits, cand, cand_cnt, near_idx, near_cap,
-                                                              near_cnt);
+    gate_recheck_kernel<T><<<dim3(std::max(1, kNumSMs * 4 / npairs), npairs), 32 * nw, rsm, st>>>(
+        a, k_pre, g, bits, cand, pcnt, near_idx, near_cap, near_cnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -272,10 +430,10 @@ int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_p
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
-template int launch_gate_prefill<float>(const GateArgs&, int, const float*, float*, float*, uint8_t*, int64_t*, int*,
-                                        int64_t*, int, int*, const __nv_bfloat16*, long, cudaStream_t);
+template int launch_gate_prefill<float>(const GateArgs&, int, const float*, float*, float*, uint8_t*, int32_t*, int*,
+                                        int64_t*, int, int*, const __nv_bfloat16*, long, float2*, cudaStream_t);
 template int launch_gate_prefill<__nv_bfloat16>(const GateArgs&, int, const __nv_bfloat16*, __nv_bfloat16*, float*,
-                                                uint8_t*, int64_t*, int*, int64_t*, int, int*, const __nv_bfloat16*,
-                                                long, cudaStream_t);
+                                                uint8_t*, int32_t*, int*, int64_t*, int, int*, const __nv_bfloat16*,
+                                                long, float2*, cudaStream_t);
 
 }  // namespace wgkv

@@ -25,6 +25,7 @@ struct GateArgs {
     const float* w2f;    // [blk][hidden]
     const double* b2f;   // [blk]
     const float* bandc;  // [blk] sum_h |w2_h| * ||W1_h||_2 (fp32 error bound constant)
+    const float4* bw;    // [blk][hidden/2] interleaved b1 / w2 pairs (tensor-core epilogue)
     const double* w1d;
     const double* b1d;
     const double* w2d;
@@ -163,14 +164,16 @@ __device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, co
 int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_post, const float* forced, float* g,
                        uint8_t* bits, size_t esz, cudaStream_t st);
 
+// cand: [nseq*kv_heads][T] token indices listed for the fp64 recheck, pcnt:
+// [nseq*kv_heads] list lengths; rope_ws: [T][d/2] cos/sin workspace (bf16 tc path)
 template <typename T>
 int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, float* g, uint8_t* bits,
-                        int64_t* cand, int* cand_cnt, int64_t* near_idx, int near_cap, int* near_cnt,
-                        const __nv_bfloat16* w1split, long n_wtiles, cudaStream_t st);
+                        int32_t* cand, int* pcnt, int64_t* near_idx, int near_cap, int* near_cnt,
+                        const __nv_bfloat16* w1split, long n_wtiles, float2* rope_ws, cudaStream_t st);
 
 // tensor-core K1 (gate_tc.cu): w1split = [L*H][4][128][128] bf16 split W1 tiles
 int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv_bfloat16* k_post, float* g,
-                   uint8_t* bits, int64_t* cand, int* cand_cnt, const __nv_bfloat16* w1split, long n_wtiles,
-                   cudaStream_t st);
+                   uint8_t* bits, int32_t* cand, int* pcnt, const __nv_bfloat16* w1split, long n_wtiles,
+                   float2* rope_ws, cudaStream_t st);
 
 }  // namespace wgkv

@@ -37,6 +37,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp yields its issue slots
+// (for warps that share SM sub-partitions with compute warps)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 // non-suspending poll (test_wait): lower wake-up latency for a thread on the
 // critical path (the MMA issuer), at the cost of issue slots while spinning
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
