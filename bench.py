@@ -256,7 +256,7 @@ def run_gpu(args, cfg):
         check(lib.wgkv_vs_prefill(h, l, 0, B, T, P(qi), P(kpost), P(vi), P(bits_ws), P(out)), "K3")
         if k3_events is not None:
             k3_events[1].record(stream)
-        launches["n"] += 5  # gate, recheck, plan, scatter, vs
+        launches["n"] += 6  # rope table, gate, recheck, plan, scatter, vs
         if world > 1:
             dist.all_gather_into_tensor(gath, out)  # rank-major head shards (C1)
 
@@ -287,7 +287,7 @@ def run_gpu(args, cfg):
                 graph["g"].replay()
             else:
                 decode_token_step()
-            launches["n"] += 3 * L  # append, attention, combine kernels (+ a counter memset node)
+            launches["n"] += 4 * L  # append, gate (side stream), attention, combine (+ a counter memset node)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -454,7 +454,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="128k", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="128k", choices=sorted(CONFIGS) + ["serve", "1m"],
+                    help="128k = the headline (configs[2]); 32k = configs[1]; serve / 1m = configs[3] / configs[4] "
+                         "(bench_configs.py)")
+    ap.add_argument("--shard-of", type=int, default=2, help="serve: hold rank 0's KV-head shard of N GPUs")
+    ap.add_argument("--topk", type=int, default=256, help="1m: select_topk_pages budget (pages per q head)")
     ap.add_argument("--slots", type=int, default=4, help="distinct resident layer-input sets")
     ap.add_argument("--tokens", type=int, default=0, help="override T (diagnostics only, not a reported config)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -462,6 +466,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-T", type=int, default=16384)
     args = ap.parse_args()
+    if args.config in ("serve", "1m"):
+        import bench_configs
+
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "secondary config; the reference arm runs on the "
+                              "headline config only"}))
+            return
+        bench_configs.main(args, load_peaks(), ClockSampler)
+        return
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
         cfg["T"] = args.tokens

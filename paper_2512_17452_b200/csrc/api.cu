@@ -474,7 +474,11 @@ int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const 
     else
         st = launch_vs_prefill_simt<float>(a, nseq, (const float*)q, (const float*)k_post, (const float*)v,
                                            (float*)out, ctx->stream);
-    if (st) return fail(st, std::string("vs prefill kernel: ") + cudaGetErrorString(cudaGetLastError()));
+    if (st) {
+        const std::string detail = wgkv_last_error();  // the launcher's own message, if it set one
+        return fail(st, std::string("vs prefill kernel: ") + cudaGetErrorString(cudaGetLastError()) +
+                            (detail.empty() ? "" : " [" + detail + "]"));
+    }
     return WGKV_OK;
 }
 
