@@ -247,18 +247,19 @@ def run_gpu(args, cfg):
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     launches = {"n": 0}
 
-    def prefill_layer(l, k3_events=None, inputs=None):
+    def prefill_layer(l, k3_events=None, inputs=None, out_buf=None):
         qi, ki, vi = inputs if inputs is not None else (Q[l % slots], K[l % slots], V[l % slots])
+        o_ = out if out_buf is None else out_buf
         check(lib.wgkv_gate_score(h, l, B, T, 0, P(ki), None, P(kpost), P(g_ws), P(bits_ws), None, 0, None), "K1")
         check(lib.wgkv_admit_prefill(h, l, 0, B, T, P(kpost), P(vi), P(g_ws), P(bits_ws)), "K2")
         if k3_events is not None:
             k3_events[0].record(stream)
-        check(lib.wgkv_vs_prefill(h, l, 0, B, T, P(qi), P(kpost), P(vi), P(bits_ws), P(out)), "K3")
+        check(lib.wgkv_vs_prefill(h, l, 0, B, T, P(qi), P(kpost), P(vi), P(bits_ws), P(o_)), "K3")
         if k3_events is not None:
             k3_events[1].record(stream)
         launches["n"] += 6  # rope table, gate, recheck, plan, scatter, vs
         if world > 1:
-            dist.all_gather_into_tensor(gath, out)  # rank-major head shards (C1)
+            dist.all_gather_into_tensor(gath, o_)  # rank-major head shards (C1)
 
     # One decode token-step over all layers, issued eagerly or replayed from a
     # CUDA graph captured once (kills per-kernel launch gaps); the step's new
@@ -276,6 +277,18 @@ def run_gpu(args, cfg):
                 dist.all_gather_into_tensor(dgath, dout)
 
     graph = {"g": None}
+
+    def _capture(fn):
+        """CUDA graph of fn's launches, captured on a side stream (recorded, not executed)."""
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        sess.set_stream(gs)
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_, stream=gs):
+            fn()
+        sess.set_stream(stream)
+        stream.wait_stream(gs)
+        return g_
 
     def decode_all(step0=0):
         for s_ in range(D):
@@ -377,53 +390,88 @@ def run_gpu(args, cfg):
         dv_h.copy_(vd[0])
         dout_h = torch.empty_like(dout, device="cpu").pin_memory()
         bufs = [(torch.empty_like(Q[0]), torch.empty_like(K[0]), torch.empty_like(V[0])) for _ in range(2)]
-        copy = torch.cuda.Stream(dev)
+        outs = [out, torch.empty_like(out)]
+        # three-stage pipeline on three streams: H2D of layer l+1's inputs, the
+        # layer's kernels, and D2H of layer l-1's output run concurrently (PCIe
+        # is full duplex); inputs and outputs are double-buffered
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ready = [torch.cuda.Event() for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
-        done_out = torch.cuda.Event()
+        computed = [torch.cuda.Event() for _ in range(2)]
+        drained = [torch.cuda.Event() for _ in range(2)]
         barrier()
         t0 = ev()
         t1 = ev()
         t0.record(stream)
+        h2d_s.wait_stream(stream)
+        d2h_s.wait_stream(stream)
         h2d = d2h = 0
+
+        def load(l):
+            b_ = l % 2
+            with torch.cuda.stream(h2d_s):
+                if l >= 2:
+                    h2d_s.wait_event(free[b_])  # layer l-2 has consumed this buffer
+                for dst, src in zip(bufs[b_], (hq_in[0], hk_in, hv_in)):
+                    dst.copy_(src, non_blocking=True)
+                ready[b_].record(h2d_s)
+
+        load(0)
         for l in range(L):
             b = l % 2
-            if l == 0:
-                with torch.cuda.stream(copy):
-                    for dst, src in zip(bufs[0], (hq_in[0], hk_in, hv_in)):
-                        dst.copy_(src, non_blocking=True)
-                    ready[0].record(copy)
-            if l + 1 < L:  # prefetch the next layer's inputs while this one computes
-                with torch.cuda.stream(copy):
-                    if l >= 1:
-                        copy.wait_event(free[(l + 1) % 2])
-                    for dst, src in zip(bufs[(l + 1) % 2], (hq_in[0], hk_in, hv_in)):
-                        dst.copy_(src, non_blocking=True)
-                    ready[(l + 1) % 2].record(copy)
+            if l + 1 < L:
+                load(l + 1)
             stream.wait_event(ready[b])
-            if l >= 1:
-                stream.wait_event(done_out)  # out buffer drained to host
-            prefill_layer(l, inputs=bufs[b])
+            if l >= 2:
+                stream.wait_event(drained[b])  # output of layer l-2 is on the host
+            prefill_layer(l, inputs=bufs[b], out_buf=outs[b])
             free[b].record(stream)
-            with torch.cuda.stream(copy):
-                copy.wait_stream(stream)
-                h_out.copy_(out, non_blocking=True)
-                done_out.record(copy)
+            computed[b].record(stream)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(computed[b])
+                h_out.copy_(outs[b], non_blocking=True)
+                drained[b].record(d2h_s)
             h2d += sum(x.numel() * x.element_size() for x in bufs[b])
             d2h += out.numel() * out.element_size()
-        stream.wait_event(done_out)
+        stream.wait_stream(d2h_s)
+        stream.wait_stream(h2d_s)
+        # decode: one CUDA graph per token-step (H2D of the step's q/k/v from a
+        # pinned staging slot, the 32 layers' kernels, D2H of the output), two
+        # graphs alternating over double-buffered staging slots
+        # per step: ONE H2D of every layer's q/k/v and ONE D2H of every layer's output
+        dq_d = torch.empty((L,) + tuple(qd[0][0].shape), dtype=torch.bfloat16, device=dev)
+        dk_d = torch.empty((L,) + tuple(kd[0][0].shape), dtype=torch.bfloat16, device=dev)
+        dv_d = torch.empty((L,) + tuple(vd[0][0].shape), dtype=torch.bfloat16, device=dev)
+        do_d = torch.empty((L,) + tuple(dout.shape), dtype=torch.bfloat16, device=dev)
+        stage = [[torch.empty_like(x, device="cpu").pin_memory() for x in (dq_d, dk_d, dv_d, do_d)] for _ in range(2)]
+
+        def e2e_step(b):
+            sq_h, sk_h, sv_h, so_h = stage[b]
+            dq_d.copy_(sq_h, non_blocking=True)
+            dk_d.copy_(sk_h, non_blocking=True)
+            dv_d.copy_(sv_h, non_blocking=True)
+            for l in range(L):
+                check(lib.wgkv_decode_layer(h, l, 0, B, P(dq_d[l]), P(dk_d[l]), P(dv_d[l]), None, P(do_d[l]), None,
+                                            None), "dec")
+            so_h.copy_(do_d, non_blocking=True)
+
+        e2e_graphs = [_capture(lambda b=b: e2e_step(b)) for b in range(2)] if not args.no_graphs else None
+        step_done = [torch.cuda.Event() for _ in range(2)]
         t_mid = ev()
         t_mid.record(stream)
-        dq_d, dk_d, dv_d = torch.empty_like(qd[0][0]), torch.empty_like(kd[0][0]), torch.empty_like(vd[0][0])
         for s_ in range(D):
-            for l in range(L):
-                dq_d.copy_(dq_h[s_], non_blocking=True)
-                dk_d.copy_(dk_h[s_], non_blocking=True)
-                dv_d.copy_(dv_h[s_], non_blocking=True)
-                check(lib.wgkv_decode_layer(h, l, 0, B, P(dq_d), P(dk_d), P(dv_d), None, P(dout), None, None), "dec")
-                dout_h.copy_(dout, non_blocking=True)
-                h2d += 3 * dq_d.numel() * dq_d.element_size()
-                d2h += dout.numel() * dout.element_size()
+            b = s_ % 2
+            if s_ >= 2:
+                step_done[b].synchronize()  # the slot's previous step has drained
+            for dst, src in zip(stage[b][:3], (dq_h[s_], dk_h[s_], dv_h[s_])):
+                dst.copy_(src.unsqueeze(0).expand_as(dst))  # this step's token inputs of every layer
+            if e2e_graphs:
+                e2e_graphs[b].replay()
+            else:
+                e2e_step(b)
+            step_done[b].record(stream)
+            h2d += sum(x.numel() * x.element_size() for x in (dq_d, dk_d, dv_d))
+            d2h += do_d.numel() * do_d.element_size()
         t1.record(stream)
         barrier()
         sess.release(0, B)
@@ -435,8 +483,11 @@ def run_gpu(args, cfg):
         e2e_pre, e2e_dec = mx.tolist()
         e2e = {"value": B * T / e2e_pre, "unit": "tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "decode_tok_s_per_gpu": B * D / e2e_dec / world,
-               "note": "one step through the C-ABI from pinned host buffers: per layer H2D of Q/K/V (double-buffered "
-                       "on a copy stream) and D2H of the attention output; decode H2D q/k/v + D2H out per layer"}
+               "note": "one step through the C-ABI from pinned host buffers. Prefill: per layer H2D of Q/K/V and D2H "
+                       "of the attention output, on their own streams (PCIe full duplex) overlapping the layer "
+                       "kernels, inputs and outputs double-buffered. Decode: per token-step a CUDA graph of one H2D "
+                       "of the 32 layers' q/k/v, the layers' kernels and one D2H of their outputs, from "
+                       "double-buffered pinned staging slots the host fills each step"}
 
     if world > 1:
         dist.barrier()
