@@ -71,7 +71,16 @@ typedef struct wgkv_config {
     long topk_budget;    /* 0: attend all Global pages; >0: select_topk_pages (engine.cpp:36-84) */
     int attn_impl;       /* WGKV_ATTN_* */
     int device;          /* CUDA device ordinal */
+    int topk_mode;       /* WGKV_TOPK_*: how select_topk_pages scores a page (topk_budget > 0) */
 } wgkv_config;
+
+/* page score used by the top-k selection (wgkv_config.topk_mode)
+ *   EXACT  max over the page's slots of q.k -- the reference's select_topk_pages
+ *          (engine.cpp:36-84); parity mode
+ *   QUEST  Quest's upper bound sum_d max(q_d min_d, q_d max_d) over per-page
+ *          elementwise key min / max kept on device; reads 1/8 of the Global K
+ *          bytes per step, NOT the reference's selection (approximate) */
+enum { WGKV_TOPK_EXACT = 0, WGKV_TOPK_QUEST = 1 };
 
 typedef struct wgkv_ctx wgkv_ctx;
 

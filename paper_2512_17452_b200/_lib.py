@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("WGKV_LIB") or os.path.join(HERE, "libwgkv_b200.so")  
 OK, EINVAL, ENOPAGES, ESTATE, ERUNTIME, ECUDA, ENOTSUP = range(7)
 BF16, F32 = 0, 1
 ATTN_AUTO, ATTN_SIMT, ATTN_TCGEN05 = 0, 1, 2
+TOPK_EXACT, TOPK_QUEST = 0, 1  # wgkv_config.topk_mode
 
 
 class WgkvError(RuntimeError):
@@ -41,7 +42,7 @@ class Config(C.Structure):
                 ("head_dim", C.c_int), ("hidden", C.c_int), ("window", C.c_long), ("tau", C.c_double),
                 ("rope_base", C.c_double), ("page_size", C.c_int), ("max_seqs", C.c_int), ("max_tokens", C.c_long),
                 ("max_prefill_tokens", C.c_long), ("capacity_pages", C.c_long), ("dtype", C.c_int),
-                ("topk_budget", C.c_long), ("attn_impl", C.c_int), ("device", C.c_int)]
+                ("topk_budget", C.c_long), ("attn_impl", C.c_int), ("device", C.c_int), ("topk_mode", C.c_int)]
 
 
 _vp, _i, _l = C.c_void_p, C.c_int, C.c_long

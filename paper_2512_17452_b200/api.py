@@ -47,13 +47,15 @@ class Session:
 
     def __init__(self, layers, q_heads, kv_heads, head_dim, hidden, window, tau=0.1, rope_base=10000.0,
                  page_size=16, max_seqs=1, max_tokens=4096, max_prefill_tokens=None, capacity_pages=0,
-                 dtype=BF16, topk_budget=0, attn_impl=ATTN_AUTO, device=0, kv_head_offset=0, gate_bank=None):
+                 dtype=BF16, topk_budget=0, attn_impl=ATTN_AUTO, device=0, kv_head_offset=0, gate_bank=None,
+                 topk_mode=0):
         self.lib = _lib.load()
         cfg = _lib.Config(layers=layers, q_heads=q_heads, kv_heads=kv_heads, kv_head_offset=kv_head_offset,
                           head_dim=head_dim, hidden=hidden, window=window, tau=tau, rope_base=rope_base,
                           page_size=page_size, max_seqs=max_seqs, max_tokens=max_tokens,
                           max_prefill_tokens=max_prefill_tokens or max_tokens, capacity_pages=capacity_pages,
-                          dtype=dtype, topk_budget=topk_budget, attn_impl=attn_impl, device=device)
+                          dtype=dtype, topk_budget=topk_budget, attn_impl=attn_impl, device=device,
+                          topk_mode=topk_mode)
         self.cfg = cfg
         self.device = torch.device("cuda", device)
         self.dtype = _TORCH_DT[dtype]

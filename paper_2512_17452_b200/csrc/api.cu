@@ -92,6 +92,8 @@ struct wgkv_ctx {
     unsigned long long* ws_thr = nullptr;  // K6: [S][Hq] selection thresholds
     uint8_t* ws_umask = nullptr;           // K6: [S][H][n_gp] union q-head masks
     int* ws_ucnt = nullptr;                // K6: [S][H][ceil(n_gp/1024)] union block counts
+    __nv_bfloat16* quest_meta = nullptr;   // K6 Quest mode: [capacity][min 128 | max 128]
+    int* quest_full = nullptr;             // K6 Quest mode: [L][S][H] pages whose metadata is final
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int max_chunks = kMaxChunks;
@@ -151,6 +153,10 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     if (c.page_size < 1 || c.page_size > 32) return fail(WGKV_ENOTSUP, "page_size must be in [1, 32]");
     if (c.hidden < 1 || c.max_seqs < 1 || c.max_tokens < 1) return fail(WGKV_EINVAL, "bad sizes");
     if (c.dtype != WGKV_BF16 && c.dtype != WGKV_F32) return fail(WGKV_EINVAL, "bad dtype");
+    if (c.topk_mode != WGKV_TOPK_EXACT && c.topk_mode != WGKV_TOPK_QUEST) return fail(WGKV_EINVAL, "bad topk_mode");
+    if (c.topk_mode == WGKV_TOPK_QUEST &&
+        (c.dtype != WGKV_BF16 || c.head_dim != 128 || c.page_size != 16 || c.q_heads / c.kv_heads > 8))
+        return fail(WGKV_ENOTSUP, "Quest page selection needs bf16, head_dim 128, page 16, GQA group <= 8");
     if (cudaSetDevice(c.device) != cudaSuccess) return fail(WGKV_ECUDA, "cudaSetDevice failed");
 
     auto* ctx = new wgkv_ctx();
@@ -219,6 +225,10 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
         ctx->ws_thr = dalloc<unsigned long long>((size_t)S * c.q_heads, o);
         ctx->ws_umask = dalloc<uint8_t>((size_t)S * H * n_gp, o);
         ctx->ws_ucnt = dalloc<int>((size_t)S * H * ((n_gp + 1023) / 1024), o);
+        if (c.topk_mode == WGKV_TOPK_QUEST) {
+            ctx->quest_meta = dalloc<__nv_bfloat16>((size_t)cap * 2 * d, o);
+            ctx->quest_full = dalloc<int>((size_t)L * S * H, o);
+        }
     }
     for (void* p : o)
         if (!p) {
@@ -447,6 +457,9 @@ int wgkv_admit_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, con
         ctx->prefilled[(size_t)layer * ctx->cfg.max_seqs + s] = 1;
         ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] = T;
     }
+    if (ctx->quest_full)  // fresh Global pages: their Quest metadata is rebuilt at the next decode
+        WGKV_CUDA_TRY(cudaMemsetAsync(ctx->quest_full + ctx->pv.head_index(layer, seq0, 0), 0,
+                                      sizeof(int) * (size_t)nseq * ctx->cfg.kv_heads, ctx->stream));
     return WGKV_OK;
 }
 
@@ -569,12 +582,12 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
         if (c.dtype == WGKV_BF16)
             st = launch_topk_decode<__nv_bfloat16>(a, nseq, c.topk_budget, (const __nv_bfloat16*)q, ctx->ws_score,
                                                    ctx->ws_sel, ctx->ws_nsel, ctx->ws_thr, ctx->ws_umask,
-                                                   ctx->ws_ucnt, ctx->ws_part,
-                                                   ctx->ws_nchunks, (__nv_bfloat16*)out, ctx->stream);
+                                                   ctx->ws_ucnt, ctx->ws_part, ctx->ws_nchunks, (__nv_bfloat16*)out,
+                                                   c.topk_mode, ctx->quest_meta, ctx->quest_full, ctx->stream);
         else
             st = launch_topk_decode<float>(a, nseq, c.topk_budget, (const float*)q, ctx->ws_score, ctx->ws_sel,
                                            ctx->ws_nsel, ctx->ws_thr, ctx->ws_umask, ctx->ws_ucnt, ctx->ws_part,
-                                           ctx->ws_nchunks, (float*)out,
+                                           ctx->ws_nchunks, (float*)out, c.topk_mode, nullptr, nullptr,
                                            ctx->stream);
         if (st) return fail(st, std::string("topk decode: ") + cudaGetErrorString(cudaGetLastError()));
         return WGKV_OK;
@@ -735,11 +748,15 @@ int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq) {
     if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
     release_kernel<<<c.layers * nseq * c.kv_heads, 256, 0, ctx->stream>>>(ctx->pv, c.layers, seq0, nseq);
     WGKV_CUDA_TRY(cudaGetLastError());
-    for (int l = 0; l < c.layers; ++l)
+    for (int l = 0; l < c.layers; ++l) {
         for (int s = seq0; s < seq0 + nseq; ++s) {
             ctx->prefilled[(size_t)l * c.max_seqs + s] = 0;
             ctx->tokens[(size_t)l * c.max_seqs + s] = 0;
         }
+        if (ctx->quest_full)
+            WGKV_CUDA_TRY(cudaMemsetAsync(ctx->quest_full + ctx->pv.head_index(l, seq0, 0), 0,
+                                          sizeof(int) * (size_t)nseq * c.kv_heads, ctx->stream));
+    }
     return WGKV_OK;
 }
 

@@ -38,7 +38,7 @@ struct DecArgs {
 template <typename E>
 int launch_topk_decode(const DecArgs& a, int nseq, long budget, const E* q, float* scores, int32_t* sel,
                        int32_t* nsel, unsigned long long* thr, uint8_t* umask, int* ucnt, float* part, int* nchunks,
-                       E* out, cudaStream_t st);
+                       E* out, int mode, __nv_bfloat16* meta, int* meta_full, cudaStream_t st);
 
 // counter_reset_by_append: K4 ran just before on the stream and zeroed the
 // work counter; K5 is then launched as its programmatic dependent (PDL)

@@ -2,6 +2,8 @@
 // selected Global pages and the Local ring, per q head (wgkv_plus_topk,
 // engine.cpp:320-324; BASELINE configs[4]).
 //
+//   quest_meta/score       WGKV_TOPK_QUEST: Quest's upper bound from per-page
+//                          key min / max (approximate; not the reference's)
 //   topk_score_mma_kernel  page score = max over the page's slots of the
 //                          UNSCALED q.k (q RoPE'd at the decode position) for
 //                          every q head of the GQA group, on the tensor pipe
@@ -205,6 +207,118 @@ __global__ void __launch_bounds__(SC_WARPS * 32) topk_score_mma_kernel(DecArgs a
                 if (g0 < gs) dst[0] = m0;
                 if (g0 + 1 < gs) dst[a.pv.n_gp] = m1;
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Quest bound (wgkv_config.topk_mode = WGKV_TOPK_QUEST; not the reference's
+// selection): score(page) = sum_d max(q_d min_d, q_d max_d) >= max_slot q.k,
+// from per-page elementwise key min / max (bf16: exact for the bf16 keys),
+// 512 B per page instead of the page's 4 KB of K.  The metadata is kept
+// current incrementally: quest_meta_kernel recomputes Global pages
+// [meta_full, ng) of each head (after a prefill all of them, then the tail page
+// and pages filled since), quest_score_kernel advances meta_full to the count
+// of full pages (a later launch, so the meta kernel's blocks all read the old
+// value).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) quest_meta_kernel(DecArgs a, const int* __restrict__ meta_full,
+                                                         __nv_bfloat16* __restrict__ meta) {
+    constexpr int d = 128;
+    const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
+    const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
+    const HeadState st = a.pv.state[hidx];
+    const int ps = a.pv.page_size;
+    const int ng = (st.global_len + ps - 1) / ps;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(a.pv.data);
+    for (int lp = meta_full[hidx] + blockIdx.x * 8 + warp; lp < ng; lp += gridDim.x * 8) {
+        const int page = a.pv.gpt[hidx * a.pv.n_gp + lp];
+        if (page < 0) continue;
+        const int valid = min(ps, st.global_len - lp * ps);
+        const __nv_bfloat16* kr = pool + (size_t)page * a.pv.page_elems() + 4 * lane;
+        float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int r = 0; r < valid; ++r) {
+            const uint2 raw = __ldg(reinterpret_cast<const uint2*>(kr + (size_t)r * d));
+            const float x[4] = {__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xffff0000u),
+                                __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xffff0000u)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                mn[e] = fminf(mn[e], x[e]);
+                mx[e] = fmaxf(mx[e], x[e]);
+            }
+        }
+        __nv_bfloat16* mo = meta + (size_t)page * 2 * d + 4 * lane;  // [min 128 | max 128], exact in bf16
+        *reinterpret_cast<uint2*>(mo) = make_uint2(pack2(mn[0], mn[1]), pack2(mn[2], mn[3]));
+        *reinterpret_cast<uint2*>(mo + d) = make_uint2(pack2(mx[0], mx[1]), pack2(mx[2], mx[3]));
+    }
+}
+
+template <int QG>  // GQA group size
+__global__ void __launch_bounds__(256) quest_score_kernel(DecArgs a, const __nv_bfloat16* __restrict__ q,
+                                                          const __nv_bfloat16* __restrict__ meta,
+                                                          int* __restrict__ meta_full, float* __restrict__ scores) {
+    constexpr int d = 128, PPW = 2;  // pages per warp (all loads issued up front)
+    const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
+    const HeadState st = a.pv.state[hidx];
+    const int ps = a.pv.page_size;
+    const int ng = (st.global_len + ps - 1) / ps;
+    if (blockIdx.x == 0 && tid == 0) meta_full[hidx] = st.global_len / ps;
+    const int p0 = blockIdx.x * 8 * PPW;
+    if (p0 >= ng) return;
+    __shared__ float Qs[QG][d];
+    __shared__ int pid[8 * PPW];
+    if (tid < 8 * PPW) pid[tid] = p0 + tid < ng ? a.pv.gpt[hidx * a.pv.n_gp + p0 + tid] : -1;
+    const long pos = st.tokens_seen - 1;
+    for (int e = tid; e < QG * (d / 2); e += blockDim.x) {
+        const int g = e / (d / 2), i = e % (d / 2);
+        const size_t off = ((size_t)s * a.q_heads + h * QG + g) * d + 2 * i;
+        const float x0 = __bfloat162float(q[off]), x1 = __bfloat162float(q[off + 1]);
+        float c, sn;
+        rope_cs(a.freq, i, pos, c, sn);
+        Qs[g][2 * i] = x0 * c - x1 * sn;
+        Qs[g][2 * i + 1] = x0 * sn + x1 * c;
+    }
+    __syncthreads();
+    uint2 mn_raw[PPW], mx_raw[PPW];
+#pragma unroll
+    for (int u = 0; u < PPW; ++u) {
+        const int page = pid[warp * PPW + u];
+        const __nv_bfloat16* mp = meta + (size_t)max(page, 0) * 2 * d + 4 * lane;
+        mn_raw[u] = __ldg(reinterpret_cast<const uint2*>(mp));
+        mx_raw[u] = __ldg(reinterpret_cast<const uint2*>(mp + d));
+    }
+#pragma unroll
+    for (int u = 0; u < PPW; ++u) {
+        const int lp = p0 + warp * PPW + u;
+        if (lp >= ng) break;  // warp-uniform
+        const float mn[4] = {__uint_as_float(mn_raw[u].x << 16), __uint_as_float(mn_raw[u].x & 0xffff0000u),
+                             __uint_as_float(mn_raw[u].y << 16), __uint_as_float(mn_raw[u].y & 0xffff0000u)};
+        const float mx[4] = {__uint_as_float(mx_raw[u].x << 16), __uint_as_float(mx_raw[u].x & 0xffff0000u),
+                             __uint_as_float(mx_raw[u].y << 16), __uint_as_float(mx_raw[u].y & 0xffff0000u)};
+        float sc[QG];
+#pragma unroll
+        for (int g = 0; g < QG; ++g) {
+            float acc = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float qq = Qs[g][4 * lane + e];
+                acc += fmaxf(qq * mn[e], qq * mx[e]);
+            }
+            sc[g] = acc;
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+            for (int g = 0; g < QG; ++g) sc[g] += __shfl_xor_sync(0xffffffffu, sc[g], o);
+        if (lane < QG) {
+            float v = sc[0];
+#pragma unroll
+            for (int g = 1; g < QG; ++g) v = lane == g ? sc[g] : v;
+            scores[((size_t)s * a.q_heads + h * QG + lane) * a.pv.n_gp + lp] =
+                pid[warp * PPW + u] >= 0 ? v : -INFINITY;
         }
     }
 }
@@ -685,7 +799,7 @@ __global__ void topk_combine_kernel(DecArgs a, const float* __restrict__ part, E
 template <typename E>
 int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, float* scores, int32_t* sel,
                        int32_t* nsel, unsigned long long* thr, uint8_t* umask, int* ucnt, float* part, int* nchunks,
-                       E* out, cudaStream_t st) {
+                       E* out, int mode, __nv_bfloat16* meta, int* meta_full, cudaStream_t st) {
     DecArgs a = a0;
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
     if (d % 32 != 0 || d > 256) return WGKV_ENOTSUP;
@@ -693,7 +807,19 @@ int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, flo
     // bf16 production path: tensor-pipe scoring + union selection streamed by K5
     constexpr bool kBf16 = sizeof(E) == 2;
     const bool fast = kBf16 && d == 128 && a.pv.page_size == 16 && gs <= 8 && a.pv.capacity < (1L << 24);
-    if (fast && gs <= 4)
+    if (mode == WGKV_TOPK_QUEST) {
+        if (!fast || !meta || !meta_full) return WGKV_ENOTSUP;
+        quest_meta_kernel<<<dim3(16, nseq * a.pv.kv_heads), 256, 0, st>>>(a, meta_full, meta);
+        const dim3 qgrid((max_pages + 15) / 16, nseq * a.pv.kv_heads);
+        const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(q);
+        switch (gs) {
+            case 1: quest_score_kernel<1><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
+            case 2: quest_score_kernel<2><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
+            case 4: quest_score_kernel<4><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
+            case 8: quest_score_kernel<8><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
+            default: return WGKV_ENOTSUP;
+        }
+    } else if (fast && gs <= 4)
         topk_score_mma_kernel<<<dim3((max_pages + SC_PAGES - 1) / SC_PAGES, nseq * a.pv.kv_heads), SC_WARPS * 32, 0,
                                 st>>>(a, reinterpret_cast<const __nv_bfloat16*>(q), scores);
     else
@@ -730,9 +856,10 @@ int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, flo
 }
 
 template int launch_topk_decode<float>(const DecArgs&, int, long, const float*, float*, int32_t*, int32_t*,
-                                       unsigned long long*, uint8_t*, int*, float*, int*, float*, cudaStream_t);
+                                       unsigned long long*, uint8_t*, int*, float*, int*, float*, int,
+                                       __nv_bfloat16*, int*, cudaStream_t);
 template int launch_topk_decode<__nv_bfloat16>(const DecArgs&, int, long, const __nv_bfloat16*, float*, int32_t*,
                                                int32_t*, unsigned long long*, uint8_t*, int*, float*, int*,
-                                               __nv_bfloat16*, cudaStream_t);
+                                               __nv_bfloat16*, int, __nv_bfloat16*, int*, cudaStream_t);
 
 }  // namespace wgkv

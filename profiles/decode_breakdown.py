@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--topk", type=int, default=0, help="topk_budget (Global pages per q head; 0 = all)")
+    ap.add_argument("--quest", action="store_true", help="topk_mode = WGKV_TOPK_QUEST (page min/max bound)")
     args = ap.parse_args()
     B, T, Hq, Hkv, d = args.batch, args.T, args.hq, args.hkv, 128
     dev = torch.device("cuda", 0)
@@ -37,7 +38,8 @@ def main():
     bank = np.zeros((1, Hkv, d * 2 * d + 2 * d + 1))
     bank[..., : d * 2 * d] = 0.02 * np.random.default_rng(0).standard_normal((1, Hkv, d * 2 * d))
     s = W.Session(1, Hq, Hkv, d, d, 1024, rope_base=5e5, max_seqs=B, max_tokens=T + 3 * args.iters + 8,
-                  max_prefill_tokens=T, attn_impl=args.impl, gate_bank=bank, topk_budget=args.topk)
+                  max_prefill_tokens=T, attn_impl=args.impl, gate_bank=bank, topk_budget=args.topk,
+                  topk_mode=W.TOPK_QUEST if args.quest else W.TOPK_EXACT)
     q = torch.randn(B, T, Hq, d, device=dev, generator=g).to(torch.bfloat16)
     k = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
     v = torch.randn(B, T, Hkv, d, device=dev, generator=g).to(torch.bfloat16)
@@ -58,7 +60,8 @@ def main():
         n_loc = min(T, 1024)
         n_glob = (st["resident_entries"] / (B * Hkv)) - n_loc
         sel = min(args.topk * 16, n_glob)
-        res_bytes = B * Hkv * (n_glob * d * 2 + (Hq // Hkv) * (sel + n_loc) * 2 * d * 2)
+        score_bytes = n_glob / 16 * 2 * d * 2 if args.quest else n_glob * d * 2  # page min/max vs every K row
+        res_bytes = B * Hkv * (score_bytes + (Hq // Hkv) * (sel + n_loc) * 2 * d * 2)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     for _ in range(5):
         check(lib.wgkv_decode_attn(h, 0, 0, B, P(qd), P(out)))

@@ -349,3 +349,56 @@ def test_topk_all_ties_take_oldest(W, dtype, T):
     o = out.double().cpu().numpy()[0]
     for p in range(hq):
         assert rel_err(o[p], ref) < TOL[dtype], p
+
+
+@pytest.mark.parametrize("budget", [2, 5])
+def test_topk_quest_bound_vs_numpy(W, orc, budget):
+    """WGKV_TOPK_QUEST (not the reference's selection): pages ranked by Quest's
+    bound sum_d max(q_d min_d, q_d max_d) over each Global page's key min / max,
+    top-`budget` (ties to the older page), attention over them + the Local ring.
+    Checked against numpy on the exported cache after every decode step (the
+    metadata is rebuilt after prefill and kept current as promotions append)."""
+    d, hq, hkv, T, steps, Wn = 128, 8, 2, 600, 12, 64
+    gs = hq // hkv
+    bank = orc.gate_random_init(1, hkv, d, d, 51, 0.1, -1.5)
+    q = bf16_np(orc.gaussian(52, (T + steps) * hq * d).reshape(1, T + steps, hq, d))
+    k = bf16_np(orc.gaussian(53, (T + steps) * hkv * d).reshape(1, T + steps, hkv, d))
+    v = bf16_np(orc.gaussian(54, (T + steps) * hkv * d).reshape(1, T + steps, hkv, d))
+    for t in range(0, T, 40):
+        k[0, t] = bf16_np(k[0, t] * 1.5)
+    dt = torch.bfloat16
+    s = W.Session(1, hq, hkv, d, d, Wn, max_tokens=T + steps, gate_bank=bank, topk_budget=budget,
+                  topk_mode=W.TOPK_QUEST)
+    s.prefill_layer(0, to_dev(q[:, :T], dt), to_dev(k[:, :T], dt), to_dev(v[:, :T], dt))
+    near_ties = checks = 0
+    for t in range(T, T + steps):
+        o = s.decode_layer(0, to_dev(q[:, t], dt), to_dev(k[:, t], dt), to_dev(v[:, t], dt)).float().cpu().numpy()[0]
+        for h in range(hkv):
+            c = s.gather(0, 0, h)
+            gk, gv, lk, lv = (np.asarray(c[x], np.float64) for x in ("global_k", "global_v", "local_k", "local_v"))
+            n = -(-gk.shape[0] // 16)
+            mn = np.stack([gk[16 * i:16 * i + 16].min(0) for i in range(n)]) if n else np.zeros((0, d))
+            mx = np.stack([gk[16 * i:16 * i + 16].max(0) for i in range(n)]) if n else np.zeros((0, d))
+            for g in range(gs):
+                p = h * gs + g
+                qr = orc.rope(q[0, t, p], t)
+                bound = np.maximum(qr * mn, qr * mx).sum(1)
+                order = sorted(range(n), key=lambda i: (-bound[i], i))  # higher first, ties to older
+                kk = min(budget, n)
+                sel = sorted(order[:kk])
+                rows = np.concatenate([np.arange(16 * i, min(16 * i + 16, gk.shape[0])) for i in sel]) if sel else \
+                    np.zeros(0, int)
+                keys = np.concatenate([gk[rows], lk])
+                vals = np.concatenate([gv[rows], lv])
+                lg = keys @ qr / math.sqrt(d)
+                w = np.exp(lg - lg.max())
+                ref = (w[:, None] * vals).sum(0) / w.sum()
+                checks += 1
+                if rel_err(o[p], ref) < TOL["bf16"]:
+                    continue
+                srt = sorted(bound, reverse=True)
+                assert kk < n, (t, p)
+                gap = (srt[kk - 1] - srt[kk]) / max(abs(srt[kk - 1]), 1e-30)
+                assert gap < 3e-2, (t, p, gap)
+                near_ties += 1
+    assert near_ties <= checks // 4, (near_ties, checks)
