@@ -170,6 +170,42 @@ __global__ void __launch_bounds__(128) admit_scatter_kernel(PoolView pv, int lay
     }
     unsigned mv = __ballot_sync(0xffffffffu, dpage >= 0);
     E* pool = reinterpret_cast<E*>(pv.data);
+    if (d * sizeof(E) == 256) {
+        // 256-byte rows (bf16, d = 128): a half warp moves one row with 16-byte
+        // vectors, so a warp moves 2 rows per instruction; up to 8 rows' K and V
+        // loads are issued before their stores (bytes in flight, not latency)
+        const int hw = lane >> 4, hl = lane & 15;
+        while (mv) {
+            int4 kr[4], vr[4];
+            int4* kd[4];
+            bool on[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                // rows 2u and 2u+1 of this batch: the (2u + hw)-th remaining lane of mv
+                unsigned m2 = mv;
+                for (int k = 0; k < 2 * u + hw && m2; ++k) m2 &= m2 - 1;
+                on[u] = m2 != 0;
+                const int src = on[u] ? __ffs(m2) - 1 : 0;
+                const int p = __shfl_sync(0xffffffffu, dpage, src);
+                const int sl = __shfl_sync(0xffffffffu, dslot, src);
+                const long ts = (long)c * ADM_CHUNK + wid * 32 + src;
+                const size_t row = (((size_t)s * T + ts) * pv.kv_heads + h) * d;
+                kd[u] = reinterpret_cast<int4*>(pool + (size_t)max(p, 0) * pv.page_elems() + (size_t)sl * d) + hl;
+                if (on[u]) {
+                    kr[u] = __ldg(reinterpret_cast<const int4*>(k_post + row) + hl);
+                    vr[u] = __ldg(reinterpret_cast<const int4*>(v + row) + hl);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (on[u]) {
+                    kd[u][0] = kr[u];
+                    kd[u][(size_t)ps * d * sizeof(E) / 16] = vr[u];
+                }
+            for (int k = 0; k < 8 && mv; ++k) mv &= mv - 1;
+        }
+        return;
+    }
     while (mv) {
         const int src = __ffs(mv) - 1;
         mv &= mv - 1;
