@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
 // concurrently with K5 (nothing reads the new slot's bit until it is the ring
 // victim W steps later).
 template <typename E>
-__global__ void __launch_bounds__(256) decode_gate_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
+__global__ void __launch_bounds__(1024) decode_gate_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
                                                            const E* __restrict__ k_pre, float* __restrict__ g_out,
                                                            const int* __restrict__ slot_rec) {
     extern __shared__ double dsh[];
@@ -405,7 +405,8 @@ __device__ __forceinline__ void gate_section(const PoolView& pv, const GateArgs&
             xs[d + 2 * i + 1] = x0 * sd + x1 * cd;
         }
         __syncthreads();
-        g = gate_fp64_block(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch);
+        g = d == 128 ? gate_fp64_block<256>(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch)
+                     : gate_fp64_block(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch);
     }
     if (tid == 0) {
         if (npage >= 0) {
@@ -429,7 +430,8 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     if (split) {  // fork: the gate on the side stream, joined by the caller with ev_join
         cudaEventRecord(ev_fork, st);
         cudaStreamWaitEvent(side, ev_fork, 0);
-        decode_gate_kernel<E><<<nseq * pv.kv_heads, 256, smem, side>>>(pv, ga, layer, seq0, k_pre, g_out, slot_rec);
+        // 1024 threads: 32 warps x 4 hidden units cover hidden = 128 in one pass
+        decode_gate_kernel<E><<<nseq * pv.kv_heads, 1024, smem, side>>>(pv, ga, layer, seq0, k_pre, g_out, slot_rec);
         cudaEventRecord(ev_join, side);
     }
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <fstream>
 #include <string>
 #include <vector>
@@ -622,7 +623,8 @@ int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* 
     const bool fused = fast_decode(ctx->cfg) && ctx->cfg.topk_budget == 0;
     int* counter = fused ? ctx->ws_nchunks + (size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads : nullptr;
     // the new token's gate forks onto the side stream and runs alongside K5
-    const bool split = !forced_g;
+    static const bool inline_gate = getenv("WGKV_DECODE_GATE_INLINE") != nullptr;  // A/B switch
+    const bool split = !forced_g && !inline_gate;
     int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, counter, split);
     if (st) return st;
     st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, fused);

@@ -24,6 +24,9 @@ constexpr int DNS = 3;       // ring stages per warp (2 CTAs / SM)
 constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
 constexpr int QROW = 136;    // padded Q row (bf16 elements)
 constexpr int PID_CAP = 2048;  // pages per work item (staged page ids)
+#ifndef WGKV_K5_MIN_PAGES
+#define WGKV_K5_MIN_PAGES 8
+#endif
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
         }
         // ~2 items per CTA, taken dynamically (work stealing) for balance
         int cp = (int)((total + 2 * gridDim.x - 1) / (2 * gridDim.x));
-        cp = max(cp, 8);
+        cp = max(cp, WGKV_K5_MIN_PAGES);  // per-item fixed costs (page ids, ring fill, merge) amortised
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
         s_cp = cp;

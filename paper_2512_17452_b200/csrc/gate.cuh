@@ -117,10 +117,11 @@ __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, con
 // sequential order by O(1e-16) relative, so bits can only differ where
 // |g - tau| < 1e-14 -- far inside the reported 1e-6 band.
 // scratch: smem >= 2*hidden + 32 doubles.  Returns g on every thread.
+template <int FD = 0>  // FD = 2d when known at compile time: the k loop unrolls, every W1 load in flight
 __device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, const double* xs, int d,
                                                   double* scratch) {
     const int tid = threadIdx.x, nt = blockDim.x, hid = gd.hidden, lane = tid & 31, nw = nt >> 5;
-    const int fd = 2 * d;
+    const int fd = FD > 0 ? FD : 2 * d;
     const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
@@ -129,11 +130,25 @@ __device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, co
     const int G4 = 4;
     for (int h0 = (tid >> 5) * G4; h0 < hid; h0 += nw * G4) {
         double s[G4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = lane; k < fd; k += 32) {
-            const double x = xs[k];
+        if constexpr (FD > 0) {
+            double wv[FD / 32][G4];
 #pragma unroll
-            for (int g = 0; g < G4; ++g)
-                if (h0 + g < hid) s[g] = fma(w1[(size_t)(h0 + g) * fd + k], x, s[g]);
+            for (int j = 0; j < FD / 32; ++j)
+#pragma unroll
+                for (int g = 0; g < G4; ++g) wv[j][g] = h0 + g < hid ? w1[(size_t)(h0 + g) * fd + lane + 32 * j] : 0.0;
+#pragma unroll
+            for (int j = 0; j < FD / 32; ++j) {
+                const double x = xs[lane + 32 * j];
+#pragma unroll
+                for (int g = 0; g < G4; ++g) s[g] = fma(wv[j][g], x, s[g]);
+            }
+        } else {
+            for (int k = lane; k < fd; k += 32) {
+                const double x = xs[k];
+#pragma unroll
+                for (int g = 0; g < G4; ++g)
+                    if (h0 + g < hid) s[g] = fma(w1[(size_t)(h0 + g) * fd + k], x, s[g]);
+            }
         }
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1)
