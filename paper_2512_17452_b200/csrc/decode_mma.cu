@@ -336,10 +336,11 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     const int gs = a.q_heads / a.pv.kv_heads;
     if (a.pv.head_dim != 128 || a.pv.page_size != 16 || gs > 16) return WGKV_ENOTSUP;
     // cached per pool (a new context may reuse a freed pool's address with
-    // another capacity, so the key includes it)
-    static CUtensorMap tp;
-    static const void* tp_base = nullptr;
-    static long tp_cap = -1;
+    // another capacity, so the key includes it); per host thread, since each
+    // context is driven by one host thread
+    static thread_local CUtensorMap tp;
+    static thread_local const void* tp_base = nullptr;
+    static thread_local long tp_cap = -1;
     if (tp_base != a.pv.data || tp_cap != a.pv.capacity) {
         if (make_tmap_3d_bf16(&tp, a.pv.data, 128, 16, 2 * (uint64_t)a.pv.capacity, 256, 16 * 256, 64, 16, 1))
             return WGKV_ECUDA;
