@@ -5,8 +5,9 @@
 // attention.cpp:155-180) for Session::decode_step (engine.cpp:309-326).
 // Grid = (page chunks, seq x kv head).  Each CTA serves the whole GQA group
 // (every K/V byte is read from HBM once per group), 4 warps stream pages
-// independently through a 4-deep per-warp TMA ring (one 16-token page = K 4 KB
-// + V 4 KB, SWIZZLE_128B so ldmatrix is conflict-free), and compute with
+// independently through a 3-deep per-warp TMA ring (one 16-token page = K 4 KB
+// + V 4 KB, ONE 4-D TMA box per page through a transposed view of the pool,
+// SWIZZLE_128B so ldmatrix is conflict-free), and compute with
 // mma.sync m16n8k16 (bf16 -> fp32): S = Q K^T with the group's q heads as
 // rows, P V with P re-used from the S accumulators in registers.  The CTA
 // merges its warps; decode_combine_kernel (attn_simt.cu) merges chunks.
@@ -187,10 +188,9 @@ __global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __gri
             uint8_t* dst = ring + (warp * DNS + slot) * PAGE_B;
             uint64_t* bar = &full[warp * DNS + slot];
             tc::mbar_arrive_expect_tx(bar, PAGE_B);
-            tc::tma_load_3d(dst, &tpool, bar, 0, 0, 2 * page);
-            tc::tma_load_3d(dst + 2048, &tpool, bar, 64, 0, 2 * page);
-            tc::tma_load_3d(dst + 4096, &tpool, bar, 0, 0, 2 * page + 1);
-            tc::tma_load_3d(dst + 6144, &tpool, bar, 64, 0, 2 * page + 1);
+            // one box per page: {64 dims, 16 slots, 2 dim halves, K and V} lands as
+            // K lo | K hi | V lo | V hi, each a [16][64] SW128 sub-tile
+            tc::tma_load_4d(dst, &tpool, bar, 0, 0, 0, 2 * page);
         };
         if (lane == 0) {
             tc::fence_proxy_async_smem();
@@ -342,7 +342,12 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     static thread_local const void* tp_base = nullptr;
     static thread_local long tp_cap = -1;
     if (tp_base != a.pv.data || tp_cap != a.pv.capacity) {
-        if (make_tmap_3d_bf16(&tp, a.pv.data, 128, 16, 2 * (uint64_t)a.pv.capacity, 256, 16 * 256, 64, 16, 1))
+        // pool as [2*cap planes][2 dim halves][16 slots][64 dims] (the half stride is
+        // smaller than the slot stride: a transposed view of [plane][slot][128])
+        const uint64_t dims[4] = {64, 16, 2, 2 * (uint64_t)a.pv.capacity};
+        const uint64_t strides[3] = {256, 128, 16 * 256};
+        const uint32_t box[4] = {64, 16, 2, 2};
+        if (make_tmap_4d_bf16(&tp, a.pv.data, dims, strides, box))
             return WGKV_ECUDA;
         tp_base = a.pv.data;
         tp_cap = a.pv.capacity;
