@@ -20,8 +20,18 @@ namespace wgkv {
 
 namespace {
 
-constexpr int DW = 4;        // warps per CTA
-constexpr int DNS = 3;       // ring stages per warp (2 CTAs / SM)
+#ifndef WGKV_K5_DW
+#define WGKV_K5_DW 4
+#endif
+#ifndef WGKV_K5_DNS
+#define WGKV_K5_DNS 3
+#endif
+#ifndef WGKV_K5_CPS
+#define WGKV_K5_CPS 2
+#endif
+constexpr int DW = WGKV_K5_DW;    // warps per CTA
+constexpr int DNS = WGKV_K5_DNS;  // ring stages per warp
+constexpr int CPS = WGKV_K5_CPS;  // CTAs per SM
 constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
 constexpr int QROW = 136;    // padded Q row (bf16 elements)
 constexpr int PID_CAP = 2048;  // pages per work item (staged page ids)
@@ -63,7 +73,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, uint32_t row, uint32_t ch
 // (a.sel / a.nsel: logical page | q-head mask << 24) instead of every page;
 // rows (q heads) that did not select a page get -inf logits for it.
 template <bool TOPK>
-__global__ void __launch_bounds__(DW * 32, 2) decode_attn_mma_kernel(const __grid_constant__ CUtensorMap tpool,
+__global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __grid_constant__ CUtensorMap tpool,
                                                                       DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                       float* __restrict__ part,
                                                                       int* __restrict__ nchunks,
@@ -355,7 +365,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     a.n_pairs = nseq * a.pv.kv_heads;
     const size_t smem =
         1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
-    if (smem > 113 * 1024) return WGKV_ENOTSUP;
+    if (smem > (size_t)(228 / CPS - 1) * 1024) return WGKV_ENOTSUP;
     const bool topk = a.sel != nullptr;
     auto kern = topk ? decode_attn_mma_kernel<true> : decode_attn_mma_kernel<false>;
     static size_t smem_set[2] = {0, 0};  // host-side only; keeps graph capture free of attribute calls
@@ -368,7 +378,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     int* counter = nchunks + (size_t)a.pv.max_seqs * a.pv.kv_heads;
     if (!counter_reset_by_append) cudaMemsetAsync(counter, 0, sizeof(int), st);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * kNumSMs);
+    cfg.gridDim = dim3(CPS * kNumSMs);
     cfg.blockDim = dim3(DW * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
