@@ -34,6 +34,10 @@
 #include "attn_tc.cuh"
 #include "tc.cuh"
 
+#ifndef WGKV_K3_WARP_ISSUE
+#define WGKV_K3_WARP_ISSUE 1
+#endif
+
 namespace wgkv {
 
 namespace {
@@ -235,7 +239,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == WARP_MMA) {
         // ================================ MMA issuer =============================
+#if WGKV_K3_WARP_ISSUE
+        // the whole warp runs the loop (warp-uniform operands stay in uniform
+        // registers); elect.sync issues each tcgen05 op from one lane
+#define K3_MMA_SS tc::mma_ss_w
+#define K3_MMA_TS tc::mma_ts_w
+#define K3_COMMIT tc::mma_commit_w
+        {
+#else
+#define K3_MMA_SS tc::mma_ss
+#define K3_MMA_TS tc::mma_ts
+#define K3_COMMIT tc::mma_commit
         if (lane == 0) {
+#endif
             constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
             constexpr uint32_t idPV = tc::idesc_bf16(128, 128, false, true);
             auto issue_S = [&](int t, int st) {
@@ -243,14 +259,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t ka = sbase + OFF_KV + st * STAGE_BYTES;
                 const uint32_t d = tmem + 256 * t + 128;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(d, kmajor_desc(qa, kk), kmajor_desc(ka, kk), idS, kk > 0);
+                for (int kk = 0; kk < 8; ++kk) K3_MMA_SS(d, kmajor_desc(qa, kk), kmajor_desc(ka, kk), idS, kk > 0);
             };
             auto issue_PV = [&](int t, int st, bool acc) {
                 const uint32_t va = sbase + OFF_KV + st * STAGE_BYTES + TILE_BYTES;
                 const uint32_t d = tmem + 256 * t, pa = tmem + 256 * t + 128;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    tc::mma_ts(d, pa + 8 * kk, tc::smem_desc_sw128(va + kk * 2048u, SUB_BYTES, 1024), idPV,
+                    K3_MMA_TS(d, pa + 8 * kk, tc::smem_desc_sw128(va + kk * 2048u, SUB_BYTES, 1024), idPV,
                                (acc || kk > 0) ? 1u : 0u);
             };
             tc::mbar_wait(&bar->q_ready, 0);
@@ -258,9 +274,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::fence_after_sync();
             for (int t = 0; t < NT; ++t) {
                 issue_S(t, 0);
-                tc::mma_commit(&bar->s_full[t]);
+                K3_COMMIT(&bar->s_full[t]);
             }
-            tc::mma_commit(&bar->k_empty[0]);
+            K3_COMMIT(&bar->k_empty[0]);
             for (int j = 0; j < nblk; ++j) {
                 const int st = j & 1;
                 for (int t = 0; t < NT; ++t) {
@@ -270,8 +286,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     K3_TR(2, j, 3 * t + 1);
                     tc::fence_after_sync();
                     issue_PV(t, st, j > 0);
-                    if (j == nblk - 1) tc::mma_commit(&bar->o_final[t]);
-                    if (t == NT - 1) tc::mma_commit(&bar->v_empty[st]);
+                    if (j == nblk - 1) K3_COMMIT(&bar->o_final[t]);
+                    if (t == NT - 1) K3_COMMIT(&bar->v_empty[st]);
                     if (j + 1 < nblk) {
                         const int sn = (j + 1) & 1;
                         if (t == 0) {
@@ -279,14 +295,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             tc::fence_after_sync();
                         }
                         issue_S(t, sn);
-                        tc::mma_commit(&bar->s_full[t]);
+                        K3_COMMIT(&bar->s_full[t]);
                         K3_TR(2, j, 3 * t + 2);
-                        if (t == NT - 1) tc::mma_commit(&bar->k_empty[sn]);
+                        if (t == NT - 1) K3_COMMIT(&bar->k_empty[sn]);
                     }
                 }
             }
         }
         __syncwarp();
+#undef K3_MMA_SS
+#undef K3_MMA_TS
+#undef K3_COMMIT
     } else {
         // ================================ softmax ================================
         // warp = (tile t, column half c, lane quarter wq): rows r of tile t,
