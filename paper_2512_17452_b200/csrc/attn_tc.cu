@@ -37,6 +37,13 @@
 #ifndef WGKV_K3_WARP_ISSUE
 #define WGKV_K3_WARP_ISSUE 1
 #endif
+// waits with a suspend-time hint (spinning warps give their issue slots to the
+// softmax warps of the same SM sub-partition): bit 0 producers, 1 MMA issuer, 2 softmax
+#ifndef WGKV_K3_SLEEP
+#define WGKV_K3_SLEEP 2
+#endif
+#define K3_WAIT(role, bar_, par_) \
+    ((WGKV_K3_SLEEP >> (role)) & 1 ? tc::mbar_wait_sleep((bar_), (par_)) : tc::mbar_wait((bar_), (par_)))
 
 namespace wgkv {
 
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int pg = __shfl_sync(0xffffffffu, cur_ids, lane >> 1);
             {
                 uint64_t* full = kv ? &bar->v_full[st] : &bar->k_full[st];
-                if (j >= NSTAGE) tc::mbar_wait(kv ? &bar->v_empty[st] : &bar->k_empty[st], ((j - NSTAGE) >> 1) & 1);
+                if (j >= NSTAGE) K3_WAIT(0, kv ? &bar->v_empty[st] : &bar->k_empty[st], ((j - NSTAGE) >> 1) & 1);
                 if (lane == 0) K3_TR(3, j, kv);
                 uint8_t* dst = sm + OFF_KV + st * STAGE_BYTES + kv * TILE_BYTES;
                 if (lane == 0) tc::mbar_arrive_expect_tx(full, TILE_BYTES);
@@ -280,9 +287,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < nblk; ++j) {
                 const int st = j & 1;
                 for (int t = 0; t < NT; ++t) {
-                    tc::mbar_wait(&bar->p_full[t], j & 1);
+                    K3_WAIT(1, &bar->p_full[t], j & 1);
                     K3_TR(2, j, 3 * t);
-                    if (t == 0) tc::mbar_wait(&bar->v_full[st], (j >> 1) & 1);
+                    if (t == 0) K3_WAIT(1, &bar->v_full[st], (j >> 1) & 1);
                     K3_TR(2, j, 3 * t + 1);
                     tc::fence_after_sync();
                     issue_PV(t, st, j > 0);
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     if (j + 1 < nblk) {
                         const int sn = (j + 1) & 1;
                         if (t == 0) {
-                            tc::mbar_wait(&bar->k_full[sn], ((j + 1) >> 1) & 1);
+                            K3_WAIT(1, &bar->k_full[sn], ((j + 1) >> 1) & 1);
                             tc::fence_after_sync();
                         }
                         issue_S(t, sn);
@@ -345,7 +352,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nblk; ++j) {
-            tc::mbar_wait(&bar->s_full[t], j & 1);
+            K3_WAIT(2, &bar->s_full[t], j & 1);
             tc::fence_after_sync();
             if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 0);
 #ifdef WGKV_DBG_NO_SOFTMAX  // diagnostic: MMA/TMA pipeline speed with the softmax removed

@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         // S3 = Ahi.Bpost_hi, S4 = Ahi.Bpost_lo, S5 = Alo.Bpost_hi -> commit
         // hl_empty + t_full; the next k_pre tile is loaded as soon as S1-S2
         // completed (and the producers have read the current one).
-        if (lane == 0) {
+        // the whole warp runs the loop (warp-uniform operands stay in uniform
+        // registers); elect.sync / lane 0 issue the tcgen05 and TMA operations
+        {
             int cur_blk = -1, b_loads = 0;
             constexpr uint32_t idG = tc::idesc_bf16(128, 128, false, false);
             const uint32_t Apre = sbase + G_OFF_A, Ahi = Apre + GT_TILE, Alo = Apre + 2 * GT_TILE;
@@ -224,9 +226,12 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 const int pair = (int)(tile / A.tiles_per_pair);
                 const int t0 = (int)((tile % A.tiles_per_pair) * 128);
                 const int s = pair / a.kv_heads, h = pair % a.kv_heads;
-                tc::mbar_arrive_expect_tx(pre_full, GT_TILE);
-                for (int hh = 0; hh < 2; ++hh)
-                    tc::tma_load_3d(sm + G_OFF_A + hh * GT_SUB, &tk, pre_full, hh * 64, h, s * (int)a.T + t0);
+                if (lane == 0) {
+                    tc::mbar_arrive_expect_tx(pre_full, GT_TILE);
+                    for (int hh = 0; hh < 2; ++hh)
+                        tc::tma_load_3d(sm + G_OFF_A + hh * GT_SUB, &tk, pre_full, hh * 64, h, s * (int)a.T + t0);
+                }
+                __syncwarp();
             };
             if (t_begin < t_end) load_pre(t_begin);
             for (long tile = t_begin; tile < t_end; ++tile) {
@@ -235,11 +240,14 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 const int blk = a.layer * a.kv_heads + pair % a.kv_heads;
                 if (blk != cur_blk) {  // (re)load W1's split tiles once the previous MMAs are done with B
                     if (it > 0) tc::mbar_wait(hl_empty, (it - 1) & 1);
-                    tc::mbar_arrive_expect_tx(b_full, 4 * GT_TILE);
-                    for (int q = 0; q < 4; ++q)
-                        for (int hh = 0; hh < 2; ++hh)
-                            tc::tma_load_3d(sm + G_OFF_B + q * GT_TILE + hh * GT_SUB, &tw, b_full, hh * 64, 0,
-                                            blk * 4 + q);
+                    if (lane == 0) {
+                        tc::mbar_arrive_expect_tx(b_full, 4 * GT_TILE);
+                        for (int q = 0; q < 4; ++q)
+                            for (int hh = 0; hh < 2; ++hh)
+                                tc::tma_load_3d(sm + G_OFF_B + q * GT_TILE + hh * GT_SUB, &tw, b_full, hh * 64, 0,
+                                                blk * 4 + q);
+                    }
+                    __syncwarp();
                     tc::mbar_wait(b_full, b_loads & 1);
                     ++b_loads;
                     cur_blk = blk;
@@ -250,10 +258,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 if (it >= 2) tc::mbar_wait(&t_empty[buf], ((it - 2) >> 1) & 1);
                 tc::fence_after_sync();
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(dt, kdesc(Apre, kk), kdesc(Bph, kk), idG, kk ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Apre, kk), kdesc(Bph, kk), idG, kk ? 1u : 0u);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(dt, kdesc(Apre, kk), kdesc(Bpl, kk), idG, 1u);
-                tc::mma_commit(pre_empty);
+                for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Apre, kk), kdesc(Bpl, kk), idG, 1u);
+                tc::mma_commit_w(pre_empty);
                 if (tile + 1 < t_end) {  // next k_pre tile once S1-S2 and the producers are done with this one
                     tc::mbar_wait(pre_read, it & 1);
                     tc::mbar_wait(pre_empty, it & 1);
@@ -262,13 +270,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 tc::mbar_wait(hl_full, it & 1);
                 tc::fence_after_sync();
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(dt, kdesc(Ahi, kk), kdesc(Bqh, kk), idG, 1u);
+                for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Ahi, kk), kdesc(Bqh, kk), idG, 1u);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(dt, kdesc(Ahi, kk), kdesc(Bql, kk), idG, 1u);
+                for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Ahi, kk), kdesc(Bql, kk), idG, 1u);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) tc::mma_ss(dt, kdesc(Alo, kk), kdesc(Bqh, kk), idG, 1u);
-                tc::mma_commit(hl_empty);
-                tc::mma_commit(&t_full[buf]);
+                for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Alo, kk), kdesc(Bqh, kk), idG, 1u);
+                tc::mma_commit_w(hl_empty);
+                tc::mma_commit_w(&t_full[buf]);
             }
         }
         __syncwarp();
