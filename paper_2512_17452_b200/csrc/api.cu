@@ -53,8 +53,14 @@ __global__ void release_kernel(PoolView pv, int layers, int seq0, int nseq) {
     __shared__ int base;
     if (threadIdx.x == 0) base = atomicAdd(pv.free_top, nl + ng);
     __syncthreads();
-    for (int i = threadIdx.x; i < nl + ng; i += blockDim.x)
-        pv.free_stack[base + i] = i < nl ? pv.lpt[hidx * pv.n_lp + i] : pv.gpt[hidx * pv.n_gp + (i - nl)];
+    // pushed in reverse allocation order (Global pages then Local, admit_plan's
+    // pop order), so re-allocating pops the same ascending physical runs: a
+    // head's Global pages stay physically contiguous, which lets K3 load a
+    // 128-key vertical block with one TMA box per dim half
+    for (int i = threadIdx.x; i < nl + ng; i += blockDim.x) {
+        const int k = nl + ng - 1 - i;  // allocation index
+        pv.free_stack[base + i] = k < ng ? pv.gpt[hidx * pv.n_gp + k] : pv.lpt[hidx * pv.n_lp + (k - ng)];
+    }
     __syncthreads();
     if (threadIdx.x == 0) pv.state[hidx] = HeadState{0, 0, 0, 0};
 }

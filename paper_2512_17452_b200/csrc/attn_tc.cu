@@ -133,8 +133,9 @@ __device__ unsigned long long g_k3_trace[4][4096][8];
 #endif
 __global__ void __launch_bounds__(NTHREADS, 1)
     vs_prefill_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                         const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tpool, VsArgs a,
-                         __nv_bfloat16* __restrict__ out) {
+                         const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tpool,
+                         const __grid_constant__ CUtensorMap tkrun, const __grid_constant__ CUtensorMap tvrun,
+                         VsArgs a, __nv_bfloat16* __restrict__ out) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bar = reinterpret_cast<Bars*>(sm + OFF_BAR);
@@ -201,6 +202,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::tma_prefetch(&tk);
             tc::tma_prefetch(&tv);
             tc::tma_prefetch(&tpool);
+            tc::tma_prefetch(&tkrun);
+            tc::tma_prefetch(&tvrun);
             tc::mbar_arrive_expect_tx(&bar->q_full, NT * TILE_BYTES);
             for (int t = 0; t < NT; ++t)
                 for (int hh = 0; hh < 2; ++hh)
@@ -236,9 +239,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (lane == 0) tc::mbar_arrive_expect_tx(full, TILE_BYTES);
                 __syncwarp();
                 if (!band) {
-                    if (lane < 2 * ppb)
+                    // physically consecutive pages (the usual case after a prefill's
+                    // single claim): one box of ppb pages per dim half
+                    const int pg0 = __shfl_sync(0xffffffffu, cur_ids, 0);
+                    if (__all_sync(0xffffffffu, lane >= ppb || cur_ids == pg0 + lane)) {
+                        if (lane < 2)
+                            tc::tma_load_3d(dst + lane * SUB_BYTES, kv ? &tvrun : &tkrun, full, lane * 64, 0, pg0);
+                    } else if (lane < 2 * ppb) {
                         tc::tma_load_3d(dst + (lane & 1) * SUB_BYTES + (lane >> 1) * ps * 128, &tpool, full,
                                         (lane & 1) * 64, 0, 2 * pg + kv);
+                    }
                 } else if (lane < 2) {
                     tc::tma_load_3d(dst + lane * SUB_BYTES, kv ? &tv : &tk, full, lane * 64, h, (int)(s * T + kb0));
                 }
@@ -577,6 +587,12 @@ int launch_vs_prefill_tc(const VsArgs& a, int nseq, const __nv_bfloat16* q, cons
     r |= make_tmap_3d_bf16(&tk, k_post, 128, Hkv, rows, 256, (uint64_t)Hkv * 256, 64, 1, 128);
     r |= make_tmap_3d_bf16(&tv, v, 128, Hkv, rows, 256, (uint64_t)Hkv * 256, 64, 1, 128);
     r |= make_tmap_3d_bf16(&tp, a.pv.data, 128, ps, 2 * (uint64_t)a.pv.capacity, 256, (uint64_t)ps * 256, 64, ps, 1);
+    // K (V) planes of consecutive pages: [page][ps slots][128 dims], page stride = 2 planes
+    CUtensorMap tkr, tvr;
+    const uint64_t plane = (uint64_t)ps * 256;
+    r |= make_tmap_3d_bf16(&tkr, a.pv.data, 128, ps, (uint64_t)a.pv.capacity, 256, 2 * plane, 64, ps, 128 / ps);
+    r |= make_tmap_3d_bf16(&tvr, static_cast<const uint8_t*>(a.pv.data) + plane, 128, ps, (uint64_t)a.pv.capacity,
+                           256, 2 * plane, 64, ps, 128 / ps);
     if (r) return WGKV_ECUDA;
     static bool attr = false;
     if (!attr) {
@@ -584,7 +600,7 @@ int launch_vs_prefill_tc(const VsArgs& a, int nseq, const __nv_bfloat16* q, cons
         attr = true;
     }
     dim3 grid((unsigned)((a.T + 127) / 128), Hq / NT, nseq);
-    vs_prefill_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tq, tk, tv, tp, a, out);
+    vs_prefill_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tq, tk, tv, tp, tkr, tvr, a, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
