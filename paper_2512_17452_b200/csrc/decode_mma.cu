@@ -35,6 +35,9 @@ constexpr int CPS = WGKV_K5_CPS;  // CTAs per SM
 constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
 constexpr int QROW = 136;    // padded Q row (bf16 elements)
 constexpr int PID_CAP = 2048;  // pages per work item (staged page ids)
+#ifndef WGKV_K5_IPC
+#define WGKV_K5_IPC 2  // work items per CTA (work stealing balance vs per-item fixed costs)
+#endif
 #ifndef WGKV_K5_MIN_PAGES
 #define WGKV_K5_MIN_PAGES 8
 #endif
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             npmax = max(npmax, np);
         }
         // ~2 items per CTA, taken dynamically (work stealing) for balance
-        int cp = (int)((total + 2 * gridDim.x - 1) / (2 * gridDim.x));
+        int cp = (int)((total + WGKV_K5_IPC * gridDim.x - 1) / (WGKV_K5_IPC * gridDim.x));
         cp = max(cp, WGKV_K5_MIN_PAGES);  // per-item fixed costs (page ids, ring fill, merge) amortised
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
