@@ -39,7 +39,7 @@ constexpr int PID_CAP = 2048;  // pages per work item (staged page ids)
 #define WGKV_K5_IPC 2  // work items per CTA (work stealing balance vs per-item fixed costs)
 #endif
 #ifndef WGKV_K5_MIN_PAGES
-#define WGKV_K5_MIN_PAGES 8
+#define WGKV_K5_MIN_PAGES 32
 #endif
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
