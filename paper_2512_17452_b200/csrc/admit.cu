@@ -278,6 +278,10 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
         gpage = -1;
         const int slot = st.local_ptr;
         int lp = pv.lpt[hidx * pv.n_lp + slot / ps];
+        // the Global tail page, loaded alongside (needed if the victim is promoted
+        // into a partly filled page): one dependent global round trip less
+        const int gi0 = st.global_len;
+        const int gp_tail = (gi0 % ps != 0) ? pv.gpt[hidx * pv.n_gp + gi0 / ps] : -1;
         if (st.local_len < W) {
             // not full: slot == local_len; a slot at a page boundary is the
             // first touch of that ring page (kvstore.cpp:102-107)
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
                     gp = pool_pop(pv);
                     pv.gpt[hidx * pv.n_gp + gi / ps] = gp;
                 } else {
-                    gp = pv.gpt[hidx * pv.n_gp + gi / ps];
+                    gp = gp_tail;
                 }
                 vpage = lp;
                 vslot = slot % ps;
