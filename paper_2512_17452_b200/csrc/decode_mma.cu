@@ -38,8 +38,11 @@ constexpr int PID_CAP = 2048;  // pages per work item (staged page ids)
 #ifndef WGKV_K5_IPC
 #define WGKV_K5_IPC 2  // work items per CTA (work stealing balance vs per-item fixed costs)
 #endif
+#ifndef WGKV_K5_RULE
+#define WGKV_K5_RULE 1
+#endif
 #ifndef WGKV_K5_MIN_PAGES
-#define WGKV_K5_MIN_PAGES 32
+#define WGKV_K5_MIN_PAGES 8
 #endif
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -113,6 +116,11 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         // ~2 items per CTA, taken dynamically (work stealing) for balance
         int cp = (int)((total + WGKV_K5_IPC * gridDim.x - 1) / (WGKV_K5_IPC * gridDim.x));
         cp = max(cp, WGKV_K5_MIN_PAGES);  // per-item fixed costs (page ids, ring fill, merge) amortised
+#if WGKV_K5_RULE == 1
+        // few, long pairs (small batches): cap the chunks per pair near 24 (the
+        // combine merges every chunk) while keeping >= grid/2 items in flight
+        cp = max(cp, (int)min((long)(npmax + 23) / 24, (2 * total + gridDim.x - 1) / gridDim.x));
+#endif
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
         s_cp = cp;
