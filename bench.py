@@ -218,9 +218,11 @@ def run_gpu(args, cfg):
     Q = [randn(B, T, hq, d) for _ in range(slots)]
     K = [randn(B, T, hkv, d) for _ in range(slots)]
     V = [randn(B, T, hkv, d) for _ in range(slots)]
-    qd = [randn(D, B, hq, d) for _ in range(slots)]
-    kd = [randn(D, B, hkv, d) for _ in range(slots)]
-    vd = [randn(D, B, hkv, d) for _ in range(slots)]
+    # decode inputs step-major, [D][slots][B][heads][d]: one copy per tensor and step
+    qd_all, kd_all, vd_all = randn(D, slots, B, hq, d), randn(D, slots, B, hkv, d), randn(D, slots, B, hkv, d)
+    qd = [qd_all[:, i] for i in range(slots)]
+    kd = [kd_all[:, i] for i in range(slots)]
+    vd = [vd_all[:, i] for i in range(slots)]
     out = torch.empty(B, T, hq, d, dtype=torch.bfloat16, device=dev)
     dout = torch.empty(B, hq, d, dtype=torch.bfloat16, device=dev)
     # rank-major head-shard blocks (concatenated along dim 0; see sharding.gather_heads)
@@ -264,9 +266,10 @@ def run_gpu(args, cfg):
     # One decode token-step over all layers, issued eagerly or replayed from a
     # CUDA graph captured once (kills per-kernel launch gaps); the step's new
     # q/k/v are copied into static buffers first, so every replay is a real step.
-    sq = [torch.empty_like(qd[i][0]) for i in range(slots)]
-    sk = [torch.empty_like(kd[i][0]) for i in range(slots)]
-    sv = [torch.empty_like(vd[i][0]) for i in range(slots)]
+    sq_all, sk_all, sv_all = (torch.empty_like(x[0]) for x in (qd_all, kd_all, vd_all))
+    sq = [sq_all[i] for i in range(slots)]
+    sk = [sk_all[i] for i in range(slots)]
+    sv = [sv_all[i] for i in range(slots)]
 
     def decode_token_step():
         for l in range(L):
@@ -292,10 +295,9 @@ def run_gpu(args, cfg):
 
     def decode_all(step0=0):
         for s_ in range(D):
-            for i in range(slots):
-                sq[i].copy_(qd[i][s_], non_blocking=True)
-                sk[i].copy_(kd[i][s_], non_blocking=True)
-                sv[i].copy_(vd[i][s_], non_blocking=True)
+            sq_all.copy_(qd_all[s_], non_blocking=True)
+            sk_all.copy_(kd_all[s_], non_blocking=True)
+            sv_all.copy_(vd_all[s_], non_blocking=True)
             if graph["g"] is not None:
                 graph["g"].replay()
             else:
