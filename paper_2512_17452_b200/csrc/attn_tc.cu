@@ -15,8 +15,8 @@
 //                columns [64c, 64c+64) of tile t: RoPE(q) in smem, then per key
 //                block tcgen05.ld S, mask, row max exchanged with the other
 //                half through smem (named barrier), online softmax (lazy
-//                rescale, threshold 2^8; 1/4 of the exp2 on the FMA pipe, bf16
-//                packing on the ALU so the MUFU only does exp2), P as bf16x2
+//                rescale, threshold 2^8; 1/4 of the exp2 on the FMA pipe,
+//                F2FP bf16 packing), P as bf16x2
 //                written back into TMEM over S, O rescale in TMEM
 //   warp 16/17 : TMA producers for K / V (Q once), 2-stage ring each with its
 //                own full/empty barriers
@@ -81,7 +81,10 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 #ifndef WGKV_PACK_ALU
-#define WGKV_PACK_ALU 1  // F2FP shares the MUFU pipe on B200 (tools/ubench_mufu.cu); PRMT packing: -3.5 % K3 time
+#define WGKV_PACK_ALU 0  // bit e: pair e packed on the ALU (2 IADD + PRMT) instead of F2FP.  F2FP shares the MUFU
+                         // pipe on B200 (tools/ubench_mufu.cu): ALU packing won 3.5 % with a lane-0 MMA issuer;
+                         // with the warp-uniform issuer all-F2FP is 0.6-1 % faster and mixed masks are slower
+                         // (profiles/r1_k3_notes.md)
 #endif
 // fp32 pair -> bf16x2 on the ALU pipe (two IADD + one PRMT) instead of F2FP,
 // which competes with MUFU.EX2 for the same pipe on B200.
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         e1 = ex2(xd.y);
                     }
                     lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(e0, e1));
-                    pa[off + e] = WGKV_PACK_ALU ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
+                    pa[off + e] = ((WGKV_PACK_ALU >> e) & 1) ? pack_bf16x2_alu(e0, e1) : tc::pack_bf16x2(e0, e1);
                 }
             };
             expo(s0, 0);
