@@ -20,6 +20,7 @@
 //   topk_emit_kernel +     fp32 parity mode: per-q-head ascending selection
 //   topk_attn_kernel       and SIMT split-KV attention over it.
 #include <algorithm>
+#include <cstdlib>
 
 #include "attn.cuh"
 
@@ -108,6 +109,7 @@ constexpr int SC_PAGES = 64;  // pages per CTA (8 per warp)
 
 __global__ void __launch_bounds__(SC_WARPS * 32) topk_score_mma_kernel(DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                         float* __restrict__ scores) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the previous kernel
     constexpr int d = 128, ps = 16;
     const int gs = a.q_heads / a.pv.kv_heads;
     const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32) topk_score_mma_kernel(DecArgs a
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) quest_meta_kernel(DecArgs a, const int* __restrict__ meta_full,
                                                          __nv_bfloat16* __restrict__ meta) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the previous kernel
     constexpr int d = 128;
     const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
     const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
@@ -258,6 +261,7 @@ template <int QG>  // GQA group size
 __global__ void __launch_bounds__(256) quest_score_kernel(DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                           const __nv_bfloat16* __restrict__ meta,
                                                           int* __restrict__ meta_full, float* __restrict__ scores) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the previous kernel
     constexpr int d = 128, PPW = 2;  // pages per warp (all loads issued up front)
     const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -349,6 +353,7 @@ constexpr int TH_STAGE_CAP = 44 * 1024;  // staged scores (dynamic smem floats)
 __global__ void __launch_bounds__(1024) topk_thresh_kernel(DecArgs a, long budget, int smem_cap,
                                                            const float* __restrict__ scores,
                                                            unsigned long long* __restrict__ thr) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the previous kernel
     extern __shared__ unsigned long long cand[];   // [TH_CAND] candidate keys, then the staged scores
     float* ssc = reinterpret_cast<float*>(cand + TH_CAND);
     __shared__ unsigned hist[TH_BINS];
@@ -564,6 +569,7 @@ __global__ void __launch_bounds__(256) topk_mask_kernel(DecArgs a, const float* 
                                                         const unsigned long long* __restrict__ thr,
                                                         uint8_t* __restrict__ umask, int* __restrict__ ucnt,
                                                         int nblk) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the previous kernel
     const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads, blk = blockIdx.x;
     const int gs = a.q_heads / a.pv.kv_heads, ps = a.pv.page_size;
     const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + s, h)];
@@ -604,7 +610,11 @@ __global__ void __launch_bounds__(256) topk_mask_kernel(DecArgs a, const float* 
 
 __global__ void __launch_bounds__(256) topk_compact_kernel(DecArgs a, const uint8_t* __restrict__ umask,
                                                            const int* __restrict__ ucnt, int nblk,
-                                                           int32_t* __restrict__ uni, int32_t* __restrict__ nuni) {
+                                                           int32_t* __restrict__ uni, int32_t* __restrict__ nuni,
+                                                           int* __restrict__ k5_counter) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the previous kernel
+    // K5 (next, a programmatic dependent) steals work from this counter
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && k5_counter) *k5_counter = 0;
     const int bh = blockIdx.y, s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads, blk = blockIdx.x;
     const int ps = a.pv.page_size;
     const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + s, h)];
@@ -796,6 +806,25 @@ __global__ void topk_combine_kernel(DecArgs a, const float* __restrict__ part, E
     }
 }
 
+// launch as a programmatic dependent of the previous kernel in the stream (its
+// launch overlaps the predecessor's tail; the kernel's griddepcontrol.wait
+// orders every read after the predecessor completes)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    static const bool off = getenv("WGKV_TOPK_NOPDL") != nullptr;  // A/B switch
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
 template <typename E>
 int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, float* scores, int32_t* sel,
                        int32_t* nsel, unsigned long long* thr, uint8_t* umask, int* ucnt, float* part, int* nchunks,
@@ -809,19 +838,19 @@ int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, flo
     const bool fast = kBf16 && d == 128 && a.pv.page_size == 16 && gs <= 8 && a.pv.capacity < (1L << 24);
     if (mode == WGKV_TOPK_QUEST) {
         if (!fast || !meta || !meta_full) return WGKV_ENOTSUP;
-        quest_meta_kernel<<<dim3(16, nseq * a.pv.kv_heads), 256, 0, st>>>(a, meta_full, meta);
+        launch_pdl(quest_meta_kernel, dim3(16, nseq * a.pv.kv_heads), 256, 0, st, a, meta_full, meta);
         const dim3 qgrid((max_pages + 15) / 16, nseq * a.pv.kv_heads);
         const __nv_bfloat16* qb = reinterpret_cast<const __nv_bfloat16*>(q);
         switch (gs) {
-            case 1: quest_score_kernel<1><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
-            case 2: quest_score_kernel<2><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
-            case 4: quest_score_kernel<4><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
-            case 8: quest_score_kernel<8><<<qgrid, 256, 0, st>>>(a, qb, meta, meta_full, scores); break;
+            case 1: launch_pdl(quest_score_kernel<1>, qgrid, 256, 0, st, a, qb, meta, meta_full, scores); break;
+            case 2: launch_pdl(quest_score_kernel<2>, qgrid, 256, 0, st, a, qb, meta, meta_full, scores); break;
+            case 4: launch_pdl(quest_score_kernel<4>, qgrid, 256, 0, st, a, qb, meta, meta_full, scores); break;
+            case 8: launch_pdl(quest_score_kernel<8>, qgrid, 256, 0, st, a, qb, meta, meta_full, scores); break;
             default: return WGKV_ENOTSUP;
         }
     } else if (fast && gs <= 4)
-        topk_score_mma_kernel<<<dim3((max_pages + SC_PAGES - 1) / SC_PAGES, nseq * a.pv.kv_heads), SC_WARPS * 32, 0,
-                                st>>>(a, reinterpret_cast<const __nv_bfloat16*>(q), scores);
+        launch_pdl(topk_score_mma_kernel, dim3((max_pages + SC_PAGES - 1) / SC_PAGES, nseq * a.pv.kv_heads),
+                   SC_WARPS * 32, 0, st, a, reinterpret_cast<const __nv_bfloat16*>(q), scores);
     else
         topk_score_kernel<E><<<dim3((max_pages + TK_PPB - 1) / TK_PPB, nseq * a.pv.kv_heads), 128,
                               sizeof(float) * gs * d, st>>>(a, q, scores);
@@ -832,15 +861,19 @@ int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, flo
         cudaFuncSetAttribute(topk_thresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)th_smem);
         cap_set = cap;
     }
-    topk_thresh_kernel<<<nseq * a.q_heads, 1024, th_smem, st>>>(a, budget, cap, scores, thr);
+    launch_pdl(topk_thresh_kernel, nseq * a.q_heads, 1024, th_smem, st, a, budget, cap, (const float*)scores, thr);
     if (fast) {
         const int nblk = (max_pages + UB - 1) / UB;
-        topk_mask_kernel<<<dim3(nblk, nseq * a.pv.kv_heads), 256, 0, st>>>(a, scores, thr, umask, ucnt, nblk);
-        topk_compact_kernel<<<dim3(nblk, nseq * a.pv.kv_heads), 256, 0, st>>>(a, umask, ucnt, nblk, sel, nsel);
+        static const bool nopdl = getenv("WGKV_TOPK_NOPDL") != nullptr;  // A/B switch
+        int* k5_counter = nchunks + (size_t)a.pv.max_seqs * a.pv.kv_heads;  // K5's work-stealing counter
+        launch_pdl(topk_mask_kernel, dim3(nblk, nseq * a.pv.kv_heads), 256, 0, st, a, (const float*)scores,
+                   (const unsigned long long*)thr, umask, ucnt, nblk);
+        launch_pdl(topk_compact_kernel, dim3(nblk, nseq * a.pv.kv_heads), 256, 0, st, a, (const uint8_t*)umask,
+                   (const int*)ucnt, nblk, sel, nsel, nopdl ? nullptr : k5_counter);
         a.sel = sel;
         a.nsel = nsel;
         if constexpr (kBf16)
-            return launch_decode_attn_mma(a, nseq, q, part, nchunks, out, st, false);
+            return launch_decode_attn_mma(a, nseq, q, part, nchunks, out, st, !nopdl);
         return WGKV_ENOTSUP;
     }
     topk_emit_kernel<<<nseq * a.q_heads, 1024, 0, st>>>(a, scores, thr, sel, nsel);
