@@ -103,16 +103,42 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     __shared__ int s_cp, s_items;
 
     // ---- device-side split: uniform chunk size from the actual page counts --
-    if (tid == 0) {
-        long total = 0;
+    // (all threads: the per-pair state loads are independent, so they are
+    // spread over the block instead of a serial loop of dependent round trips)
+    __shared__ long s_wtot[DW];
+    __shared__ int s_wmax[DW], s_wscan[DW];
+    {
+        // pass 1: each thread owns a contiguous run of pairs; page counts staged in item_base
+        const int run = (npairs + blockDim.x - 1) / blockDim.x;
+        const int p0 = tid * run, p1 = min(npairs, p0 + run);
+        long tot = 0;
         int npmax = 0;
-        for (int p = 0; p < npairs; ++p) {
+        for (int p = p0; p < p1; ++p) {
             const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
             const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
             const int np = ngv + (st.local_len + ps - 1) / ps;
-            total += np;
+            item_base[p] = np;
+            tot += np;
             npmax = max(npmax, np);
         }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, o));
+        }
+        if (lane == 0) {
+            s_wtot[warp] = tot;
+            s_wmax[warp] = npmax;
+        }
+        __syncthreads();
+        tot = 0;
+        npmax = 0;
+#pragma unroll
+        for (int w = 0; w < DW; ++w) {
+            tot += s_wtot[w];
+            npmax = max(npmax, s_wmax[w]);
+        }
+        const long total = tot;
         // ~2 items per CTA, taken dynamically (work stealing) for balance
         int cp = (int)((total + WGKV_K5_IPC * gridDim.x - 1) / (WGKV_K5_IPC * gridDim.x));
         cp = max(cp, WGKV_K5_MIN_PAGES);  // per-item fixed costs (page ids, ring fill, merge) amortised
@@ -123,19 +149,30 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
 #endif
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
-        s_cp = cp;
-        int acc = 0;
-        for (int p = 0; p < npairs; ++p) {
-            const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
-            const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
-            const int np = ngv + (st.local_len + ps - 1) / ps;
-            item_base[p] = acc;
-            const int nc = max(1, (np + cp - 1) / cp);
-            acc += nc;
-            if (blockIdx.x == 0) nchunks[p] = nc;
+        // pass 2: chunks per pair, exclusive scan into item_base
+        int nc_run = 0;
+        for (int p = p0; p < p1; ++p) nc_run += max(1, (item_base[p] + cp - 1) / cp);
+        int incl = nc_run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        item_base[npairs] = acc;
-        s_items = acc;
+        if (lane == 31) s_wscan[warp] = incl;
+        __syncthreads();  // also: every pass-1 read of s_wtot / s_wmax is done
+        int acc = incl - nc_run;
+        for (int w = 0; w < warp; ++w) acc += s_wscan[w];
+        for (int p = p0; p < p1; ++p) {
+            const int nc = max(1, (item_base[p] + cp - 1) / cp);
+            item_base[p] = acc;
+            if (blockIdx.x == 0) nchunks[p] = nc;
+            acc += nc;
+        }
+        if (p1 == npairs && p0 < p1) {
+            item_base[npairs] = acc;
+            s_items = acc;
+        }
+        if (tid == 0) s_cp = cp;
     }
     if (tid < DW * DNS) tc::mbar_init(&full[tid], 1);
     tc::fence_barrier_init();
