@@ -189,8 +189,17 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) break;
+        // pair of this item: the last bh with item_base[bh] <= item (binary search)
         int bh = 0;
-        while (item_base[bh + 1] <= item) ++bh;
+        for (int lo = 0, hi = npairs - 1; lo <= hi;) {
+            const int mid = (lo + hi) >> 1;
+            if (item_base[mid] <= item) {
+                bh = mid;
+                lo = mid + 1;
+            } else {
+                hi = mid - 1;
+            }
+        }
         const int chunk = item - item_base[bh];
         const int s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
         const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
