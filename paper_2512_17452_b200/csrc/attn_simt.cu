@@ -314,82 +314,70 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
 }
 
 // merge chunk partials of one (seq, q head): out = sum e^(m_c-M) o_c / sum e^(m_c-M) l_c.
-// The block reduces every chunk's (m, l) and publishes the weights through
-// smem; then the 8 warps each sum every 8th chunk row with coalesced
-// float2 loads (independent across chunks: this kernel is latency-bound) and
-// the warp sums are reduced in smem.
+// Latency-bound: each of the 8 warps merges every 8th chunk online (m, l and
+// the row of a chunk are loaded together, the loads of successive chunks are
+// independent), so the partials are read in one round of L2 accesses; the
+// 8 warp results are merged through smem.
 template <typename E>
 __global__ void __launch_bounds__(256) decode_combine_kernel(DecArgs a, const float* __restrict__ part,
                                                              E* __restrict__ out) {
-    constexpr int MAXC = kMaxChunks;
+    constexpr int NW = 8;
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
     const int sp = blockIdx.x, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
     const int bh = s * a.pv.kv_heads + h;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t pstride = (size_t)gs * (d + 2);
     const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
-    __shared__ float w[MAXC];
-    __shared__ float red[8][256];
-    __shared__ float invL;
+    __shared__ float wm[NW], wl[NW];
+    __shared__ float wacc[NW][256];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // partials of the attention kernel (PDL)
-    const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, MAXC);
-    __shared__ float wred[8];
-    // (m, l) of every chunk: block max, then weights and block sum of l
-    float M = -INFINITY;
-    for (int c = tid; c < nch; c += blockDim.x) M = fmaxf(M, base[(size_t)c * pstride + d]);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    if (lane == 0) wred[warp] = M;
-    __syncthreads();
-    M = wred[0];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) M = fmaxf(M, wred[k]);
-    float L = 0.f;
-    for (int c = tid; c < nch; c += blockDim.x) {
-        const float mc = base[(size_t)c * pstride + d];
-        const float wc = mc == -INFINITY ? 0.f : __expf(mc - M);
-        w[c] = wc;
-        L += wc * base[(size_t)c * pstride + d + 1];
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    __syncthreads();  // every wred[] read of M is done
-    if (lane == 0) wred[warp] = L;
-    __syncthreads();
-    if (tid == 0) {
-        float t = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) t += wred[k];
-        invL = 1.f / t;
-    }
-    __syncthreads();
+    const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, kMaxChunks);
+    float m = -INFINITY, l = 0.f;
     float2 acc[4];  // columns 2*lane + 64*j (d <= 256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = make_float2(0.f, 0.f);
 #pragma unroll 4
-    for (int c = warp; c < nch; c += 8) {
-        const float wc = w[c];
+    for (int c = warp; c < nch; c += NW) {
         const float* r = base + (size_t)c * pstride;
+        const float mc = r[d], lc = r[d + 1];
+        float2 x[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (2 * lane + 64 * j < d) {
-                const float2 x = *reinterpret_cast<const float2*>(r + 2 * lane + 64 * j);
-                acc[j].x = fmaf(wc, x.x, acc[j].x);
-                acc[j].y = fmaf(wc, x.y, acc[j].y);
-            }
+            x[j] = 2 * lane + 64 * j < d ? *reinterpret_cast<const float2*>(r + 2 * lane + 64 * j) : make_float2(0.f, 0.f);
+        if (mc == -INFINITY) continue;  // empty chunk (uniform across the warp)
+        const float mn = fmaxf(m, mc);
+        const float sa = m == -INFINITY ? 0.f : __expf(m - mn), sb = __expf(mc - mn);
+        l = l * sa + lc * sb;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc[j].x = acc[j].x * sa + x[j].x * sb;
+            acc[j].y = acc[j].y * sa + x[j].y * sb;
+        }
+        m = mn;
+    }
+    if (lane == 0) {
+        wm[warp] = m;
+        wl[warp] = l;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         if (2 * lane + 64 * j < d) {
-            red[warp][2 * lane + 64 * j] = acc[j].x;
-            red[warp][2 * lane + 64 * j + 1] = acc[j].y;
+            wacc[warp][2 * lane + 64 * j] = acc[j].x;
+            wacc[warp][2 * lane + 64 * j + 1] = acc[j].y;
         }
     __syncthreads();
-    for (int e = tid; e < d; e += blockDim.x) {
-        float t = 0.f;
+    float M = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t += red[k][e];
-        out[((size_t)s * a.q_heads + p) * d + e] = from_f<E>(t * invL);
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w]);
+    for (int e = tid; e < d; e += blockDim.x) {
+        float t = 0.f, L = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float f = wm[w] == -INFINITY ? 0.f : __expf(wm[w] - M);
+            t += f * wacc[w][e];
+            L += f * wl[w];
+        }
+        out[((size_t)s * a.q_heads + p) * d + e] = from_f<E>(t / L);
     }
 }
 
