@@ -164,6 +164,9 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     if (c.topk_mode == WGKV_TOPK_QUEST &&
         (c.dtype != WGKV_BF16 || c.head_dim != 128 || c.page_size != 16 || c.q_heads / c.kv_heads > 8))
         return fail(WGKV_ENOTSUP, "Quest page selection needs bf16, head_dim 128, page 16, GQA group <= 8");
+    if ((c.max_tokens + c.page_size - 1) / c.page_size + 1 + (c.window + c.page_size - 1) / c.page_size >
+        (long)kMaxChunks * kDecPidCap)
+        return fail(WGKV_ENOTSUP, "max_tokens exceeds the decode work split (kMaxChunks * kDecPidCap pages per head)");
     if (cudaSetDevice(c.device) != cudaSuccess) return fail(WGKV_ECUDA, "cudaSetDevice failed");
 
     auto* ctx = new wgkv_ctx();

@@ -16,6 +16,9 @@ struct VsArgs {
 // partial-buffer chunks per (seq, kv head): enough for a single kv head to
 // spread over every SM (1M-token contexts with 8-way head sharding)
 constexpr int kMaxChunks = 512;
+// K5 pages per work item (staged page ids); max_tokens per head is bounded by
+// kMaxChunks * kDecPidCap pages (checked at context creation)
+constexpr int kDecPidCap = 1024;
 
 struct DecArgs {
     PoolView pv;
