@@ -18,7 +18,7 @@ struct VsArgs {
 constexpr int kMaxChunks = 512;
 // K5 pages per work item (staged page ids); max_tokens per head is bounded by
 // kMaxChunks * kDecPidCap pages (checked at context creation)
-constexpr int kDecPidCap = 1024;
+constexpr int kDecPidCap = 2048;
 
 struct DecArgs {
     PoolView pv;

@@ -34,8 +34,7 @@ constexpr int DNS = WGKV_K5_DNS;  // ring stages per warp
 constexpr int CPS = WGKV_K5_CPS;  // CTAs per SM
 constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
 constexpr int QROW = 136;    // padded Q row (bf16 elements)
-constexpr int PID_CAP = kDecPidCap;  // pages per work item (staged page ids; 4 KB of smem leaves room for
-                                    // the side-stream gate CTA next to the 2 K5 CTAs of an SM)
+constexpr int PID_CAP = kDecPidCap;  // pages per work item (staged page ids)
 #ifndef WGKV_K5_IPC
 #define WGKV_K5_IPC 2  // work items per CTA (work stealing balance vs per-item fixed costs)
 #endif
