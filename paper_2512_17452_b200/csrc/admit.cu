@@ -254,20 +254,34 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
     double* xs = dsh;                       // [2d]
     double* scratch = xs + 2 * d;           // [2*hidden + 32]
     float* kpost = reinterpret_cast<float*>(scratch + 2 * ga.hidden + 32);  // [d]
-    __shared__ HeadState st;
     __shared__ int vpage, vslot, gpage, gslot, npage, nslot, event;
-    if (tid == 0) st = pv.state[hidx];
-    __syncthreads();
-    const long pos = st.tokens_seen;
     const size_t in = ((size_t)s * pv.kv_heads + h) * d;
+    E* pool = reinterpret_cast<E*>(pv.data);
+    // the new token's inputs do not depend on the cache state: loads first
+    const bool kt = tid < d / 2, et = tid < d;
+    const float x0 = kt ? to_f(k_pre[in + 2 * tid]) : 0.f, x1 = kt ? to_f(k_pre[in + 2 * tid + 1]) : 0.f;
+    const E vnew = et ? v[in + tid] : E();
+    // every thread reads the state and the ring page under local_ptr itself
+    // (broadcast loads), so the victim's K/V is fetched speculatively in the
+    // same round as its admission bit instead of after thread 0's decision
+    HeadState st = pv.state[hidx];
+    const long pos = st.tokens_seen;
+    const int slot = st.local_ptr;
+    int lp = pv.lpt[hidx * pv.n_lp + slot / ps];
+    const bool ring_full = st.local_len >= W;
+    E vk = E(), vv = E();
+    if (ring_full && lp >= 0 && et) {
+        const E* ks = pool + (size_t)lp * pv.page_elems() + (size_t)(slot % ps) * d;
+        vk = ks[tid];
+        vv = ks[tid + (size_t)ps * d];
+    }
     // RoPE of the stored key (fp32); the fp64 gate feature is built after the
     // dependent-launch trigger below
-    for (int i = tid; i < d / 2; i += blockDim.x) {
-        const float x0 = to_f(k_pre[in + 2 * i]), x1 = to_f(k_pre[in + 2 * i + 1]);
+    if (kt) {
         float c, sn;
-        rope_cs(ga.freq, i, pos, c, sn);
-        kpost[2 * i] = x0 * c - x1 * sn;
-        kpost[2 * i + 1] = x0 * sn + x1 * c;
+        rope_cs(ga.freq, tid, pos, c, sn);
+        kpost[2 * tid] = x0 * c - x1 * sn;
+        kpost[2 * tid + 1] = x0 * sn + x1 * c;
     }
     // ---- routing decision (thread 0).  Lazy promotion inspects the VICTIM's
     // stored bit (written W steps ago), never the new token's gate -- so the new
@@ -276,13 +290,11 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
         event = 0;
         vpage = -1;
         gpage = -1;
-        const int slot = st.local_ptr;
-        int lp = pv.lpt[hidx * pv.n_lp + slot / ps];
         // the Global tail page, loaded alongside (needed if the victim is promoted
         // into a partly filled page): one dependent global round trip less
         const int gi0 = st.global_len;
         const int gp_tail = (gi0 % ps != 0) ? pv.gpt[hidx * pv.n_gp + gi0 / ps] : -1;
-        if (st.local_len < W) {
+        if (!ring_full) {
             // not full: slot == local_len; a slot at a page boundary is the
             // first touch of that ring page (kvstore.cpp:102-107)
             if (slot % ps == 0) {
@@ -318,14 +330,14 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
         nslot = slot % ps;
     }
     __syncthreads();
-    E* pool = reinterpret_cast<E*>(pv.data);
-    // promote: copy victim (K, V, gate, pos, bit) to the Global append slot
+    // promote: the victim (K, V fetched above; gate, pos, bit) to the Global
+    // append slot, then the new token's K/V into the ring slot (each thread
+    // read its victim element before overwriting it)
     if (event == 1 && gpage >= 0 && vpage >= 0) {
-        const E* ks = pool + (size_t)vpage * pv.page_elems() + (size_t)vslot * d;
-        E* kd = pool + (size_t)gpage * pv.page_elems() + (size_t)gslot * d;
-        for (int e = tid; e < d; e += blockDim.x) {
-            kd[e] = ks[e];
-            kd[e + (size_t)ps * d] = ks[e + (size_t)ps * d];
+        if (et) {
+            E* kd = pool + (size_t)gpage * pv.page_elems() + (size_t)gslot * d;
+            kd[tid] = vk;
+            kd[tid + (size_t)ps * d] = vv;
         }
         if (tid == 0) {
             const size_t a = (size_t)vpage * ps + vslot, b = (size_t)gpage * ps + gslot;
@@ -334,13 +346,11 @@ __global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArg
             pv.adm[b] = pv.adm[a];
         }
     }
-    __syncthreads();
-    // write the new token's K/V into the ring slot
     if (npage >= 0) {
-        E* kd = pool + (size_t)npage * pv.page_elems() + (size_t)nslot * d;
-        for (int e = tid; e < d; e += blockDim.x) {
-            kd[e] = from_f<E>(kpost[e]);
-            kd[e + (size_t)ps * d] = v[in + e];
+        if (et) {
+            E* kd = pool + (size_t)npage * pv.page_elems() + (size_t)nslot * d;
+            kd[tid] = from_f<E>(kpost[tid]);
+            kd[tid + (size_t)ps * d] = vnew;
         }
         if (tid == 0) pv.pos[(size_t)npage * ps + nslot] = (int32_t)pos;
     }
