@@ -62,7 +62,10 @@ def test_ctx_create_validates_like_the_reference():
                 dtype=0, topk_budget=0, attn_impl=0, device=0)
     h = C.c_void_p()
     for bad, code in (({"tau": 1.0}, _lib.EINVAL), ({"window": 0}, _lib.EINVAL), ({"head_dim": 7}, _lib.EINVAL),
-                      ({"q_heads": 3, "kv_heads": 2}, _lib.EINVAL)):
+                      ({"q_heads": 3, "kv_heads": 2}, _lib.EINVAL),
+                      # beyond K5's work split: kMaxChunks (512) x 2048 pages per head
+                      ({"max_tokens": 512 * 2048 * 16}, _lib.ENOTSUP),
+                      ({"topk_mode": 1, "page_size": 8}, _lib.ENOTSUP), ({"topk_mode": 2}, _lib.EINVAL)):
         cfg = _lib.Config(**{**base, **bad})
         assert lib.wgkv_ctx_create(C.byref(cfg), C.byref(h)) == code
 
