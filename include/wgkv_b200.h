@@ -169,6 +169,12 @@ int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk,
  * resident entries, out[1] = global entries, out[2] = tokens seen,
  * out[3] = pages allocated */
 int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out);
+/* cache_snapshot (kvstore.cpp:269-286) of sequence slot `seq`: lines
+ * "layer head global|local pos gate" (gate %.17g of the stored fp32 value),
+ * caches layer-major then kv head, Global then Local in position order.
+ * *len = text length; buf (may be NULL) receives it NUL-terminated when
+ * cap > *len, else WGKV_EINVAL. */
+int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* len);
 /* HeadCache::release for every (layer, kv head) of the slots */
 int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq);
 /* pool occupancy: out[0] = capacity, out[1] = free pages */

@@ -249,6 +249,7 @@ class Ref(_Base):
         L.wr_session_head_state.argtypes = [C.c_void_p, C.c_int, C.c_int, _lp]
         L.wr_session_gather.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _lp, _dp, _dp, _dp, _lp, _dp]
         L.wr_session_select_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_long, _lp, _lp]
+        L.wr_session_snapshot.argtypes = [C.c_void_p, C.c_char_p, C.c_long, _lp]
         L.wr_gate_save.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.wr_thread_budget.restype = C.c_int
         L.wr_policy_trace.argtypes = [C.c_int, C.c_long, C.c_long, _u8p, C.c_int, C.c_long, C.c_long, C.c_double,
@@ -457,3 +458,24 @@ class Session:
                                    _ptr(out["global_pos"], _lp), _ptr(out["global_gate"]), _ptr(out["local_k"]),
                                    _ptr(out["local_v"]), _ptr(out["local_pos"], _lp), _ptr(out["local_gate"]))
         return out
+
+    def snapshot(self, native: bool = True) -> str:
+        """cache_snapshot (kvstore.cpp:269-286): one line per resident entry,
+        "layer head global|local pos gate(%.17g)", caches in Session order
+        (layer-major, then kv head), Global then Local in position order.
+        native: the reference's own function (reference backend); else this
+        Python restatement over gather()."""
+        if native and self.P == "wr_":
+            n = C.c_long(0)
+            _check(self.lib.wr_session_snapshot(self.h, None, 0, C.byref(n)), "snapshot")
+            buf = C.create_string_buffer(n.value + 1)
+            _check(self.lib.wr_session_snapshot(self.h, buf, n.value + 1, C.byref(n)), "snapshot")
+            return buf.value.decode()
+        lines = []
+        for layer in range(self.layers):
+            for head in range(self.kv_heads):
+                g = self.gather(layer, head)
+                for kind in ("global", "local"):
+                    for pos, gate in zip(g[kind + "_pos"], g[kind + "_gate"]):
+                        lines.append("%d %d %s %d %.17g\n" % (layer, head, kind, pos, gate))
+        return "".join(lines)

@@ -17,6 +17,7 @@
 #include <exception>
 #include <memory>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "wgkv/attention.hpp"
@@ -395,6 +396,24 @@ int wr_session_gather(void* sp, int layer, int h, double* gk, double* gv, long* 
     if (lpos) std::memcpy(lpos, kv.local_pos.data(), sizeof(long) * L);
     if (lgate) std::memcpy(lgate, kv.local_gate.data(), sizeof(double) * L);
     return 0;
+}
+
+// cache_snapshot (kvstore.cpp:269-286) over the session's caches in Session
+// order (layer-major, then kv head); *len = text length, copied (NUL
+// terminated) when cap > len.
+int wr_session_snapshot(void* sp, char* buf, long cap, long* len) {
+    try {
+        auto& s = *static_cast<RefSession*>(sp);
+        const std::string t = cache_snapshot({s.caches.data(), s.caches.size()}, s.pool);
+        *len = static_cast<long>(t.size());
+        if (buf && cap > *len) {
+            std::memcpy(buf, t.data(), t.size());
+            buf[t.size()] = 0;
+        }
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
 }
 
 int wr_session_select_topk(void* sp, int layer, int h, const double* q, long budget, long* logical, long* n_sel) {

@@ -65,6 +65,7 @@ SIGNATURES = {
     "wgkv_cache_state": ([_vp, _i, _i, _i, C.POINTER(C.c_int64)], _i),
     "wgkv_cache_export": ([_vp, _i, _i, _i] + [_vp] * 8, _i),
     "wgkv_cache_stats": ([_vp, _i, _i, C.POINTER(C.c_int64)], _i),
+    "wgkv_cache_snapshot": ([_vp, _i, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], _i),
     "wgkv_release": ([_vp, _i, _i], _i),
     "wgkv_pool_info": ([_vp, C.POINTER(C.c_int64)], _i),
     "wgkv_vs_pair_count": ([_vp, _l, _l], C.c_uint64),

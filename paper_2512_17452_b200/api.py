@@ -158,6 +158,15 @@ class Session:
         check(self.lib.wgkv_cache_export(self.h, layer, seq, head, *ptrs), "gather")
         return out
 
+    def snapshot(self, seq=0) -> str:
+        """cache_snapshot (kvstore.cpp:269-286) of sequence slot `seq` (the
+        reference's text format; gates are the stored fp32 values)."""
+        n = C.c_size_t(0)
+        check(self.lib.wgkv_cache_snapshot(self.h, seq, None, 0, C.byref(n)), "cache_snapshot")
+        buf = C.create_string_buffer(n.value + 1)
+        check(self.lib.wgkv_cache_snapshot(self.h, seq, buf, n.value + 1, C.byref(n)), "cache_snapshot")
+        return buf.value.decode()
+
     def stats(self, seq0=0, nseq=1) -> dict:
         v = (C.c_int64 * 4)()
         check(self.lib.wgkv_cache_stats(self.h, seq0, nseq, v), "cache_stats")

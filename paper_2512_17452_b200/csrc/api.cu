@@ -730,6 +730,45 @@ int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk,
     return WGKV_OK;
 }
 
+// cache_snapshot (kvstore.cpp:269-286) of one sequence slot: the reference's
+// text format, caches in Session order (layer-major, then kv head), Global
+// then Local entries in position order, gate printed with %.17g (the device
+// keeps gates in fp32, so the digits are those of the fp32 value).
+int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* len) {
+    if (!ctx || !len) return fail(WGKV_EINVAL, "null argument");
+    const auto& c = ctx->cfg;
+    if (seq < 0 || seq >= c.max_seqs) return fail(WGKV_EINVAL, "seq out of range");
+    std::string text;
+    char line[128];
+    for (int l = 0; l < c.layers; ++l)
+        for (int h = 0; h < c.kv_heads; ++h) {
+            int64_t lens[6];
+            int st = wgkv_cache_state(ctx, l, seq, h, lens);
+            if (st) return st;
+            const size_t G = (size_t)lens[2], Lc = (size_t)lens[0];
+            std::vector<int64_t> gpos(G), lpos(Lc);
+            std::vector<float> gg(G), lg(Lc);
+            st = wgkv_cache_export(ctx, l, seq, h, nullptr, nullptr, gpos.data(), gg.data(), nullptr, nullptr,
+                                   lpos.data(), lg.data());
+            if (st) return st;
+            for (size_t i = 0; i < G; ++i) {
+                std::snprintf(line, sizeof(line), "%d %d global %ld %.17g\n", l, h, (long)gpos[i], (double)gg[i]);
+                text += line;
+            }
+            for (size_t i = 0; i < Lc; ++i) {
+                std::snprintf(line, sizeof(line), "%d %d local %ld %.17g\n", l, h, (long)lpos[i], (double)lg[i]);
+                text += line;
+            }
+        }
+    *len = text.size();
+    if (buf) {
+        if (cap <= text.size()) return fail(WGKV_EINVAL, "snapshot buffer too small (see *len)");
+        std::memcpy(buf, text.data(), text.size());
+        buf[text.size()] = 0;
+    }
+    return WGKV_OK;
+}
+
 int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
     const auto& c = ctx->cfg;

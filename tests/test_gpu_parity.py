@@ -231,6 +231,8 @@ def test_policy_sessions_vs_oracle(W, orc, kind):
             assert rel_err(o[p], ro[p]) < TOL["bf16"]
     for h in range(hkv):
         assert np.array_equal(s.gather(0, 0, h)["global_pos"], r.gather(0, h)["global_pos"])
+    # cache_snapshot (kvstore.cpp:269-286) text, identical (forced gates are 0 / 1, exact in fp32)
+    assert s.snapshot(0) == r.snapshot(native=False)
 
 
 # -------------------------------------------------------------- error paths --

@@ -81,3 +81,7 @@ def test_session_identical(orc, ref, hq, hkv, topk, ps):
             ga, gb = sa.gather(l, h), sb.gather(l, h)
             for key in ga:
                 assert np.array_equal(ga[key], gb[key]), key
+    # cache_snapshot text (kvstore.cpp:269-286): the reference's own function
+    # pins the Python restatement the GPU test compares against
+    snap = sb.snapshot(native=True)
+    assert snap and snap == sb.snapshot(native=False) == sa.snapshot()
