@@ -41,6 +41,9 @@ constexpr int PID_CAP = kDecPidCap;  // pages per work item (staged page ids)
 #ifndef WGKV_K5_RULE
 #define WGKV_K5_RULE 1
 #endif
+#ifndef WGKV_K5_CAPCH
+#define WGKV_K5_CAPCH 24  // chunks per (seq, kv head) pair the few-long-pairs rule aims at
+#endif
 #ifndef WGKV_K5_MIN_PAGES
 #define WGKV_K5_MIN_PAGES 8
 #endif
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
 #if WGKV_K5_RULE == 1
         // few, long pairs (small batches): cap the chunks per pair near 24 (the
         // combine merges every chunk) while keeping >= grid/2 items in flight
-        cp = max(cp, (int)min((long)(npmax + 23) / 24, (2 * total + gridDim.x - 1) / gridDim.x));
+        cp = max(cp, (int)min((long)(npmax + WGKV_K5_CAPCH - 1) / WGKV_K5_CAPCH, (2 * total + gridDim.x - 1) / gridDim.x));
 #endif
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
