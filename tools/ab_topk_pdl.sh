@@ -1,3 +1,6 @@
+#!/bin/bash
+# Interleaved A/B of the top-k decode chain: PDL launches (product) vs plain launches (WGKV_TOPK_NOPDL=1),
+# printing K5-with-selection and whole-decode-layer microseconds from profiles/decode_breakdown.py.
 for args in "--T 1048576 --batch 1 --hq 4 --hkv 1 --topk 256" "--topk 256" "--T 1048576 --batch 1 --hq 4 --hkv 1 --topk 256 --quest"; do
 for r in 1 2; do
   for v in 0 1; do
