@@ -90,6 +90,15 @@ public:
     }
     // HeadCache::release (kvstore.cpp:243-251) for every head of the slots
     void release(int seq0, int nseq) { throw_on(wgkv_release(ctx_, seq0, nseq), "release"); }
+    // cache_snapshot (kvstore.cpp:269-286) of one sequence slot (gate digits of the stored fp32 value)
+    std::string cache_snapshot(int seq = 0) {
+        size_t n = 0;
+        throw_on(wgkv_cache_snapshot(ctx_, seq, nullptr, 0, &n), "cache_snapshot");
+        std::string text(n + 1, '\0');
+        throw_on(wgkv_cache_snapshot(ctx_, seq, text.data(), text.size(), &n), "cache_snapshot");
+        text.resize(n);
+        return text;
+    }
 
     wgkv_ctx* handle() const { return ctx_; }
 
