@@ -302,7 +302,7 @@ def run_gpu(args, cfg):
                 graph["g"].replay()
             else:
                 decode_token_step()
-            launches["n"] += 4 * L  # append, gate (side stream), attention, combine (+ a counter memset node)
+            launches["n"] += 2 * L  # per layer: K5 (attention over the pre-append cache) + finish (merge, new token, K4)
 
     def barrier():
         torch.cuda.synchronize(dev)

@@ -72,6 +72,10 @@ typedef struct wgkv_config {
     int attn_impl;       /* WGKV_ATTN_* */
     int device;          /* CUDA device ordinal */
     int topk_mode;       /* WGKV_TOPK_*: how select_topk_pages scores a page (topk_budget > 0) */
+    long decode_chunk_pages; /* 0: K5 sizes its split-KV chunks from the step's work (fastest);
+                              * > 0: pages per chunk pinned, so a (seq, kv head)'s decode arithmetic
+                              * -- and its output bits -- do not depend on which other heads share
+                              * the launch (KV-head sharding reproduces the unsharded result) */
 } wgkv_config;
 
 /* page score used by the top-k selection (wgkv_config.topk_mode)
@@ -146,7 +150,8 @@ int wgkv_prefill_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, con
  * K1(T=1, exact fp64) + K4: RoPE + gate + HeadCache::local_write with lazy
  * promotion (kvstore.cpp:122-158) for the token at position tokens_seen.
  *   k_pre, v [nseq][kv_heads][d]; events_out (optional, device int32
- *   [nseq][kv_heads]): 0 none, 1 promoted, 2 dropped; g_out optional float. */
+ *   [nseq][kv_heads]): 0 none, 1 promoted, 2 dropped, -1 failed (out of
+ *   pages, latched; the head is left unchanged); g_out optional float. */
 int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
                         const float* forced_g, float* g_out, int32_t* events_out);
 /* K5 (+K6 when topk_budget > 0): gather-free split-KV attention over the
@@ -156,6 +161,21 @@ int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void
 int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out);
 int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, const void* k_pre, const void* v,
                       const float* forced_g, void* out, float* g_out, int32_t* events_out);
+
+/* GateTrace of one decode step (records.hpp:11-29; engine.cpp:300-305 records
+ * g and g >= tau for every decoded token).  Device pointers, [nseq][kv_heads],
+ * any may be NULL.  The decode gate is evaluated in fp64 in the reference's
+ * exact operation order (sequential dots, sequential z2 sum), so bits equal
+ * the reference's except possibly where near_tau is set. */
+typedef struct wgkv_decode_trace {
+    float* g;          /* the new token's gate score (fp32 copy of the fp64 value) */
+    uint8_t* bits;     /* g >= tau (admission bit the ring will promote on) */
+    uint8_t* near_tau; /* 1 where |g - tau| < 1e-6: reported per north_star */
+    int32_t* events;   /* ring victim: 0 none, 1 promoted, 2 dropped, -1 failed (ENOPAGES latched) */
+} wgkv_decode_trace;
+/* wgkv_decode_layer with the full trace (trace may be NULL) */
+int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, const void* k_pre,
+                             const void* v, const float* forced_g, void* out, const wgkv_decode_trace* trace);
 
 /* ---- state, export, lifecycle (host, synchronising) ----------------------
  * lens[0..5] = local_len, local_ptr, global_len, tokens_seen, n_local_pages,

@@ -201,6 +201,13 @@ class Oracle(_Base):
         L.wo_sigmoid.restype = C.c_double
         L.wo_softmax.argtypes = [_dp, C.c_long, _dp]
         L.wo_attn_dense.argtypes = [_dp, C.c_long, _dp, _dp, C.c_long, C.c_int, C.c_double, C.c_long, _dp, _u64p]
+        L.wo_rope_rows.argtypes = [_dp, C.c_long, C.c_int, C.c_long, C.c_double]
+
+    def rope_rows(self, k, pos0: int = 0, base: float = 10000.0) -> np.ndarray:
+        """apply_rope_inplace on rows [n][d]: row r at position pos0 + r (numerics.cpp:71-77)."""
+        k = _f64(k).copy()
+        _check(self.lib.wo_rope_rows(_ptr(k), k.shape[0], k.shape[1], pos0, base), "rope_rows")
+        return k
 
     def uniform_int(self, seed: int, lo: int, hi: int, n: int) -> np.ndarray:
         out = np.empty(n, np.int64)
@@ -250,6 +257,7 @@ class Ref(_Base):
         L.wr_session_gather.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _lp, _dp, _dp, _dp, _lp, _dp]
         L.wr_session_select_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_long, _lp, _lp]
         L.wr_session_snapshot.argtypes = [C.c_void_p, C.c_char_p, C.c_long, _lp]
+        L.wr_session_cache_stats.argtypes = [C.c_void_p, _dp]
         L.wr_gate_save.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.wr_thread_budget.restype = C.c_int
         L.wr_policy_trace.argtypes = [C.c_int, C.c_long, C.c_long, _u8p, C.c_int, C.c_long, C.c_long, C.c_double,
@@ -458,6 +466,25 @@ class Session:
                                    _ptr(out["global_pos"], _lp), _ptr(out["global_gate"]), _ptr(out["local_k"]),
                                    _ptr(out["local_v"]), _ptr(out["local_pos"], _lp), _ptr(out["local_gate"]))
         return out
+
+    def cache_stats(self) -> dict:
+        """cache_stats (kvstore.cpp:253-267) over the session's caches: the
+        reference's own function (reference backend), else recounted from
+        gather() per its definition."""
+        if self.P == "wr_":
+            v = np.zeros(3)
+            _check(self.lib.wr_session_cache_stats(self.h, _ptr(v)), "cache_stats")
+            return dict(resident_entries=int(v[0]), admitted_fraction=float(v[1]), pages_allocated=int(v[2]))
+        res = glob = seen = pages = 0
+        for layer in range(self.layers):
+            for head in range(self.kv_heads):
+                hc = HeadCache(self.b, layer, head, 1, handle=self.lib.wo_session_head(self.h, layer, head))
+                s = hc.state()
+                res += s["local_len"] + s["global_len"]
+                glob += s["global_len"]
+                seen += s["tokens_seen"]
+                pages += s["n_local_pages"] + s["n_global_pages"]
+        return dict(resident_entries=res, admitted_fraction=glob / seen if seen else 0.0, pages_allocated=pages)
 
     def snapshot(self, native: bool = True) -> str:
         """cache_snapshot (kvstore.cpp:269-286): one line per resident entry,

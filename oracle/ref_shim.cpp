@@ -416,6 +416,21 @@ int wr_session_snapshot(void* sp, char* buf, long cap, long* len) {
     }
 }
 
+// cache_stats (kvstore.cpp:253-267) over every HeadCache of the session:
+// out = {resident_entries, admitted_fraction, pages_allocated}
+int wr_session_cache_stats(void* sp, double* out) {
+    try {
+        auto& s = *static_cast<RefSession*>(sp);
+        const CacheStats st = cache_stats({s.caches.data(), s.caches.size()}, s.pool);
+        out[0] = static_cast<double>(st.resident_entries);
+        out[1] = st.admitted_fraction;
+        out[2] = static_cast<double>(st.pages_allocated);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
 int wr_session_select_topk(void* sp, int layer, int h, const double* q, long budget, long* logical, long* n_sel) {
     auto& s = *static_cast<RefSession*>(sp);
     try {

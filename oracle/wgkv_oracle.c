@@ -128,6 +128,16 @@ int wo_rope(double* k, int head_dim, long position, double base, double sign) {
     return WO_OK;
 }
 
+/* apply_rope_inplace over consecutive rows (numerics.cpp:71-77): row r of
+ * [rows][head_dim] at position pos0 + r */
+int wo_rope_rows(double* k, long rows, int head_dim, long pos0, double base) {
+    for (long r = 0; r < rows; ++r) {
+        const int st = wo_rope(k + r * head_dim, head_dim, pos0 + r, base, 1.0);
+        if (st != WO_OK) return st;
+    }
+    return WO_OK;
+}
+
 /* max-subtracted softmax; -inf -> exact 0; all -inf is an error (numerics.cpp:13-31) */
 int wo_softmax(const double* logits, long n, double* out) {
     if (n <= 0) return WO_EINVAL;

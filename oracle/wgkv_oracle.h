@@ -57,6 +57,8 @@ double wo_sigmoid(double x);
 double wo_dot(const double* a, const double* b, long n);
 int wo_rope(double* k, int head_dim, long position, double base, double sign);
 int wo_softmax(const double* logits, long n, double* out);
+/* wo_rope over rows [rows][head_dim], row r at position pos0 + r (sign +1) */
+int wo_rope_rows(double* k, long rows, int head_dim, long pos0, double base);
 
 /* ---- gating (gating.cpp:49-59, 149-190) --------------------------------
  * One parameter block per (layer, kv-head) in layer-major order, each of

@@ -42,7 +42,13 @@ class Config(C.Structure):
                 ("head_dim", C.c_int), ("hidden", C.c_int), ("window", C.c_long), ("tau", C.c_double),
                 ("rope_base", C.c_double), ("page_size", C.c_int), ("max_seqs", C.c_int), ("max_tokens", C.c_long),
                 ("max_prefill_tokens", C.c_long), ("capacity_pages", C.c_long), ("dtype", C.c_int),
-                ("topk_budget", C.c_long), ("attn_impl", C.c_int), ("device", C.c_int), ("topk_mode", C.c_int)]
+                ("topk_budget", C.c_long), ("attn_impl", C.c_int), ("device", C.c_int), ("topk_mode", C.c_int),
+                ("decode_chunk_pages", C.c_long)]
+
+
+class DecodeTrace(C.Structure):
+    """wgkv_decode_trace: device pointers (or None) of the step's GateTrace."""
+    _fields_ = [("g", C.c_void_p), ("bits", C.c_void_p), ("near_tau", C.c_void_p), ("events", C.c_void_p)]
 
 
 _vp, _i, _l = C.c_void_p, C.c_int, C.c_long
@@ -62,6 +68,7 @@ SIGNATURES = {
     "wgkv_decode_step_kv": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp], _i),
     "wgkv_decode_attn": ([_vp, _i, _i, _i, _vp, _vp], _i),
     "wgkv_decode_layer": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "wgkv_decode_layer_traced": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, C.POINTER(DecodeTrace)], _i),
     "wgkv_cache_state": ([_vp, _i, _i, _i, C.POINTER(C.c_int64)], _i),
     "wgkv_cache_export": ([_vp, _i, _i, _i] + [_vp] * 8, _i),
     "wgkv_cache_stats": ([_vp, _i, _i, C.POINTER(C.c_int64)], _i),

@@ -48,14 +48,14 @@ class Session:
     def __init__(self, layers, q_heads, kv_heads, head_dim, hidden, window, tau=0.1, rope_base=10000.0,
                  page_size=16, max_seqs=1, max_tokens=4096, max_prefill_tokens=None, capacity_pages=0,
                  dtype=BF16, topk_budget=0, attn_impl=ATTN_AUTO, device=0, kv_head_offset=0, gate_bank=None,
-                 topk_mode=0):
+                 topk_mode=0, decode_chunk_pages=0):
         self.lib = _lib.load()
         cfg = _lib.Config(layers=layers, q_heads=q_heads, kv_heads=kv_heads, kv_head_offset=kv_head_offset,
                           head_dim=head_dim, hidden=hidden, window=window, tau=tau, rope_base=rope_base,
                           page_size=page_size, max_seqs=max_seqs, max_tokens=max_tokens,
                           max_prefill_tokens=max_prefill_tokens or max_tokens, capacity_pages=capacity_pages,
                           dtype=dtype, topk_budget=topk_budget, attn_impl=attn_impl, device=device,
-                          topk_mode=topk_mode)
+                          topk_mode=topk_mode, decode_chunk_pages=decode_chunk_pages)
         self.cfg = cfg
         self.device = torch.device("cuda", device)
         self.dtype = _TORCH_DT[dtype]
@@ -125,18 +125,31 @@ class Session:
         return (out, g, bits) if want_gates else out
 
     # ---- decode ------------------------------------------------------------
-    def decode_layer(self, layer, q, k_pre, v, seq0=0, forced_gates=None, out=None, want_events=False):
-        """q [nseq][q_heads][d], k_pre/v [nseq][kv_heads][d] -> out [nseq][q_heads][d]."""
+    def decode_layer(self, layer, q, k_pre, v, seq0=0, forced_gates=None, out=None, want_events=False,
+                     want_trace=False):
+        """q [nseq][q_heads][d], k_pre/v [nseq][kv_heads][d] -> out [nseq][q_heads][d].
+
+        want_events: also return (g, events); want_trace: also return the step's
+        GateTrace dict (g, bits, near_tau, events) -- wgkv_decode_layer_traced."""
         nseq = q.shape[0]
         if out is None:
             out = torch.empty_like(q)
-        g = ev = None
-        if want_events:
-            g = torch.empty((nseq, self.cfg.kv_heads), dtype=torch.float32, device=self.device)
-            ev = torch.empty((nseq, self.cfg.kv_heads), dtype=torch.int32, device=self.device)
-        check(self.lib.wgkv_decode_layer(self.h, layer, seq0, nseq, _p(q), _p(k_pre), _p(v), _p(forced_gates),
-                                         _p(out), _p(g), _p(ev)), "Session::decode_step")
-        return (out, g, ev) if want_events else out
+        tr = None
+        if want_events or want_trace:
+            H = self.cfg.kv_heads
+            tr = dict(g=torch.empty((nseq, H), dtype=torch.float32, device=self.device),
+                      bits=torch.empty((nseq, H), dtype=torch.uint8, device=self.device),
+                      near_tau=torch.empty((nseq, H), dtype=torch.uint8, device=self.device),
+                      events=torch.empty((nseq, H), dtype=torch.int32, device=self.device))
+            ct = _lib.DecodeTrace(*(tr[k].data_ptr() for k in ("g", "bits", "near_tau", "events")))
+            check(self.lib.wgkv_decode_layer_traced(self.h, layer, seq0, nseq, _p(q), _p(k_pre), _p(v),
+                                                    _p(forced_gates), _p(out), C.byref(ct)), "Session::decode_step")
+        else:
+            check(self.lib.wgkv_decode_layer_traced(self.h, layer, seq0, nseq, _p(q), _p(k_pre), _p(v),
+                                                    _p(forced_gates), _p(out), None), "Session::decode_step")
+        if want_trace:
+            return out, tr
+        return (out, tr["g"], tr["events"]) if want_events else out
 
     # ---- state / audit -------------------------------------------------------
     def state(self, layer, seq, head) -> dict:

@@ -16,6 +16,7 @@
 // K4 replaces HeadCache::local_write + promote (kvstore.cpp:122-158) fused
 // with the decode-time gate (gate_forward, gating.cpp:158-171) and RoPE.
 #include "admit.cuh"
+#include "append.cuh"
 #include "gate.cuh"
 
 namespace wgkv {
@@ -80,15 +81,7 @@ __global__ void __launch_bounds__(1024) admit_plan_kernel(PoolView pv, int layer
     const long hidx = pv.head_index(layer, seq0 + s, h);
     if (tid == 0) {
         co[nchunk] = G;
-        const int need = ng + nl;
-        int top = atomicSub(pv.free_top, need);
-        if (top < need) {
-            atomicAdd(pv.free_top, need);
-            atomicExch(pv.err, WGKV_ENOPAGES);
-            page_base = -1;
-        } else {
-            page_base = top;
-        }
+        page_base = pool_claim(pv, ng + nl);
         // on a failed claim the head keeps no pages (the error is latched and
         // surfaces at the next wgkv_sync, like the reference's throw)
         HeadState st;
@@ -230,227 +223,26 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 }
 
 // ---------------------------------------------------------------------------
-// K4: decode append.  One CTA (256 threads) per (seq, kv head).
+// K4 standalone: one CTA per (seq, kv head) of the call (append.cuh)
 // ---------------------------------------------------------------------------
 template <typename E>
-__device__ __forceinline__ void gate_section(const PoolView& pv, const GateArgs& ga, int layer, int s, int h, long pos,
-                                             size_t in, int npage, int nslot, const E* __restrict__ k_pre,
-                                             const float* __restrict__ forced_g, float* __restrict__ g_out,
-                                             double* xs, double* scratch);
-
-// mode 0: append + gate; mode 1: append only (slot recorded for mode 2 =
-// decode_gate_kernel on a side stream).
-template <typename E>
-__global__ void __launch_bounds__(256) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0, long W,
-                                                             const E* __restrict__ k_pre, const E* __restrict__ v,
-                                                             const float* __restrict__ forced_g,
-                                                             float* __restrict__ g_out, int32_t* __restrict__ events,
-                                                             int* __restrict__ work_counter, int mode,
-                                                             int* __restrict__ slot_rec) {
-    extern __shared__ double dsh[];
-    const int s = blockIdx.x / pv.kv_heads, h = blockIdx.x % pv.kv_heads;
-    const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
-    const long hidx = pv.head_index(layer, seq0 + s, h);
-    double* xs = dsh;                       // [2d]
-    double* scratch = xs + 2 * d;           // [2*hidden + 32]
-    float* kpost = reinterpret_cast<float*>(scratch + 2 * ga.hidden + 32);  // [d]
-    __shared__ int vpage, vslot, gpage, gslot, npage, nslot, event;
-    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
-    E* pool = reinterpret_cast<E*>(pv.data);
-    // the new token's inputs do not depend on the cache state: loads first
-    const bool kt = tid < d / 2, et = tid < d;
-    const float x0 = kt ? to_f(k_pre[in + 2 * tid]) : 0.f, x1 = kt ? to_f(k_pre[in + 2 * tid + 1]) : 0.f;
-    const E vnew = et ? v[in + tid] : E();
-    // every thread reads the state and the ring page under local_ptr itself
-    // (broadcast loads), so the victim's K/V is fetched speculatively in the
-    // same round as its admission bit instead of after thread 0's decision
-    HeadState st = pv.state[hidx];
-    const long pos = st.tokens_seen;
-    const int slot = st.local_ptr;
-    int lp = pv.lpt[hidx * pv.n_lp + slot / ps];
-    const bool ring_full = st.local_len >= W;
-    E vk = E(), vv = E();
-    if (ring_full && lp >= 0 && et) {
-        const E* ks = pool + (size_t)lp * pv.page_elems() + (size_t)(slot % ps) * d;
-        vk = ks[tid];
-        vv = ks[tid + (size_t)ps * d];
-    }
-    // RoPE of the stored key (fp32); the fp64 gate feature is built after the
-    // dependent-launch trigger below
-    if (kt) {
-        float c, sn;
-        rope_cs(ga.freq, tid, pos, c, sn);
-        kpost[2 * tid] = x0 * c - x1 * sn;
-        kpost[2 * tid + 1] = x0 * sn + x1 * c;
-    }
-    // ---- routing decision (thread 0).  Lazy promotion inspects the VICTIM's
-    // stored bit (written W steps ago), never the new token's gate -- so the new
-    // token's gate is off the critical path of this step's attention.
-    if (tid == 0) {
-        event = 0;
-        vpage = -1;
-        gpage = -1;
-        // the Global tail page, loaded alongside (needed if the victim is promoted
-        // into a partly filled page): one dependent global round trip less
-        const int gi0 = st.global_len;
-        const int gp_tail = (gi0 % ps != 0) ? pv.gpt[hidx * pv.n_gp + gi0 / ps] : -1;
-        if (!ring_full) {
-            // not full: slot == local_len; a slot at a page boundary is the
-            // first touch of that ring page (kvstore.cpp:102-107)
-            if (slot % ps == 0) {
-                lp = pool_pop(pv);
-                pv.lpt[hidx * pv.n_lp + slot / ps] = lp;
-            }
-            st.local_len += 1;
-        } else {
-            // inspect the victim under local_ptr (kvstore.cpp:143-147)
-            const size_t mi = (size_t)(lp < 0 ? 0 : lp) * ps + slot % ps;
-            if (lp < 0) {
-                event = 0;  // head lost its pages to an earlier ENOPAGES
-            } else if (pv.adm[mi]) {
-                event = 1;
-                const int gi = st.global_len;
-                int gp;
-                if (gi % ps == 0) {
-                    gp = pool_pop(pv);
-                    pv.gpt[hidx * pv.n_gp + gi / ps] = gp;
-                } else {
-                    gp = gp_tail;
-                }
-                vpage = lp;
-                vslot = slot % ps;
-                gpage = gp;
-                gslot = gi % ps;
-                if (gp >= 0) st.global_len += 1;
-            } else {
-                event = 2;
-            }
-        }
-        npage = lp;
-        nslot = slot % ps;
-    }
-    __syncthreads();
-    // promote: the victim (K, V fetched above; gate, pos, bit) to the Global
-    // append slot, then the new token's K/V into the ring slot (each thread
-    // read its victim element before overwriting it)
-    if (event == 1 && gpage >= 0 && vpage >= 0) {
-        if (et) {
-            E* kd = pool + (size_t)gpage * pv.page_elems() + (size_t)gslot * d;
-            kd[tid] = vk;
-            kd[tid + (size_t)ps * d] = vv;
-        }
-        if (tid == 0) {
-            const size_t a = (size_t)vpage * ps + vslot, b = (size_t)gpage * ps + gslot;
-            pv.gate[b] = pv.gate[a];
-            pv.pos[b] = pv.pos[a];
-            pv.adm[b] = pv.adm[a];
-        }
-    }
-    if (npage >= 0) {
-        if (et) {
-            E* kd = pool + (size_t)npage * pv.page_elems() + (size_t)nslot * d;
-            kd[tid] = from_f<E>(kpost[tid]);
-            kd[tid + (size_t)ps * d] = vnew;
-        }
-        if (tid == 0) pv.pos[(size_t)npage * ps + nslot] = (int32_t)pos;
-    }
-    if (tid == 0) {
-        HeadState nst = st;
-        nst.local_ptr = (int)((st.local_ptr + 1) % W);
-        nst.tokens_seen += 1;
-        pv.state[hidx] = nst;
-        if (events) events[(size_t)s * pv.kv_heads + h] = event;
-        if (work_counter) {  // K5's work-stealing counter and this (seq, head)'s chunk-merge counter
-            if (blockIdx.x == 0) work_counter[0] = 0;
-            work_counter[1 + blockIdx.x] = 0;
-        }
-    }
-    // everything K5 reads (pages, tables, state) is written: let the attention
-    // kernel (launched as a programmatic dependent) start now
-    __threadfence();
-    __syncthreads();
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (mode == 1 && !forced_g) {  // the gate runs as mode 2 on a side stream
-        if (tid == 0) slot_rec[(size_t)s * pv.kv_heads + h] = npage >= 0 ? npage * ps + nslot : -1;
-        return;
-    }
-    gate_section(pv, ga, layer, s, h, pos, in, npage, nslot, k_pre, forced_g, g_out, xs, scratch);
-}
-
-// Mode 2 of K4: the new token's gate only, for the slot mode 1 recorded.  Runs
-// concurrently with K5 (nothing reads the new slot's bit until it is the ring
-// victim W steps later).
-template <typename E>
-__global__ void __launch_bounds__(1024) decode_gate_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
-                                                           const E* __restrict__ k_pre, float* __restrict__ g_out,
-                                                           const int* __restrict__ slot_rec) {
-    extern __shared__ double dsh[];
-    const int s = blockIdx.x / pv.kv_heads, h = blockIdx.x % pv.kv_heads;
-    const int d = pv.head_dim, ps = pv.page_size;
-    double* xs = dsh;
-    double* scratch = xs + 2 * d;
-    const long hidx = pv.head_index(layer, seq0 + s, h);
-    const long pos = pv.state[hidx].tokens_seen - 1;
-    const int rec = slot_rec[(size_t)s * pv.kv_heads + h];
-    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
-    gate_section(pv, ga, layer, s, h, pos, in, rec >= 0 ? rec / ps : -1, rec >= 0 ? rec % ps : 0, k_pre,
-                 (const float*)nullptr, g_out, xs, scratch);
-}
-
-// the new token's gate (gate_forward, gating.cpp:158-171), fp64, written into
-// its ring slot's metadata (whole CTA)
-template <typename E>
-__device__ __forceinline__ void gate_section(const PoolView& pv, const GateArgs& ga, int layer, int s, int h, long pos,
-                                             size_t in, int npage, int nslot, const E* __restrict__ k_pre,
-                                             const float* __restrict__ forced_g, float* __restrict__ g_out,
-                                             double* xs, double* scratch) {
-    const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
-    double g;
-    if (forced_g) {
-        g = forced_g[(size_t)s * pv.kv_heads + h];
-    } else {
-        for (int i = tid; i < d / 2; i += blockDim.x) {
-            const double x0 = to_f(k_pre[in + 2 * i]), x1 = to_f(k_pre[in + 2 * i + 1]);
-            const double angle = (double)pos * ga.freq[i];
-            const double cd = cos(angle), sd = sin(angle);
-            xs[2 * i] = x0;
-            xs[2 * i + 1] = x1;
-            xs[d + 2 * i] = x0 * cd - x1 * sd;
-            xs[d + 2 * i + 1] = x0 * sd + x1 * cd;
-        }
-        __syncthreads();
-        g = d == 128 ? gate_fp64_block<256>(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch)
-                     : gate_fp64_block(ga.gd(), layer * pv.kv_heads + h, xs, d, scratch);
-    }
-    if (tid == 0) {
-        if (npage >= 0) {
-            const size_t b = (size_t)npage * ps + nslot;
-            pv.gate[b] = (float)g;
-            pv.adm[b] = g >= ga.tau ? 1 : 0;
-        }
-        if (g_out) g_out[(size_t)s * pv.kv_heads + h] = (float)g;
-    }
+__global__ void __launch_bounds__(kAppendThreads) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
+                                                                        long W, const E* __restrict__ k_pre,
+                                                                        const E* __restrict__ v,
+                                                                        const float* __restrict__ forced_g,
+                                                                        DecodeTrace tr) {
+    extern __shared__ __align__(16) uint8_t append_smem[];
+    append_token<E>(pv, ga, layer, seq0, blockIdx.x / pv.kv_heads, blockIdx.x % pv.kv_heads, W, k_pre, v, forced_g,
+                    tr, append_smem);
 }
 
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
-                         const E* k_pre, const E* v, const float* forced_g, float* g_out, int32_t* events,
-                         int* work_counter, int* slot_rec, cudaStream_t st, cudaStream_t side,
-                         cudaEvent_t ev_fork, cudaEvent_t ev_join) {
-    const size_t smem = sizeof(double) * (2 * pv.head_dim + 2 * ga.hidden + 32) + sizeof(float) * pv.head_dim;
-    const bool split = side != nullptr && forced_g == nullptr;
-    decode_append_kernel<E><<<nseq * pv.kv_heads, 256, smem, st>>>(pv, ga, layer, seq0, W, k_pre, v, forced_g, g_out,
-                                                                   events, work_counter, split ? 1 : 0, slot_rec);
-    if (split) {  // fork: the gate on the side stream, joined by the caller with ev_join
-        cudaEventRecord(ev_fork, st);
-        cudaStreamWaitEvent(side, ev_fork, 0);
-        // 1024 threads: 32 warps x 4 hidden units cover hidden = 128 in one pass.
-        // (256-thread CTAs, which fit beside the two persistent K5 CTAs of an SM,
-        // measured 3-4 % faster per eager decode layer but 1.5 % slower in the
-        // graph-captured serving bench -- kept at 1024.)
-        decode_gate_kernel<E><<<nseq * pv.kv_heads, 1024, smem, side>>>(pv, ga, layer, seq0, k_pre, g_out, slot_rec);
-        cudaEventRecord(ev_join, side);
-    }
+                         const E* k_pre, const E* v, const float* forced_g, const DecodeTrace& tr, cudaStream_t st) {
+    const size_t smem = append_smem_bytes(pv.head_dim, ga.hidden);
+    if (ensure_smem(decode_append_kernel<E>, smem) != cudaSuccess) return WGKV_ECUDA;
+    decode_append_kernel<E><<<nseq * pv.kv_heads, kAppendThreads, smem, st>>>(pv, ga, layer, seq0, W, k_pre, v,
+                                                                               forced_g, tr);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -458,8 +250,7 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     template int launch_admit_prefill<E>(const PoolView&, int, int, int, long, long, const E*, const E*,          \
                                          const float*, const uint8_t*, int32_t*, cudaStream_t);                   \
     template int launch_decode_append<E>(const PoolView&, const GateArgs&, int, int, int, long, const E*, const E*, \
-                                         const float*, float*, int32_t*, int*, int*, cudaStream_t, cudaStream_t,  \
-                                         cudaEvent_t, cudaEvent_t);
+                                         const float*, const DecodeTrace&, cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)
 #undef INST

@@ -7,7 +7,10 @@
 #include <cstring>
 #include <cstdlib>
 #include <fstream>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "admit.cuh"
@@ -20,7 +23,51 @@ using namespace wgkv;
 static thread_local std::string g_last_error;
 void wgkv_set_error(const std::string& msg) { g_last_error = msg; }
 
+namespace wgkv {
+
+int num_sms() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+    return n;
+}
+
+cudaError_t ensure_smem_attr(const void* func, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{func, dev}];
+    if (smem <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
+
+}  // namespace wgkv
+
 namespace {
+
+// every entry point runs on its context's device (one host thread may drive
+// contexts on several GPUs) and restores the caller's device on return
+struct DevGuard {
+    int prev = -1, dev;
+    explicit DevGuard(int d) : dev(d) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
 
 int fail(int code, const std::string& msg) {
     wgkv_set_error(msg);
@@ -50,19 +97,94 @@ __global__ void release_kernel(PoolView pv, int layers, int seq0, int nseq) {
     const HeadState st = pv.state[hidx];
     const int ng = (st.global_len + pv.page_size - 1) / pv.page_size;
     const int nl = (min(st.local_len, 0x7fffffff) + pv.page_size - 1) / pv.page_size;
+    const int n = nl + ng;
+    auto page_at = [&](int i) -> int {  // i-th page in reverse allocation order
+        const int k = n - 1 - i;
+        return k < ng ? pv.gpt[hidx * pv.n_gp + k] : pv.lpt[hidx * pv.n_lp + (k - ng)];
+    };
+    // pass 1: count the pages the head really owns (a failed allocation left
+    // -1 in its table; those are never pushed)
+    __shared__ int wsum[32];
     __shared__ int base;
-    if (threadIdx.x == 0) base = atomicAdd(pv.free_top, nl + ng);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int cnt = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) cnt += page_at(i) >= 0;
+    for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) wsum[wid] = cnt;
     __syncthreads();
-    // pushed in reverse allocation order (Global pages then Local, admit_plan's
-    // pop order), so re-allocating pops the same ascending physical runs: a
-    // head's Global pages stay physically contiguous, which lets K3 load a
-    // 128-key vertical block with one TMA box per dim half
-    for (int i = threadIdx.x; i < nl + ng; i += blockDim.x) {
-        const int k = nl + ng - 1 - i;  // allocation index
-        pv.free_stack[base + i] = k < ng ? pv.gpt[hidx * pv.n_gp + k] : pv.lpt[hidx * pv.n_lp + (k - ng)];
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < nw; ++w) tot += wsum[w];
+        base = atomicAdd(pv.free_top, tot);
+    }
+    __syncthreads();
+    // pass 2: order-preserving compaction.  Pushed in reverse allocation order
+    // (Global pages then Local, admit_plan's pop order), so re-allocating pops
+    // the same ascending physical runs: a head's Global pages stay physically
+    // contiguous, which lets K3 load a 128-key vertical block with one TMA box
+    // per dim half
+    __shared__ int wpre[32];
+    int run = base;
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const int page = i < n ? page_at(i) : -1;
+        const unsigned m = __ballot_sync(0xffffffffu, page >= 0);
+        __syncthreads();
+        if (lane == 0) wpre[wid] = __popc(m);
+        __syncthreads();
+        int off = run;
+        for (int w = 0; w < wid; ++w) off += wpre[w];
+        if (page >= 0) pv.free_stack[off + __popc(m & ((1u << lane) - 1u))] = page;
+        for (int w = 0; w < nw; ++w) run += wpre[w];
     }
     __syncthreads();
     if (threadIdx.x == 0) pv.state[hidx] = HeadState{0, 0, 0, 0};
+}
+
+// HeadCache::gather (kvstore.cpp:205-241) of one head into position order:
+// rows [0, G) Global by logical index, rows [G, G+Lc) the ring unrolled from
+// `start`; one warp per row, K/V widened to fp32 (k/v may be null)
+__global__ void export_rows_kernel(PoolView pv, long hidx, long W, int G, int Lc, int start, int esz,
+                                   float* __restrict__ k, float* __restrict__ v, float* __restrict__ gate,
+                                   int32_t* __restrict__ pos) {
+    const int lane = threadIdx.x & 31;
+    const long r = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= (long)G + Lc) return;
+    const int ps = pv.page_size, d = pv.head_dim;
+    int page, slot;
+    if (r < G) {
+        page = pv.gpt[hidx * pv.n_gp + r / ps];
+        slot = (int)(r % ps);
+    } else {
+        const long ring = (start + (r - G)) % W;
+        page = pv.lpt[hidx * pv.n_lp + ring / ps];
+        slot = (int)(ring % ps);
+    }
+    if (page < 0) {  // failed allocation (latched ENOPAGES): report an empty entry
+        if (lane == 0) {
+            gate[r] = 0.f;
+            pos[r] = -1;
+        }
+        return;
+    }
+    const size_t mi = (size_t)page * ps + slot;
+    if (lane == 0) {
+        gate[r] = pv.gate[mi];
+        pos[r] = pv.pos[mi];
+    }
+    if (!k) return;
+    const size_t e0 = (size_t)page * pv.page_elems() + (size_t)slot * d, e1 = e0 + (size_t)ps * d;
+    for (int e = lane; e < d; e += 32) {
+        if (esz == 2) {
+            const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(pv.data);
+            k[r * d + e] = __bfloat162float(p[e0 + e]);
+            v[r * d + e] = __bfloat162float(p[e1 + e]);
+        } else {
+            const float* p = reinterpret_cast<const float*>(pv.data);
+            k[r * d + e] = p[e0 + e];
+            v[r * d + e] = p[e1 + e];
+        }
+    }
 }
 
 }  // namespace
@@ -92,7 +214,7 @@ struct wgkv_ctx {
     int64_t* ws_near = nullptr;
     float* ws_part = nullptr;
     int* ws_nchunks = nullptr;
-    int* ws_slot = nullptr;  // [S*H] new-token ring slot recorded by K4 for the side-stream gate
+    int* ws_tokpos = nullptr;  // [S*H] the new token's position per (seq, kv head) (deferred append)
     float* ws_score = nullptr;  // K6: [S][Hq][n_gp] page scores
     int32_t* ws_sel = nullptr;  // K6: [S][Hq][n_gp] selected logical pages
     int32_t* ws_nsel = nullptr; // K6: [S][Hq]
@@ -101,8 +223,6 @@ struct wgkv_ctx {
     int* ws_ucnt = nullptr;                // K6: [S][H][ceil(n_gp/1024)] union block counts
     __nv_bfloat16* quest_meta = nullptr;   // K6 Quest mode: [capacity][min 128 | max 128]
     int* quest_full = nullptr;             // K6 Quest mode: [L][S][H] pages whose metadata is final
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int max_chunks = kMaxChunks;
     long near_cap = 0;
     // host mirrors for lifecycle checks and grid sizing
@@ -154,20 +274,26 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     if (c.layers < 1 || c.q_heads < 1 || c.kv_heads < 1 || c.q_heads % c.kv_heads != 0)
         return fail(WGKV_EINVAL, "wgkv_ctx_create: bad head/layer geometry");
     if (c.head_dim <= 0 || c.head_dim % 2 != 0) return fail(WGKV_EINVAL, "rope: head_dim must be even");
-    if (c.head_dim % 32 != 0 || c.head_dim > 256) return fail(WGKV_ENOTSUP, "head_dim must be a multiple of 32 <= 256");
+    // any even d <= 256 (the reference's ModelConfig default is 16, model.hpp:15); the
+    // tensor-core kernels take d = 128, everything else runs the SIMT kernels
+    if (c.head_dim > 256) return fail(WGKV_ENOTSUP, "head_dim must be <= 256");
     if (c.window < 1) return fail(WGKV_EINVAL, "HeadCache: window must be >= 1");
     if (!(c.tau > 0.0 && c.tau < 1.0)) return fail(WGKV_EINVAL, "binarize: tau must lie in (0,1)");
     if (c.page_size < 1 || c.page_size > 32) return fail(WGKV_ENOTSUP, "page_size must be in [1, 32]");
     if (c.hidden < 1 || c.max_seqs < 1 || c.max_tokens < 1) return fail(WGKV_EINVAL, "bad sizes");
     if (c.dtype != WGKV_BF16 && c.dtype != WGKV_F32) return fail(WGKV_EINVAL, "bad dtype");
     if (c.topk_mode != WGKV_TOPK_EXACT && c.topk_mode != WGKV_TOPK_QUEST) return fail(WGKV_EINVAL, "bad topk_mode");
+    if (c.decode_chunk_pages < 0) return fail(WGKV_EINVAL, "decode_chunk_pages must be >= 0");
     if (c.topk_mode == WGKV_TOPK_QUEST &&
         (c.dtype != WGKV_BF16 || c.head_dim != 128 || c.page_size != 16 || c.q_heads / c.kv_heads > 8))
         return fail(WGKV_ENOTSUP, "Quest page selection needs bf16, head_dim 128, page 16, GQA group <= 8");
     if ((c.max_tokens + c.page_size - 1) / c.page_size + 1 + (c.window + c.page_size - 1) / c.page_size >
         (long)kMaxChunks * kDecPidCap)
         return fail(WGKV_ENOTSUP, "max_tokens exceeds the decode work split (kMaxChunks * kDecPidCap pages per head)");
-    if (cudaSetDevice(c.device) != cudaSuccess) return fail(WGKV_ECUDA, "cudaSetDevice failed");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || c.device < 0 || c.device >= ndev)
+        return fail(WGKV_EINVAL, "wgkv_ctx_create: no such CUDA device");
+    DevGuard dg_(c.device);
 
     auto* ctx = new wgkv_ctx();
     ctx->cfg = c;
@@ -227,7 +353,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
     // per-pair chunk counts | work-stealing counter | per-pair merge counters
     ctx->ws_nchunks = dalloc<int>(2 * (size_t)S * H + 1, o);
-    ctx->ws_slot = dalloc<int>((size_t)S * H, o);
+    ctx->ws_tokpos = dalloc<int>((size_t)S * H, o);
     if (c.topk_budget > 0) {
         ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
         ctx->ws_sel = dalloc<int32_t>((size_t)S * c.q_heads * n_gp, o);
@@ -255,6 +381,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     cudaMemcpy(pv.free_top, &top, sizeof(top), cudaMemcpyHostToDevice);
     cudaMemcpy(pv.err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
     cudaMemset(pv.state, 0, sizeof(HeadState) * (size_t)L * S * H);
+    cudaMemset(ctx->ws_nchunks, 0, sizeof(int) * (2 * (size_t)S * H + 1));  // K5 work counter starts at 0
     // zeroed pages: K3/K5 may stream stale slots of a partially filled page
     // (masked out), which must at least be finite
     cudaMemset(pv.data, 0, (size_t)cap * 2 * ps * d * ctx->esz);
@@ -265,9 +392,6 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
         delete ctx;
         return fail(WGKV_ECUDA, "wgkv_ctx_create: init failed");
     }
-    cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
     ctx->prefilled.assign((size_t)L * S, 0);
     ctx->tokens.assign((size_t)L * S, 0);
     *out = ctx;
@@ -276,24 +400,23 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
 
 int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     if (!ctx) return WGKV_OK;
-    cudaSetDevice(ctx->cfg.device);
+    DevGuard dg_(ctx->cfg.device);
     cudaDeviceSynchronize();
     for (void* p : ctx->owned) cudaFree(p);
-    if (ctx->side) cudaStreamDestroy(ctx->side);
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     delete ctx;
     return WGKV_OK;
 }
 
 int wgkv_set_stream(wgkv_ctx* ctx, void* stream) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     ctx->stream = static_cast<cudaStream_t>(stream);
     return WGKV_OK;
 }
 
 int wgkv_sync(wgkv_ctx* ctx) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     int32_t err = 0;
     WGKV_CUDA_TRY(cudaMemcpy(&err, ctx->pv.err, sizeof(err), cudaMemcpyDeviceToHost));
@@ -309,6 +432,7 @@ int wgkv_sync(wgkv_ctx* ctx) {
 
 int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_heads) {
     if (!ctx || !bank) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     const auto& c = ctx->cfg;
     if (bank_layers != c.layers || bank_heads < c.kv_head_offset + c.kv_heads)
         return fail(WGKV_EINVAL, "Session: gate bank shape does not match model");
@@ -383,6 +507,7 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
 // GateBank::load (gating.cpp:107-147): "WGKV", u32 version/L/H/head_dim/hidden, f64 blocks
 int wgkv_gate_load(wgkv_ctx* ctx, const char* path) {
     if (!ctx || !path) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     std::ifstream is(path, std::ios::binary);
     if (!is) return fail(WGKV_ERUNTIME, std::string("GateBank::load: cannot open ") + path);
     char magic[4];
@@ -414,6 +539,7 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
                     void* k_post_out, float* g_out, uint8_t* bits_out, int64_t* near_idx, int near_cap,
                     int* near_count) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     int st = check_slots(ctx, layer, 0, nseq, T);
     if (st) return st;
     if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
@@ -448,6 +574,7 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
 int wgkv_admit_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* k_post, const void* v,
                        const float* g, const uint8_t* bits) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     int st = check_slots(ctx, layer, seq0, nseq, T);
     if (st) return st;
     if (T < 1) return fail(WGKV_EINVAL, "Session::prefill: empty prompt");
@@ -476,6 +603,7 @@ int wgkv_admit_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, con
 int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* q, const void* k_post,
                     const void* v, const uint8_t* bits, void* out) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     int st = check_slots(ctx, layer, seq0, nseq, T);
     if (st) return st;
     VsArgs a{};
@@ -508,6 +636,7 @@ int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const 
 int wgkv_prefill_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* q, const void* k_pre,
                        const void* v, const float* forced_g, void* out, float* g_out, uint8_t* bits_out) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     int st = check_slots(ctx, layer, seq0, nseq, T);
     if (st) return st;
     if (T < 1) return fail(WGKV_EINVAL, "Session::prefill: empty prompt");
@@ -534,9 +663,9 @@ static int decode_check(wgkv_ctx* ctx, int layer, int seq0, int nseq) {
 }
 
 static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
-                              const float* forced_g, float* g_out, int32_t* events_out, int* work_counter,
-                              bool split_gate) {
+                              const float* forced_g, const DecodeTrace& tr) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s)
@@ -546,13 +675,11 @@ static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, cons
     GateArgs ga = ctx->gate_args(layer, 1, 0);
     if (ctx->cfg.dtype == WGKV_BF16)
         st = launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
-                                                 (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g,
-                                                 g_out, events_out, work_counter, ctx->ws_slot, ctx->stream,
-                                                 split_gate ? ctx->side : nullptr, ctx->ev_fork, ctx->ev_join);
+                                                 (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g, tr,
+                                                 ctx->stream);
     else
         st = launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
-                                         (const float*)v, forced_g, g_out, events_out, work_counter, ctx->ws_slot,
-                                         ctx->stream, split_gate ? ctx->side : nullptr, ctx->ev_fork, ctx->ev_join);
+                                         (const float*)v, forced_g, tr, ctx->stream);
     if (st) return fail(st, "decode append kernel failed");
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
     return WGKV_OK;
@@ -563,8 +690,19 @@ static bool fast_decode(const wgkv_config& c) {
            c.attn_impl != WGKV_ATTN_SIMT;
 }
 
-static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out, bool fused) {
+// the deferred append (decode_finish.cu): bf16 fast path without top-k
+static bool defer_append(const wgkv_config& c) {
+    static const bool off = getenv("WGKV_DECODE_NODEFER") != nullptr;  // A/B switch
+    return !off && fast_decode(c) && c.topk_budget == 0;
+}
+
+// fin != null: deferred append -- K5 over the pre-append cache, then the
+// finish kernel (merge + the new token + K4); the K5 counter was left at 0 by
+// the previous merge kernel
+static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out,
+                            const FinishArgs* fin) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
     const auto& c = ctx->cfg;
@@ -573,9 +711,10 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
     // upper bound of resident pages per head: Global <= tokens - W entries
     const long gmax = tmax > c.window ? tmax - c.window : 0;
     const long np = (gmax + c.page_size - 1) / c.page_size + (c.window + c.page_size - 1) / c.page_size;
-    const long target = (long)kNumSMs * 4;
+    const long target = (long)num_sms() * 4;
     long cp = (np * nseq * c.kv_heads + target - 1) / target;
     cp = std::max(cp, 4L);
+    if (c.decode_chunk_pages > 0) cp = c.decode_chunk_pages;  // pinned split (SIMT path; K5 pins on device)
     cp = std::max(cp, (np + ctx->max_chunks - 1) / ctx->max_chunks);
     DecArgs a{};
     a.pv = ctx->pv;
@@ -588,6 +727,8 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
     a.freq = ctx->freq;
     a.n_pairs = nseq * c.kv_heads;
     a.nchunks = nullptr;
+    a.window = c.window;
+    a.pin_cp = (int)std::min<long>(c.decode_chunk_pages, kDecPidCap);
     if (c.topk_budget > 0) {  // wgkv_plus_topk (engine.cpp:320-324)
         if (c.dtype == WGKV_BF16)
             st = launch_topk_decode<__nv_bfloat16>(a, nseq, c.topk_budget, (const __nv_bfloat16*)q, ctx->ws_score,
@@ -602,47 +743,76 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
         if (st) return fail(st, std::string("topk decode: ") + cudaGetErrorString(cudaGetLastError()));
         return WGKV_OK;
     }
-    if (fast_decode(c))
+    if (fin) {
+        a.defer = 1;
+        a.tokpos = ctx->ws_tokpos;
         st = launch_decode_attn_mma(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part, ctx->ws_nchunks,
-                                    (__nv_bfloat16*)out, ctx->stream, fused);
-    else if (c.dtype == WGKV_BF16)
+                                    (__nv_bfloat16*)out, ctx->stream, true, fin);
+    } else if (fast_decode(c)) {
+        st = launch_decode_attn_mma(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part, ctx->ws_nchunks,
+                                    (__nv_bfloat16*)out, ctx->stream, false);
+    } else if (c.dtype == WGKV_BF16) {
         st = launch_decode_attn_simt<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)q, ctx->ws_part,
                                                     (__nv_bfloat16*)out, ctx->stream);
-    else
+    } else {
         st = launch_decode_attn_simt<float>(a, nseq, (const float*)q, ctx->ws_part, (float*)out, ctx->stream);
+    }
     if (st) return fail(st, std::string("decode attention: ") + cudaGetErrorString(cudaGetLastError()));
     return WGKV_OK;
 }
 
 int wgkv_decode_step_kv(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
                         const float* forced_g, float* g_out, int32_t* events_out) {
-    return decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, nullptr, false);
+    return decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g,
+                              DecodeTrace{g_out, nullptr, nullptr, events_out});
 }
 
 int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, void* out) {
-    return decode_attn_impl(ctx, layer, seq0, nseq, q, out, false);
+    return decode_attn_impl(ctx, layer, seq0, nseq, q, out, nullptr);
 }
 
-// K4 -> K5 -> combine chained with programmatic dependent launch: K4 publishes
-// the ring write and triggers, then computes the new token's gate while K5
-// streams the cache (the gate is only read W steps later, at promotion time).
+// One decode layer.  bf16 fast path: K5 streams the cache as it was before
+// this step's append and needs nothing in front of it; the finish kernel
+// merges K5's chunks with the new token and runs the append (K4, exact fp64
+// gate) beside the merge.  Other configurations: K4, then K5 / SIMT.
+int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, const void* k_pre,
+                             const void* v, const float* forced_g, void* out, const wgkv_decode_trace* trace) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
+    DecodeTrace tr{};
+    if (trace) tr = DecodeTrace{trace->g, trace->bits, trace->near_tau, trace->events};
+    if (!defer_append(ctx->cfg)) {
+        int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, tr);
+        if (st) return st;
+        return decode_attn_impl(ctx, layer, seq0, nseq, q, out, nullptr);
+    }
+    int st = decode_check(ctx, layer, seq0, nseq);
+    if (st) return st;
+    for (int s = seq0; s < seq0 + nseq; ++s)
+        if (ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] >= ctx->cfg.max_tokens)
+            return fail(WGKV_EINVAL, "sequence exceeds max_tokens");
+    if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
+    FinishArgs fin{};
+    fin.ga = ctx->gate_args(layer, 1, 0);
+    fin.k_new = (const __nv_bfloat16*)k_pre;
+    fin.v_new = (const __nv_bfloat16*)v;
+    fin.forced_g = forced_g;
+    fin.tr = tr;
+    st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, &fin);
+    if (st) return st;
+    for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
+    return WGKV_OK;
+}
+
 int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q, const void* k_pre, const void* v,
                       const float* forced_g, void* out, float* g_out, int32_t* events_out) {
-    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
-    const bool fused = fast_decode(ctx->cfg) && ctx->cfg.topk_budget == 0;
-    int* counter = fused ? ctx->ws_nchunks + (size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads : nullptr;
-    // the new token's gate forks onto the side stream and runs alongside K5
-    static const bool inline_gate = getenv("WGKV_DECODE_GATE_INLINE") != nullptr;  // A/B switch
-    const bool split = !forced_g && !inline_gate;
-    int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, g_out, events_out, counter, split);
-    if (st) return st;
-    st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, fused);
-    if (split) cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);  // join (capture-safe)
-    return st;
+    const wgkv_decode_trace tr{g_out, nullptr, nullptr, events_out};
+    return wgkv_decode_layer_traced(ctx, layer, seq0, nseq, q, k_pre, v, forced_g, out, &tr);
 }
 
 int wgkv_cache_state(wgkv_ctx* ctx, int layer, int seq, int kv_head, int64_t* lens) {
     if (!ctx || !lens) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     const auto& c = ctx->cfg;
     if (layer < 0 || layer >= c.layers || seq < 0 || seq >= c.max_seqs || kv_head < 0 || kv_head >= c.kv_heads)
         return fail(WGKV_EINVAL, "index out of range");
@@ -660,73 +830,51 @@ int wgkv_cache_state(wgkv_ctx* ctx, int layer, int seq, int kv_head, int64_t* le
     return WGKV_OK;
 }
 
-static float elem_to_f(const uint8_t* p, size_t esz) {
-    if (esz == 4) {
-        float f;
-        std::memcpy(&f, p, 4);
-        return f;
-    }
-    uint16_t h;
-    std::memcpy(&h, p, 2);
-    const uint32_t u = (uint32_t)h << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
-}
-
 int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk, float* gv, int64_t* gpos,
                       float* ggate, float* lk, float* lv, int64_t* lpos, float* lgate) {
     int64_t lens[6];
     int st = wgkv_cache_state(ctx, layer, seq, kv_head, lens);
     if (st) return st;
+    DevGuard dg_(ctx->cfg.device);
     const auto& c = ctx->cfg;
-    const int ps = c.page_size, d = c.head_dim;
+    const int d = c.head_dim;
+    const long G = lens[2], Lc = lens[0], rows = G + Lc;
+    if (rows == 0) return WGKV_OK;
+    // one device gather (position order, kvstore.cpp:205-241) into a scratch
+    // buffer, then one copy per output: K/V only when asked for
+    const bool kv = gk || gv || lk || lv;
+    const size_t kvn = kv ? (size_t)rows * d : 0;
+    void* scratch = nullptr;
+    const size_t bytes = 2 * kvn * sizeof(float) + (size_t)rows * (sizeof(float) + sizeof(int32_t));
+    WGKV_CUDA_TRY(cudaMalloc(&scratch, bytes));
+    float* dk = kv ? static_cast<float*>(scratch) : nullptr;
+    float* dv = kv ? dk + kvn : nullptr;
+    float* dg = static_cast<float*>(scratch) + 2 * kvn;
+    int32_t* dp = reinterpret_cast<int32_t*>(dg + rows);
     const long hidx = ctx->pv.head_index(layer, seq, kv_head);
-    std::vector<int32_t> lpt(ctx->pv.n_lp), gpt(ctx->pv.n_gp);
-    WGKV_CUDA_TRY(cudaMemcpy(lpt.data(), ctx->pv.lpt + hidx * ctx->pv.n_lp, sizeof(int32_t) * lpt.size(),
-                             cudaMemcpyDeviceToHost));
-    WGKV_CUDA_TRY(cudaMemcpy(gpt.data(), ctx->pv.gpt + hidx * ctx->pv.n_gp, sizeof(int32_t) * gpt.size(),
-                             cudaMemcpyDeviceToHost));
-    const size_t pbytes = (size_t)2 * ps * d * ctx->esz;
-    std::vector<uint8_t> page(pbytes);
-    std::vector<float> pg(ps);
-    std::vector<int32_t> pp(ps);
-    auto fetch = [&](int p) -> int {
-        WGKV_CUDA_TRY(cudaMemcpy(page.data(), (uint8_t*)ctx->pv.data + (size_t)p * pbytes, pbytes,
-                                 cudaMemcpyDeviceToHost));
-        WGKV_CUDA_TRY(cudaMemcpy(pg.data(), ctx->pv.gate + (size_t)p * ps, sizeof(float) * ps, cudaMemcpyDeviceToHost));
-        WGKV_CUDA_TRY(cudaMemcpy(pp.data(), ctx->pv.pos + (size_t)p * ps, sizeof(int32_t) * ps, cudaMemcpyDeviceToHost));
-        return WGKV_OK;
+    const long start = Lc < c.window ? 0 : lens[1];  // ring unrolled oldest-first from local_ptr when full
+    export_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, ctx->stream>>>(ctx->pv, hidx, c.window, (int)G,
+                                                                             (int)Lc, (int)start, (int)ctx->esz, dk,
+                                                                             dv, dg, dp);
+    cudaError_t e = cudaGetLastError();
+    std::vector<int32_t> pos(rows);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    auto cp = [&](void* dst, const void* src, size_t n) {
+        if (dst && n && e == cudaSuccess) e = cudaMemcpy(dst, src, n, cudaMemcpyDeviceToHost);
     };
-    auto emit = [&](int slot, long row, float* k, float* v, int64_t* pos, float* gate) {
-        for (int e = 0; e < d; ++e) {
-            if (k) k[row * d + e] = elem_to_f(page.data() + ((size_t)slot * d + e) * ctx->esz, ctx->esz);
-            if (v) v[row * d + e] = elem_to_f(page.data() + ((size_t)(ps + slot) * d + e) * ctx->esz, ctx->esz);
-        }
-        if (pos) pos[row] = pp[slot];
-        if (gate) gate[row] = pg[slot];
-    };
-    int cur = -1;
-    for (long g = 0; g < lens[2]; ++g) {
-        const int p = gpt[g / ps];
-        if (p != cur) {
-            if ((st = fetch(p))) return st;
-            cur = p;
-        }
-        emit((int)(g % ps), g, gk, gv, gpos, ggate);
-    }
-    // unroll the ring oldest-first from local_ptr when full (kvstore.cpp:229-239)
-    const long W = c.window, Lc = lens[0], start = Lc < W ? 0 : lens[1];
-    cur = -1;
-    for (long n = 0; n < Lc; ++n) {
-        const long ring = (start + n) % W;
-        const int p = lpt[ring / ps];
-        if (p != cur) {
-            if ((st = fetch(p))) return st;
-            cur = p;
-        }
-        emit((int)(ring % ps), n, lk, lv, lpos, lgate);
-    }
+    cp(gk, dk, sizeof(float) * G * d);
+    cp(gv, dv, sizeof(float) * G * d);
+    cp(lk, dk ? dk + G * d : nullptr, sizeof(float) * Lc * d);
+    cp(lv, dv ? dv + G * d : nullptr, sizeof(float) * Lc * d);
+    cp(ggate, dg, sizeof(float) * G);
+    cp(lgate, dg + G, sizeof(float) * Lc);
+    cp(pos.data(), dp, sizeof(int32_t) * rows);
+    cudaFree(scratch);
+    WGKV_CUDA_TRY(e);
+    for (long r = 0; r < G; ++r)
+        if (gpos) gpos[r] = pos[r];
+    for (long r = 0; r < Lc; ++r)
+        if (lpos) lpos[r] = pos[G + r];
     return WGKV_OK;
 }
 
@@ -736,6 +884,7 @@ int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk,
 // keeps gates in fp32, so the digits are those of the fp32 value).
 int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* len) {
     if (!ctx || !len) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     const auto& c = ctx->cfg;
     if (seq < 0 || seq >= c.max_seqs) return fail(WGKV_EINVAL, "seq out of range");
     std::string text;
@@ -752,11 +901,11 @@ int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* l
                                    lpos.data(), lg.data());
             if (st) return st;
             for (size_t i = 0; i < G; ++i) {
-                std::snprintf(line, sizeof(line), "%d %d global %ld %.17g\n", l, h, (long)gpos[i], (double)gg[i]);
+                std::snprintf(line, sizeof(line), "%d %d global %ld %.17g\n", l, c.kv_head_offset + h, (long)gpos[i], (double)gg[i]);
                 text += line;
             }
             for (size_t i = 0; i < Lc; ++i) {
-                std::snprintf(line, sizeof(line), "%d %d local %ld %.17g\n", l, h, (long)lpos[i], (double)lg[i]);
+                std::snprintf(line, sizeof(line), "%d %d local %ld %.17g\n", l, c.kv_head_offset + h, (long)lpos[i], (double)lg[i]);
                 text += line;
             }
         }
@@ -771,7 +920,9 @@ int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* l
 
 int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     const auto& c = ctx->cfg;
+    if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     std::vector<HeadState> st((size_t)c.layers * c.max_seqs * c.kv_heads);
     WGKV_CUDA_TRY(cudaMemcpy(st.data(), ctx->pv.state, sizeof(HeadState) * st.size(), cudaMemcpyDeviceToHost));
@@ -794,6 +945,7 @@ int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out) {
 
 int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
     const auto& c = ctx->cfg;
     if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
     release_kernel<<<c.layers * nseq * c.kv_heads, 256, 0, ctx->stream>>>(ctx->pv, c.layers, seq0, nseq);
@@ -812,6 +964,7 @@ int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq) {
 
 int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     int32_t top = 0;
     WGKV_CUDA_TRY(cudaMemcpy(&top, ctx->pv.free_top, sizeof(top), cudaMemcpyDeviceToHost));
@@ -824,6 +977,7 @@ int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out) {
 // wgkv_gate_score listed for the fp64 recheck, out[1] = reported near-tau tokens
 extern "C" int wgkv_dbg_gate_counts(wgkv_ctx* ctx, int* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     std::vector<int> pc((size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads);
     WGKV_CUDA_TRY(cudaMemcpy(pc.data(), ctx->ws_pcnt, sizeof(int) * pc.size(), cudaMemcpyDeviceToHost));

@@ -1,6 +1,8 @@
 // attn.cuh -- K3 / K5 argument blocks and launchers.
 #pragma once
+#include "append.cuh"
 #include "common.cuh"
+#include "gate.cuh"
 
 namespace wgkv {
 
@@ -33,6 +35,15 @@ struct DecArgs {
     // logical page | q-head mask << 24, and their count; null = all pages
     const int32_t* sel;
     const int32_t* nsel;
+    // deferred append (bf16 fast path): K5 attends the cache as it was BEFORE
+    // this step's append -- Global, the ring minus a dropped victim -- and the
+    // finish kernel adds the new token and runs the append (K4) beside the
+    // chunk merge.  tokpos [nseq*kv_heads] receives the new token's position.
+    int defer;
+    long window;
+    int* tokpos;
+    int* counter;  // K5 work-stealing counter, reset to 0 by the kernel that merges its partials
+    int pin_cp;    // > 0: pages per chunk fixed (wgkv_config.decode_chunk_pages)
 };
 
 // K6: select_topk_pages + per-q-head attention over the selection (topk.cu).
@@ -43,10 +54,25 @@ int launch_topk_decode(const DecArgs& a, int nseq, long budget, const E* q, floa
                        int32_t* nsel, unsigned long long* thr, uint8_t* umask, int* ucnt, float* part, int* nchunks,
                        E* out, int mode, __nv_bfloat16* meta, int* meta_full, cudaStream_t st);
 
-// counter_reset_by_append: K4 ran just before on the stream and zeroed the
-// work counter; K5 is then launched as its programmatic dependent (PDL)
+// the deferred append (a.defer): inputs of the new token and the gate / trace
+// outputs, consumed by the finish kernel (decode_finish.cu)
+struct FinishArgs {
+    GateArgs ga;
+    const __nv_bfloat16* k_new;  // [nseq][kv_heads][d] pre-RoPE
+    const __nv_bfloat16* v_new;  // [nseq][kv_heads][d]
+    const float* forced_g;       // [nseq][kv_heads] or null
+    DecodeTrace tr;
+};
+
+// counter_reset_by_append: the kernel just before on the stream zeroed the work
+// counter; K5 is then launched as its programmatic dependent (PDL).  fin != null
+// (deferred append, a.defer = 1): K5 then the finish kernel (merge + new token
+// + K4) instead of the combine kernel.
 int launch_decode_attn_mma(const DecArgs& a, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
-                           __nv_bfloat16* out, cudaStream_t st, bool counter_reset_by_append);
+                           __nv_bfloat16* out, cudaStream_t st, bool counter_reset_by_append,
+                           const FinishArgs* fin = nullptr);
+int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, const float* part,
+                         __nv_bfloat16* out, const FinishArgs& fin, cudaStream_t st);
 
 template <typename T>
 int launch_vs_prefill_simt(const VsArgs& a, int nseq, const T* q, const T* k_post, const T* v, T* out,

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(128) vs_prefill_simt_kernel(VsArgs a, const E*
 #pragma unroll
         for (int c = 0; c < MAXC; ++c) o[r][c] = 0.f;
     }
-    const int nc = d / 32;
+    const int nc = (d + 31) / 32;  // column blocks of 32 (the last one partial when d % 32 != 0)
 
     const long s_lo = i0 - W + 1 > 0 ? i0 - W + 1 : 0;
     // vertical prefix length (clamped to what K2 stored: 0 after a failed page claim)
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) vs_prefill_simt_kernel(VsArgs a, const E*
                 if (pjj != 0.f) {
 #pragma unroll
                     for (int c = 0; c < MAXC; ++c)
-                        if (c < nc) o[r][c] = fmaf(pjj, Vs[j * d + lane + 32 * c], o[r][c]);
+                        if (c < nc && lane + 32 * c < d) o[r][c] = fmaf(pjj, Vs[j * d + lane + 32 * c], o[r][c]);
                 }
             }
             __syncwarp();
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(128) vs_prefill_simt_kernel(VsArgs a, const E*
         const size_t off = (((size_t)s * T + i) * a.q_heads + p) * d;
 #pragma unroll
         for (int c = 0; c < MAXC; ++c)
-            if (c < nc) out[off + lane + 32 * c] = from_f<E>(o[r][c] * inv);
+            if (c < nc && lane + 32 * c < d) out[off + lane + 32 * c] = from_f<E>(o[r][c] * inv);
     }
 }
 
@@ -176,9 +176,9 @@ template <typename E>
 int launch_vs_prefill_simt(const VsArgs& a, int nseq, const E* q, const E* k_post, const E* v, E* out,
                            cudaStream_t st) {
     const int d = a.pv.head_dim;
-    if (d % 32 != 0 || d > 256) return WGKV_ENOTSUP;
+    if (d % 2 != 0 || d > 256) return WGKV_ENOTSUP;
     const size_t smem = sizeof(float) * ((size_t)VS_QT * d + (size_t)VS_KT * (d + 1) + (size_t)VS_KT * d + 128);
-    cudaFuncSetAttribute(vs_prefill_simt_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ensure_smem(vs_prefill_simt_kernel<E>, smem) != cudaSuccess) return WGKV_ECUDA;
     dim3 grid((unsigned)((a.T + VS_QT - 1) / VS_QT), a.q_heads, nseq);
     vs_prefill_simt_kernel<E><<<grid, 128, smem, st>>>(a, q, k_post, v, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
     }
     __syncthreads();
     const E* pool = reinterpret_cast<const E*>(a.pv.data);
-    const int nc = d / 32;
+    const int nc = (d + 31) / 32;  // column blocks of 32 (the last one partial when d % 32 != 0)
     float m[DC_MAXG], l[DC_MAXG], o[DC_MAXG][8];
 #pragma unroll
     for (int g = 0; g < DC_MAXG; ++g) {
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
                     const float pjj = __shfl_sync(0xffffffffu, pj, jj);
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
-                        if (c < nc) o[g][c] = fmaf(pjj, to_f(vb[(size_t)(j0 + jj) * d + lane + 32 * c]), o[g][c]);
+                        if (c < nc && lane + 32 * c < d) o[g][c] = fmaf(pjj, to_f(vb[(size_t)(j0 + jj) * d + lane + 32 * c]), o[g][c]);
                 }
             }
         }
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
     for (int g = 0; g < gs && g < DC_MAXG; ++g) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-            if (c < nc) rw[g * (d + 2) + lane + 32 * c] = o[g][c];
+            if (c < nc && lane + 32 * c < d) rw[g * (d + 2) + lane + 32 * c] = o[g][c];
         if (lane == 0) {
             rw[g * (d + 2) + d] = m[g];
             rw[g * (d + 2) + d + 1] = l[g];
@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecArgs a, const fl
     __shared__ float wm[NW], wl[NW];
     __shared__ float wacc[NW][256];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // partials of the attention kernel (PDL)
+    if (blockIdx.x == 0 && tid == 0 && a.counter) *a.counter = 0;  // K5's work counter, for the next launch
     const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, kMaxChunks);
     float m = -INFINITY, l = 0.f;
     float2 acc[4];  // columns 2*lane + 64*j (d <= 256)
@@ -384,9 +385,9 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecArgs a, const fl
 template <typename E>
 int launch_decode_attn_simt(const DecArgs& a, int nseq, const E* q, float* part, E* out, cudaStream_t st) {
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
-    if (d % 32 != 0 || d > 256 || gs > DC_MAXG) return WGKV_ENOTSUP;
+    if (d % 2 != 0 || d > 256 || gs > DC_MAXG) return WGKV_ENOTSUP;
     const size_t smem = sizeof(float) * ((size_t)gs * d + (size_t)4 * gs * (d + 2));
-    cudaFuncSetAttribute(decode_attn_simt_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ensure_smem(decode_attn_simt_kernel<E>, smem) != cudaSuccess) return WGKV_ECUDA;
     decode_attn_simt_kernel<E><<<dim3(a.n_chunks, nseq * a.pv.kv_heads), 128, smem, st>>>(a, q, part);
     decode_combine_kernel<E><<<nseq * a.q_heads, 256, 0, st>>>(a, part, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;

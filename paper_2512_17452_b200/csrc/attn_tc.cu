@@ -597,11 +597,7 @@ int launch_vs_prefill_tc(const VsArgs& a, int nseq, const __nv_bfloat16* q, cons
     r |= make_tmap_3d_bf16(&tvr, static_cast<const uint8_t*>(a.pv.data) + plane, 128, ps, (uint64_t)a.pv.capacity,
                            256, 2 * plane, 64, ps, 128 / ps);
     if (r) return WGKV_ECUDA;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(vs_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-        attr = true;
-    }
+    if (ensure_smem(vs_prefill_tc_kernel, SMEM_BYTES) != cudaSuccess) return WGKV_ECUDA;
     dim3 grid((unsigned)((a.T + 127) / 128), Hq / NT, nseq);
     vs_prefill_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tq, tk, tv, tp, tkr, tvr, a, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;

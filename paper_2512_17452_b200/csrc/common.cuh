@@ -11,7 +11,17 @@
 
 namespace wgkv {
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (148 on B200), cached per device; grids are
+// sized from it, never from a constant
+int num_sms();
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device context: set it
+// once per (kernel, device) for the largest size requested so far (host-only,
+// thread-safe; never a stream operation, so graph capture is unaffected)
+cudaError_t ensure_smem_attr(const void* func, size_t smem);
+template <typename F>
+inline cudaError_t ensure_smem(F* func, size_t smem) {
+    return ensure_smem_attr(reinterpret_cast<const void*>(func), smem);
+}
 
 // ---------------------------------------------------------------------------
 // element conversion
@@ -60,13 +70,38 @@ struct PoolView {
 // Pops one page from the device free stack; -1 (and the error latch) when
 // exhausted (KvPool::alloc_page "out of pages", kvstore.cpp:23-31).
 __device__ __forceinline__ int pool_pop(const PoolView& pv) {
-    int top = atomicSub(pv.free_top, 1);
-    if (top <= 0) {
-        atomicAdd(pv.free_top, 1);
+    // CAS loop: the counter only ever moves down by a claim that succeeds, so a
+    // failing pop never makes a concurrent claim fail spuriously
+    int top = *reinterpret_cast<volatile int32_t*>(pv.free_top);
+    for (;;) {
+        if (top <= 0) {
+            atomicExch(pv.err, WGKV_ENOPAGES);
+            return -1;
+        }
+        const int seen = atomicCAS(pv.free_top, top, top - 1);
+        if (seen == top) break;
+        top = seen;
+    }
+    const int page = pv.free_stack[top - 1];
+    if (page < 0) {  // a corrupted stack entry is an allocation failure, never a page
         atomicExch(pv.err, WGKV_ENOPAGES);
         return -1;
     }
-    return pv.free_stack[top - 1];
+    return page;
+}
+// claims n pages at once (LIFO order: page i = free_stack[base - 1 - i]);
+// returns base (the old top) or -1 with the error latched
+__device__ __forceinline__ int pool_claim(const PoolView& pv, int n) {
+    int top = *reinterpret_cast<volatile int32_t*>(pv.free_top);
+    for (;;) {
+        if (top < n) {
+            atomicExch(pv.err, WGKV_ENOPAGES);
+            return -1;
+        }
+        const int seen = atomicCAS(pv.free_top, top, top - n);
+        if (seen == top) return top;
+        top = seen;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -90,6 +125,13 @@ __device__ __forceinline__ void rope_cs_fast(const double* __restrict__ freq, in
     double r = fma(-k, 6.28318530717958623199592693708837032, angle);
     r = fma(-k, 2.44929359829470635445213186455000e-16, r);
     __sincosf((float)r, &s, &c);
+}
+
+// one interleaved pair rotated in fp32 with pinned roundings (no contraction),
+// so every site that forms a cached key from k_pre produces the same bits
+__device__ __forceinline__ void rope_pair_f32(float x0, float x1, float c, float s, float& y0, float& y1) {
+    y0 = __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s));
+    y1 = __fadd_rn(__fmul_rn(x0, s), __fmul_rn(x1, c));
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,154 @@
+// decode_finish.cu -- the second kernel of a decode layer with the deferred
+// append (bf16 fast path, DecArgs::defer).
+//
+// Session::decode_step (engine.cpp:291-327) appends the new token
+// (HeadCache::local_write, kvstore.cpp:135-158) and then attends Global ||
+// Local (attn_ragged, attention.cpp:155-180).  On B200 the attention kernel
+// (K5, decode_mma.cu) instead streams the cache as it was BEFORE the append --
+// every Global page, the ring minus a dropped victim -- so nothing sits in
+// front of it; this kernel then, in one launch:
+//   * combine CTAs, one per (seq, q head): merge K5's chunk partials and the
+//     new token itself (its logit from the RoPE'd q and k, value v), which is
+//     exactly the reference's attended set after local_write;
+//   * append CTAs, one per (seq, kv head): K4 (append.cuh) -- lazy promotion of
+//     the ring victim, the new token into the ring, its exact fp64 gate --
+//     which may only start once K5 has read the victim slot, i.e. now.
+// Both roles run concurrently, so K4 costs no extra step on the layer's path.
+#include "attn.cuh"
+
+namespace wgkv {
+
+
+__global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a, const __nv_bfloat16* __restrict__ q,
+                                                                       const float* __restrict__ part,
+                                                                       __nv_bfloat16* __restrict__ out, FinishArgs fin,
+                                                                       int ncomb) {
+    extern __shared__ __align__(16) uint8_t fsm[];
+    // the next kernel on the stream may launch now; it waits for our completion
+    asm volatile("griddepcontrol.launch_dependents;");
+    // K5 has finished: partials written, the ring's victim slots read
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int tid = threadIdx.x;
+    if ((int)blockIdx.x >= ncomb) {  // ---- append role: K4 for one (seq, kv head)
+        const int r = blockIdx.x - ncomb;
+        append_token<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, r / a.pv.kv_heads, r % a.pv.kv_heads, a.window,
+                                    fin.k_new, fin.v_new, fin.forced_g, fin.tr, fsm);
+        return;
+    }
+    // ---- combine role: one (seq, q head) --------------------------------------
+    constexpr int NW = kAppendThreads / 32;
+    constexpr int d = 128;
+    const int gs = a.q_heads / a.pv.kv_heads;
+    const int sp = blockIdx.x, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
+    const int bh = s * a.pv.kv_heads + h;
+    const int lane = tid & 31, warp = tid >> 5;
+    const size_t pstride = (size_t)gs * (d + 2);
+    const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
+    float* wm = reinterpret_cast<float*>(fsm);  // [NW]
+    float* wl = wm + NW;                         // [NW]
+    float* wacc = wl + NW;                       // [NW][d]
+    if (blockIdx.x == 0 && tid == 0) *a.counter = 0;  // K5's work counter, for the next launch
+    const int nch = min(a.nchunks[bh], kMaxChunks);
+    float m = -INFINITY, l = 0.f;
+    float2 acc[2];  // columns 2*lane + 64*j
+    acc[0] = acc[1] = make_float2(0.f, 0.f);
+    auto merge = [&](float mc, float lc, const float2 (&x)[2]) {
+        const float mn = fmaxf(m, mc);
+        const float sa = m == -INFINITY ? 0.f : __expf(m - mn), sb = __expf(mc - mn);
+        l = l * sa + lc * sb;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            acc[j].x = acc[j].x * sa + x[j].x * sb;
+            acc[j].y = acc[j].y * sa + x[j].y * sb;
+        }
+        m = mn;
+    };
+    // each warp merges every NW-th chunk online; the row, m and l of a chunk
+    // are loaded together (one round of L2 reads per warp)
+#pragma unroll 4
+    for (int c = warp; c < nch; c += NW) {
+        const float* rr = base + (size_t)c * pstride;
+        const float mc = rr[d], lc = rr[d + 1];
+        float2 x[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) x[j] = *reinterpret_cast<const float2*>(rr + 2 * lane + 64 * j);
+        if (mc == -INFINITY) continue;  // empty chunk (uniform across the warp)
+        merge(mc, lc, x);
+    }
+    if (warp == NW - 1) {
+        // the new token at its position: logit = RoPE(q) . bf16(RoPE(k)) / sqrt(d)
+        // (the key as it will be cached), weight on v
+        const long pos = a.tokpos[bh];
+        const size_t qo = ((size_t)s * a.q_heads + p) * d, ko = ((size_t)s * a.pv.kv_heads + h) * d;
+        float dotp = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int i = lane + 32 * j;  // pair index (d / 2 = 64 pairs)
+            float c, sn;
+            rope_cs(a.freq, i, pos, c, sn);
+            float q0, q1, k0, k1;
+            rope_pair_f32(__bfloat162float(q[qo + 2 * i]), __bfloat162float(q[qo + 2 * i + 1]), c, sn, q0, q1);
+            rope_pair_f32(__bfloat162float(fin.k_new[ko + 2 * i]), __bfloat162float(fin.k_new[ko + 2 * i + 1]), c, sn,
+                      k0, k1);
+            k0 = __bfloat162float(__float2bfloat16_rn(k0));
+            k1 = __bfloat162float(__float2bfloat16_rn(k1));
+            dotp = fmaf(q0, k0, fmaf(q1, k1, dotp));
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) dotp += __shfl_xor_sync(0xffffffffu, dotp, o);
+        float2 x[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const __nv_bfloat162 vv = *reinterpret_cast<const __nv_bfloat162*>(fin.v_new + ko + 2 * lane + 64 * j);
+            x[j] = __bfloat1622float2(vv);
+        }
+        merge(dotp * rsqrtf((float)d), 1.f, x);
+    }
+    if (lane == 0) {
+        wm[warp] = m;
+        wl[warp] = l;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        wacc[warp * d + 2 * lane + 64 * j] = acc[j].x;
+        wacc[warp * d + 2 * lane + 64 * j + 1] = acc[j].y;
+    }
+    __syncthreads();
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wm[w]);
+    for (int e = tid; e < d; e += blockDim.x) {
+        float t = 0.f, L = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float f = wm[w] == -INFINITY ? 0.f : __expf(wm[w] - M);
+            t += f * wacc[w * d + e];
+            L += f * wl[w];
+        }
+        out[((size_t)s * a.q_heads + p) * d + e] = __float2bfloat16_rn(t / L);
+    }
+}
+
+int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, const float* part, __nv_bfloat16* out,
+                         const FinishArgs& fin, cudaStream_t st) {
+    if (a.pv.head_dim != 128 || !a.tokpos || !a.counter || !a.nchunks) return WGKV_ENOTSUP;
+    const int ncomb = nseq * a.q_heads, napp = nseq * a.pv.kv_heads;
+    const size_t smem = std::max(append_smem_bytes(a.pv.head_dim, fin.ga.hidden),
+                                 sizeof(float) * (2 * (kAppendThreads / 32) + (kAppendThreads / 32) * 128));
+    if (ensure_smem(decode_finish_kernel, smem) != cudaSuccess) return WGKV_ECUDA;
+    // programmatic dependent of K5: the launch overlaps K5's tail
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncomb + napp);
+    cfg.blockDim = dim3(kAppendThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, decode_finish_kernel, a, q, part, out, fin, ncomb);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+}  // namespace wgkv

@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     const int gs = a.q_heads / a.pv.kv_heads;
     const int npairs = a.n_pairs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // launched as a programmatic dependent of K4: wait for its trigger (pages,
-    // tables and ring state of this step are then visible)
+    // launched as a programmatic dependent of the previous kernel (K4, or the
+    // previous layer's finish kernel): wait for it (pages, tables, ring state)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     uint8_t* ring = sm;                                                                    // [DW][DNS][8 KB]
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm + DW * DNS * PAGE_B);          // [16][QROW]
@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
             const int np = ngv + (st.local_len + ps - 1) / ps;
             item_base[p] = np;
+            if (!TOPK && a.defer && blockIdx.x == 0) a.tokpos[p] = st.tokens_seen;  // the new token (finish kernel)
             tot += np;
             npmax = max(npmax, np);
         }
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         // combine merges every chunk) while keeping >= grid/2 items in flight
         cp = max(cp, (int)min((long)(npmax + WGKV_K5_CAPCH - 1) / WGKV_K5_CAPCH, (2 * total + gridDim.x - 1) / gridDim.x));
 #endif
+        if (a.pin_cp > 0) cp = a.pin_cp;  // pinned split: per-head arithmetic independent of the launch
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
         cp = min(cp, PID_CAP);  // host guarantees npmax <= max_chunks * PID_CAP
         // pass 2: chunks per pair, exclusive scan into item_base
@@ -210,7 +212,9 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         const int s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
         const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
         const HeadState st = a.pv.state[hidx];
-        const long pos = st.tokens_seen - 1;
+        // the query's position: after the append (K4 ran first) or, deferred, the
+        // token about to be appended
+        const long pos = (!TOPK && a.defer) ? st.tokens_seen : st.tokens_seen - 1;
         const int ngp = (st.global_len + ps - 1) / ps;
         const int ng = TOPK ? a.nsel[bh] : ngp;  // virtual Global pages
         const int NP = ng + (st.local_len + ps - 1) / ps;
@@ -218,6 +222,21 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         const int32_t* usel = TOPK ? a.sel + (size_t)bh * a.pv.n_gp : nullptr;
         const bool last_sel = TOPK && ng > 0 && (usel[ng - 1] & 0xFFFFFF) == ngp - 1;
         const int vp0 = chunk * cp, vp1 = min(NP, vp0 + cp);
+        // deferred append: a full ring's victim (slot local_ptr, position pos - W)
+        // stays attended only when admitted (it is being promoted); a dropped
+        // victim is masked -- the attended set equals the reference's after
+        // local_write (kvstore.cpp:135-158, engine.cpp:308-326)
+        int vm_vp = -1, vm_slot = 0;
+        if (!TOPK && a.defer && st.local_len >= a.window) {
+            const int vvp = ng + st.local_ptr / ps;
+            if (vvp >= vp0 && vvp < vp1) {
+                const int lpg = a.pv.lpt[hidx * a.pv.n_lp + st.local_ptr / ps];
+                if (lpg >= 0 && !a.pv.adm[(size_t)lpg * ps + st.local_ptr % ps]) {
+                    vm_vp = vvp;
+                    vm_slot = st.local_ptr % ps;
+                }
+            }
+        }
         const size_t pstride = (size_t)gs * (d + 2);
         float* pout = part + ((size_t)bh * a.max_chunks + chunk) * pstride;
 
@@ -250,7 +269,9 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                                 : min(ps, st.local_len - (vp - ng) * ps);
             else
                 valid = vp < ng ? min(ps, st.global_len - vp * ps) : min(ps, st.local_len - (vp - ng) * ps);
-            return pids[vp - vp0];
+            const int pid = pids[vp - vp0];
+            if (!TOPK && pid < 0) valid = 0;  // failed allocation (latched ENOPAGES): fully masked
+            return pid;
         };
         auto issue = [&](int k) {  // k-th page of this warp (ring slot (kq + k) % DNS)
             int valid;
@@ -326,6 +347,13 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                     for (int e = 0; e < 2; ++e)
                         if (nt * 8 + t0 + e >= valid) sc[nt][e] = -INFINITY;
             }
+            if (!TOPK && vp0 + warp + k * DW == vm_vp) {  // the dropped victim (deferred append)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (nt * 8 + t0 + e == vm_slot) sc[nt][e] = -INFINITY;
+            }
             if (TOPK && !(((uint32_t)pidv >> (24 + (lane >> 2))) & 1u))  // row lane/4 did not select this page
                 sc[0][0] = sc[0][1] = sc[1][0] = sc[1][1] = -INFINITY;
             float mx = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
@@ -333,7 +361,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
             const float mn = fmaxf(m, mx);
             const float alpha = (m == -INFINITY) ? 0.f : ex2f(m - mn);
-            const float mb = (TOPK && mn == -INFINITY) ? 0.f : mn;  // row with nothing selected yet
+            const float mb = mn == -INFINITY ? 0.f : mn;  // row with nothing attended yet (masked pages)
             const float p00 = ex2f(sc[0][0] - mb), p01 = ex2f(sc[0][1] - mb);
             const float p10 = ex2f(sc[1][0] - mb), p11 = ex2f(sc[1][1] - mb);
             float ls = p00 + p01 + p10 + p11;
@@ -404,7 +432,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
 }
 
 int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
-                           __nv_bfloat16* out, cudaStream_t st, bool counter_reset_by_append) {
+                           __nv_bfloat16* out, cudaStream_t st, bool counter_reset_by_append, const FinishArgs* fin) {
     DecArgs a = a0;
     const int gs = a.q_heads / a.pv.kv_heads;
     if (a.pv.head_dim != 128 || a.pv.page_size != 16 || gs > 16) return WGKV_ENOTSUP;
@@ -431,17 +459,15 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     if (smem > (size_t)(228 / CPS - 1) * 1024) return WGKV_ENOTSUP;
     const bool topk = a.sel != nullptr;
     auto kern = topk ? decode_attn_mma_kernel<true> : decode_attn_mma_kernel<false>;
-    static size_t smem_set[2] = {0, 0};  // host-side only; keeps graph capture free of attribute calls
-    if (smem > smem_set[topk]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        smem_set[topk] = smem;
-    }
+    if (ensure_smem(kern, smem) != cudaSuccess) return WGKV_ECUDA;
     // work-stealing counter: one int past the per-(seq, kv head) chunk counts;
-    // zeroed by K4 when it precedes us (PDL), else by a memset here
+    // left at 0 by every kernel that merges K5's partials (combine / finish),
+    // zeroed again by the kernel before us (PDL) or by a memset here
     int* counter = nchunks + (size_t)a.pv.max_seqs * a.pv.kv_heads;
+    a.counter = counter;
     if (!counter_reset_by_append) cudaMemsetAsync(counter, 0, sizeof(int), st);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CPS * kNumSMs);
+    cfg.gridDim = dim3(CPS * num_sms());
     cfg.blockDim = dim3(DW * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -452,6 +478,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     cfg.numAttrs = counter_reset_by_append ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, tp, a, q, part, nchunks, counter);
     a.nchunks = nchunks;
+    if (fin) return launch_decode_finish(a, nseq, q, part, out, *fin, st);
     extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
     return launch_decode_combine_bf16(a, nseq, part, out, st);
 }

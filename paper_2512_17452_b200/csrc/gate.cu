@@ -192,7 +192,7 @@ __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, flo
         __syncwarp();
         feature_fp64_warp(kf, d, a.pos0 + t, a.freq, xs);
         const int blk = a.layer * a.bank_heads + a.head_offset + h;
-        const double g = d == 128 ? gate_fp64_warp<256>(a.gd(), blk, xs, d, terms) : gate_fp64_warp(a.gd(), blk, xs, d, terms);
+        const double g = gate_fp64_warp(a.gd(), blk, xs, d, terms);
         if (lane == 0) {
             g_out[gi] = (float)g;
             bits_out[gi] = g >= a.tau ? 1 : 0;
@@ -210,12 +210,12 @@ __global__ void gate_recheck_kernel(GateArgs a, const T* __restrict__ k_pre, flo
 // listed tokens of one (seq, kv head), so every W1 element fetched serves 64
 // tokens (the per-token warp form re-reads the head's 256 KB fp64 W1 from L2
 // for every token).  X = [k_pre ; RoPE_fp64(k_pre)] for the 64 tokens is built
-// in smem exactly as feature_fp64_warp does; z1 = W1 . x in fp64 (DFMA, k in
-// order); then, per token, the reference's order for the rest: terms
-// w2_h * gelu(z1_h + b1_h), z2 = b2 + sum_h terms (sequential), sigmoid, clamp
-// (gating.cpp:158-171).  Only the dot's rounding differs from the reference
-// (FMA), by O(1e-16) relative: bits can differ only where |g - tau| < 1e-14,
-// inside the reported 1e-6 band.
+// in smem exactly as feature_fp64_warp does; z1 = W1 . x in fp64 with k in
+// ascending order and the product and sum rounded separately (dot,
+// numerics.cpp:94-99, built without FMA contraction); then, per token, the
+// reference's order for the rest: terms w2_h * gelu(z1_h + b1_h),
+// z2 = b2 + sum_h terms (sequential), sigmoid, clamp (gating.cpp:158-171).
+// The fp64 score equals the reference's up to libm ulps (cos/sin/erf/exp).
 // ---------------------------------------------------------------------------
 constexpr int RC_C = 64;   // tokens per work item
 constexpr int RC_KC = 32;  // k chunk of W1 staged per step
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc8[i][j] = fma(wv[j], xv[i], acc8[i][j]);
+                    for (int j = 0; j < 4; ++j) acc8[i][j] = __dadd_rn(acc8[i][j], __dmul_rn(wv[j], xv[i]));
             }
         }
         __syncthreads();  // Wt becomes the terms buffer
@@ -366,28 +366,19 @@ int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, 
     }
     if (!done) {
         const size_t smem = sizeof(float) * ((size_t)2 * a.d * GT_XS + 2 * GT_KC * GT_HID + 2 * GT_TOK);
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(gate_prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr_set = true;
-        }
+        if (ensure_smem(gate_prefill_kernel<T>, smem) != cudaSuccess) return WGKV_ECUDA;
         dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
         gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, pcnt);
     }
     if (a.d == 128 && a.hidden == 128) {
-        static bool rc_attr = false;
-        if (!rc_attr) {
-            cudaFuncSetAttribute(gate_recheck_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)RC_SMEM);
-            rc_attr = true;
-        }
-        gate_recheck_gemm_kernel<T><<<kNumSMs, 256, RC_SMEM, st>>>(a, npairs, k_pre, g, bits, cand, pcnt, near_idx,
+        if (ensure_smem(gate_recheck_gemm_kernel<T>, RC_SMEM) != cudaSuccess) return WGKV_ECUDA;
+        gate_recheck_gemm_kernel<T><<<num_sms(), 256, RC_SMEM, st>>>(a, npairs, k_pre, g, bits, cand, pcnt, near_idx,
                                                                    near_cap, near_cnt);
         return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
     }
     const int nw = 8;
     const size_t rsm = sizeof(double) * nw * (2 * a.d + a.hidden) + sizeof(float) * nw * a.d;
-    gate_recheck_kernel<T><<<dim3(std::max(1, kNumSMs * 4 / npairs), npairs), 32 * nw, rsm, st>>>(
+    gate_recheck_kernel<T><<<dim3(std::max(1, num_sms() * 4 / npairs), npairs), 32 * nw, rsm, st>>>(
         a, k_pre, g, bits, cand, pcnt, near_idx, near_cap, near_cnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
@@ -422,10 +413,10 @@ __global__ void forced_gate_kernel(GateArgs a, int nseq, const T* __restrict__ k
 int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_post, const float* forced, float* g,
                        uint8_t* bits, size_t esz, cudaStream_t st) {
     if (esz == 2)
-        forced_gate_kernel<__nv_bfloat16><<<kNumSMs * 8, 256, 0, st>>>(
+        forced_gate_kernel<__nv_bfloat16><<<num_sms() * 8, 256, 0, st>>>(
             a, nseq, (const __nv_bfloat16*)k_pre, (__nv_bfloat16*)k_post, forced, g, bits);
     else
-        forced_gate_kernel<float><<<kNumSMs * 8, 256, 0, st>>>(a, nseq, (const float*)k_pre, (float*)k_post, forced,
+        forced_gate_kernel<float><<<num_sms() * 8, 256, 0, st>>>(a, nseq, (const float*)k_pre, (float*)k_post, forced,
                                                                g, bits);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }

@@ -65,40 +65,46 @@ __device__ __forceinline__ void feature_fp64_warp(const float* kpre, int d, long
     __syncwarp();
 }
 
-// z2 = b2 + sum_h w2[h] * gelu(W1[h].x + b1[h]) (gating.cpp:158-171) by one
-// warp: lanes own hidden units, each dot is sequential in k; the z2 sum is
-// sequential in h on lane 0.  terms: smem scratch [hidden].
-template <int FD = 0>  // FD = 2d when known at compile time (fully unrolled loads)
+// dot (numerics.cpp:94-99) in the reference's operation order: s = 0, then
+// s += w[k] * x[k] for ascending k with the product and the sum rounded
+// separately (the reference is built without FMA contraction).
+__device__ __forceinline__ double dot_ref(const double* __restrict__ w, const double* __restrict__ x, int n) {
+    double s = 0.0;
+    int k = 0;
+    for (; k + 4 <= n; k += 4) {  // loads of a group issued together; the sum stays sequential
+        const double2 w01 = *reinterpret_cast<const double2*>(w + k);
+        const double2 w23 = *reinterpret_cast<const double2*>(w + k + 2);
+        s = __dadd_rn(s, __dmul_rn(w01.x, x[k]));
+        s = __dadd_rn(s, __dmul_rn(w01.y, x[k + 1]));
+        s = __dadd_rn(s, __dmul_rn(w23.x, x[k + 2]));
+        s = __dadd_rn(s, __dmul_rn(w23.y, x[k + 3]));
+    }
+    for (; k < n; ++k) s = __dadd_rn(s, __dmul_rn(w[k], x[k]));
+    return s;
+}
+
+// sigmoid + the reference clamp to [5e-324, nextafter(1, 0)] (gating.cpp:168-170)
+__device__ __forceinline__ double gate_from_z2(double z2) {
+    const double g = sigmoid_ref(z2);
+    const double lo = 4.9406564584124654e-324, hi = 0.99999999999999988898;
+    return g < lo ? lo : (g > hi ? hi : g);
+}
+
+// gate_forward (gating.cpp:158-171) by one warp, reference operation order
+// throughout: lanes own hidden units h = lane, lane + 32, ...; each z1 is a
+// sequential dot_ref over the feature; terms w2[h] * gelu(z1 + b1[h]) go to
+// smem and lane 0 sums z2 = b2 + terms[0] + terms[1] + ... in order.  So the
+// fp64 result equals the reference's up to the libm ulps of cos/sin (RoPE),
+// erf and exp.  terms: smem scratch [hidden].  W1 rows are 16-byte aligned
+// (2d even).
 __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, const double* xs, int d, double* terms) {
     const int lane = threadIdx.x & 31;
-    const int fd = FD > 0 ? FD : 2 * d, hid = gd.hidden;
+    const int fd = 2 * d, hid = gd.hidden;
     const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
-    // dot products: lanes stride over k (coalesced W1 rows, 4 rows in flight),
-    // shuffle-tree sums; fp64 throughout.  The summation order differs from the
-    // reference's sequential loop by O(1e-16) relative -- bits can differ only
-    // where |g - tau| < 1e-14, inside the reported 1e-6 band.
-    for (int h0 = 0; h0 < hid; h0 += 4) {
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int j = 0; j < fd / 32; ++j) {  // fd % 32 == 0 (d % 32 == 0 is enforced)
-            const int k = lane + 32 * j;
-            const double x = xs[k];
-#pragma unroll
-            for (int g = 0; g < 4; ++g)
-                if (h0 + g < hid) s[g] = fma(w1[(size_t)(h0 + g) * fd + k], x, s[g]);
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-            for (int g = 0; g < 4; ++g) s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
-        if (lane < 4 && h0 + lane < hid) {
-            const double sv = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
-            const int h = h0 + lane;
-            terms[h] = __dmul_rn(w2[h], gelu_ref(__dadd_rn(sv, b1[h])));
-        }
-    }
+    for (int h = lane; h < hid; h += 32)
+        terms[h] = __dmul_rn(w2[h], gelu_ref(__dadd_rn(dot_ref(w1 + (size_t)h * fd, xs, fd), b1[h])));
     __syncwarp();
     double z2 = 0.0;
     if (lane == 0) {
@@ -106,73 +112,28 @@ __device__ __forceinline__ double gate_fp64_warp(const GateDev& gd, int blk, con
         for (int h = 0; h < hid; ++h) z2 = __dadd_rn(z2, terms[h]);
     }
     z2 = __shfl_sync(0xffffffffu, z2, 0);
-    double g = sigmoid_ref(z2);
-    const double lo = 4.9406564584124654e-324, hi = 0.99999999999999988898;  // 5e-324, nextafter(1, 0)
-    g = g < lo ? lo : (g > hi ? hi : g);
-    return g;
+    return gate_from_z2(z2);
 }
-// Block-parallel fp64 gate (decode path, one token per CTA): the 2d-term dot
-// of each hidden unit is split in its k_pre and k_post halves across threads
-// and the z2 sum is a tree.  The summation order differs from the reference's
-// sequential order by O(1e-16) relative, so bits can only differ where
-// |g - tau| < 1e-14 -- far inside the reported 1e-6 band.
-// scratch: smem >= 2*hidden + 32 doubles.  Returns g on every thread.
-template <int FD = 0>  // FD = 2d when known at compile time: the k loop unrolls, every W1 load in flight
-__device__ __forceinline__ double gate_fp64_block(const GateDev& gd, int blk, const double* xs, int d,
-                                                  double* scratch) {
-    const int tid = threadIdx.x, nt = blockDim.x, hid = gd.hidden, lane = tid & 31, nw = nt >> 5;
-    const int fd = FD > 0 ? FD : 2 * d;
+
+// The hidden-unit terms of gate_forward for one token by `nthr` threads
+// starting at thread `t0` of the block (thread t0 + u owns units u, u + nthr,
+// ...): terms[h] = w2[h] * gelu(dot_ref(W1[h], x) + b1[h]).  The caller sums
+// them in order with gate_z2_ref after a barrier.
+__device__ __forceinline__ void gate_terms_ref(const GateDev& gd, int blk, const double* xs, int d, double* terms,
+                                               int t0, int nthr) {
+    const int u0 = (int)threadIdx.x - t0;
+    if (u0 < 0 || u0 >= nthr) return;
+    const int fd = 2 * d, hid = gd.hidden;
     const double* w1 = gd.w1d + (size_t)blk * hid * fd;
     const double* b1 = gd.b1d + (size_t)blk * hid;
     const double* w2 = gd.w2d + (size_t)blk * hid;
-    // four hidden units per warp at a time: coalesced W1 row reads with
-    // 4 x (2d/32) independent loads in flight per lane, shuffle-tree reductions
-    const int G4 = 4;
-    for (int h0 = (tid >> 5) * G4; h0 < hid; h0 += nw * G4) {
-        double s[G4] = {0.0, 0.0, 0.0, 0.0};
-        if constexpr (FD > 0) {
-            double wv[FD / 32][G4];
-#pragma unroll
-            for (int j = 0; j < FD / 32; ++j)
-#pragma unroll
-                for (int g = 0; g < G4; ++g) wv[j][g] = h0 + g < hid ? w1[(size_t)(h0 + g) * fd + lane + 32 * j] : 0.0;
-#pragma unroll
-            for (int j = 0; j < FD / 32; ++j) {
-                const double x = xs[lane + 32 * j];
-#pragma unroll
-                for (int g = 0; g < G4; ++g) s[g] = fma(wv[j][g], x, s[g]);
-            }
-        } else {
-            for (int k = lane; k < fd; k += 32) {
-                const double x = xs[k];
-#pragma unroll
-                for (int g = 0; g < G4; ++g)
-                    if (h0 + g < hid) s[g] = fma(w1[(size_t)(h0 + g) * fd + k], x, s[g]);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-            for (int g = 0; g < G4; ++g) s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
-        if (lane < G4 && h0 + lane < hid) scratch[h0 + lane] = lane == 0 ? s[0] : lane == 1 ? s[1] : lane == 2 ? s[2] : s[3];
-    }
-    __syncthreads();
-    double part = 0.0;
-    for (int h = tid; h < hid; h += nt) {
-        const double z1 = scratch[h] + b1[h];
-        part += w2[h] * gelu_ref(z1);
-    }
-    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    __syncthreads();
-    double* red = scratch + 2 * hid;
-    if ((tid & 31) == 0) red[tid >> 5] = part;
-    __syncthreads();
+    for (int h = u0; h < hid; h += nthr)
+        terms[h] = __dmul_rn(w2[h], gelu_ref(__dadd_rn(dot_ref(w1 + (size_t)h * fd, xs, fd), b1[h])));
+}
+__device__ __forceinline__ double gate_z2_ref(const GateDev& gd, int blk, const double* terms) {
     double z2 = gd.b2d[blk];
-    for (int w = 0; w < (nt >> 5); ++w) z2 += red[w];
-    double g = sigmoid_ref(z2);
-    const double lo = 4.9406564584124654e-324, hi = 0.99999999999999988898;
-    g = g < lo ? lo : (g > hi ? hi : g);
-    return g;
+    for (int h = 0; h < gd.hidden; ++h) z2 = __dadd_rn(z2, terms[h]);
+    return z2;
 }
 
 // effective_gate override (engine.cpp:126-151): RoPE only; g = forced, bit = g >= tau

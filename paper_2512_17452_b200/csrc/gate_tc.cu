@@ -368,19 +368,15 @@ int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv
     if (make_tmap_3d_bf16(&tk, k_pre, 128, (uint64_t)a.kv_heads, (uint64_t)nseq * a.T, 256, (uint64_t)a.kv_heads * 256,
                           64, 1, 128))
         return WGKV_ECUDA;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gate_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
-        attr = true;
-    }
-    rope_table_kernel<<<kNumSMs * 8, 256, 0, st>>>(a.freq, a.pos0, a.T, a.d / 2, rope_ws);
+    if (ensure_smem(gate_tc_kernel, G_SMEM) != cudaSuccess) return WGKV_ECUDA;
+    rope_table_kernel<<<num_sms() * 8, 256, 0, st>>>(a.freq, a.pos0, a.T, a.d / 2, rope_ws);
     GateTcArgs A;
     A.g = a;
     A.nseq = nseq;
     A.tiles_per_pair = (a.T + 127) / 128;
     A.total_tiles = A.tiles_per_pair * nseq * a.kv_heads;
     A.rope = rope_ws;
-    const int grid = (int)std::min<long>(kNumSMs, A.total_tiles);
+    const int grid = (int)std::min<long>(num_sms(), A.total_tiles);
     gate_tc_kernel<<<grid, G_THREADS, G_SMEM, st>>>(tw, tk, A, k_pre, k_post, g, bits, cand, pcnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }

@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(128) topk_attn_kernel(DecArgs a, const E* __re
     }
     __syncthreads();
     const E* pool = reinterpret_cast<const E*>(a.pv.data);
-    const int nc = d / 32;
+    const int nc = (d + 31) / 32;  // column blocks of 32 (the last one partial when d % 32 != 0)
     float m = -INFINITY, l = 0.f, o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int vp = vp0 + warp; vp < vp1; vp += 4) {
         int page, valid;
@@ -747,14 +747,14 @@ __global__ void __launch_bounds__(128) topk_attn_kernel(DecArgs a, const E* __re
                 const float pjj = __shfl_sync(0xffffffffu, pj, jj);
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    if (c < nc) o[c] = fmaf(pjj, to_f(vb[(size_t)(j0 + jj) * d + lane + 32 * c]), o[c]);
+                    if (c < nc && lane + 32 * c < d) o[c] = fmaf(pjj, to_f(vb[(size_t)(j0 + jj) * d + lane + 32 * c]), o[c]);
             }
         }
     }
     float* rw = red + (size_t)warp * (d + 2);
 #pragma unroll
     for (int c = 0; c < 8; ++c)
-        if (c < nc) rw[lane + 32 * c] = o[c];
+        if (c < nc && lane + 32 * c < d) rw[lane + 32 * c] = o[c];
     if (lane == 0) {
         rw[d] = m;
         rw[d + 1] = l;
@@ -831,7 +831,7 @@ int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, flo
                        E* out, int mode, __nv_bfloat16* meta, int* meta_full, cudaStream_t st) {
     DecArgs a = a0;
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
-    if (d % 32 != 0 || d > 256) return WGKV_ENOTSUP;
+    if (d % 2 != 0 || d > 256) return WGKV_ENOTSUP;
     const int max_pages = a.pv.n_gp;
     // bf16 production path: tensor-pipe scoring + union selection streamed by K5
     constexpr bool kBf16 = sizeof(E) == 2;
@@ -854,13 +854,9 @@ int launch_topk_decode(const DecArgs& a0, int nseq, long budget, const E* q, flo
     else
         topk_score_kernel<E><<<dim3((max_pages + TK_PPB - 1) / TK_PPB, nseq * a.pv.kv_heads), 128,
                               sizeof(float) * gs * d, st>>>(a, q, scores);
-    static int cap_set = 0;
     const int cap = std::min(max_pages, TH_STAGE_CAP);
     const size_t th_smem = (size_t)TH_CAND * 8 + (size_t)cap * 4;
-    if (cap > cap_set) {
-        cudaFuncSetAttribute(topk_thresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)th_smem);
-        cap_set = cap;
-    }
+    if (ensure_smem(topk_thresh_kernel, th_smem) != cudaSuccess) return WGKV_ECUDA;
     launch_pdl(topk_thresh_kernel, nseq * a.q_heads, 1024, th_smem, st, a, budget, cap, (const float*)scores, thr);
     if (fast) {
         const int nblk = (max_pages + UB - 1) / UB;

@@ -4,6 +4,9 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the reference's parallel_for reads WGKV_THREADS once (numerics.cpp:119-128):
+# let the reference oracle (oracle/_ref) use every host core
+os.environ.setdefault("WGKV_THREADS", str(os.cpu_count() or 1))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

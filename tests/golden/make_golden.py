@@ -62,8 +62,22 @@ def session_case(ref, name, L, hq, hkv, d, hidden, n, steps, W, tau, base, ps, t
     print(name, "global_len", glen.tolist())
 
 
+def gate_bank_file(ref, name, L, H, d, hidden, seed, w_std, b2):
+    """A ".wgkv" v1 gate bank written by the reference's own GateBank::save
+    (gating.cpp:107-122); wgkv_gate_load must read it (tests/test_gpu_configs.py)."""
+    bank = ref.gate_random_init(L, H, d, hidden, seed, w_std, b2)
+    path = os.path.join(HERE, name + ".wgkv")
+    st = ref.lib.wr_gate_save(path.encode(), L, H, d, hidden, bank.ctypes.data_as(O._dp))
+    assert st == 0, st
+    np.save(os.path.join(HERE, name + "_bank.npy"), bank)
+    print(name, os.path.getsize(path), "bytes")
+
+
 def main():
     ref = O.Ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "gate_bank":
+        gate_bank_file(ref, "gate_bank_d32", L=2, H=2, d=32, hidden=32, seed=4100, w_std=0.5, b2=-2.5)
+        return
     # Llama-shaped head geometry (d=128, hidden=d as config.cpp:175), GQA 4,
     # window shorter than the prompt so Global, Local and promotion all occur.
     session_case(ref, "session_gqa4_d128", L=1, hq=8, hkv=2, d=128, hidden=128, n=160, steps=24, W=48, tau=0.1,
@@ -72,6 +86,7 @@ def main():
                  base=5e5, ps=16, topk=3, w_std=0.1, b2=-2.5, seed=2000)
     session_case(ref, "session_small_l2", L=2, hq=4, hkv=4, d=16, hidden=16, n=48, steps=24, W=8, tau=0.1,
                  base=1e4, ps=16, topk=0, w_std=0.5, b2=-2.5, seed=3000)
+    gate_bank_file(ref, "gate_bank_d32", L=2, H=2, d=32, hidden=32, seed=4100, w_std=0.5, b2=-2.5)
 
 
 if __name__ == "__main__":

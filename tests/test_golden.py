@@ -43,3 +43,12 @@ def test_oracle_reproduces_golden(orc, path):
             assert np.array_equal(e, z["decode_events"][si, l])
     pos = np.concatenate([s.gather(l, h)["global_pos"] for l in range(c["L"]) for h in range(c["hkv"])])
     assert np.array_equal(pos, z["global_pos"])
+
+
+def test_oracle_reads_reference_gate_file(orc):
+    """tests/golden/gate_bank_d32.wgkv was written by the reference's own
+    GateBank::save (gating.cpp:107-122, make_golden.py); the oracle's loader
+    (and, on the GPU, wgkv_gate_load) must read back exactly the bank it saved."""
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    bank = np.load(os.path.join(here, "gate_bank_d32_bank.npy"))
+    assert np.array_equal(orc.gate_load(os.path.join(here, "gate_bank_d32.wgkv")), bank)

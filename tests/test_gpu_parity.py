@@ -19,7 +19,9 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 import oracle as O  # noqa: E402
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "session_*d128.npz")))
+# every reference-generated session: d = 128 (Llama head geometry) and the
+# reference's own default ModelConfig geometry (d = 16, session_small_l2)
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "session_*.npz")))
 TOL = {"bf16": 1e-2, "f32": 1e-5}
 
 
@@ -74,13 +76,13 @@ def test_gate_bits_bit_exact(W, orc, w_std, b2):
 
 
 # ----------------------------------------------------------- golden vectors --
-def _run_golden(W, path, dtype):
+def _run_golden(W, path, dtype, impl):
     z = np.load(path)
     L, hq, hkv, d, hid, n, steps, Wn, ps, topk = (int(x) for x in z["cfg"])
     dt = torch.bfloat16 if dtype == "bf16" else torch.float32
     s = W.Session(L, hq, hkv, d, hid, Wn, tau=float(z["tau"]), rope_base=float(z["base"]), page_size=ps,
                   max_tokens=n + steps, dtype=W.BF16 if dtype == "bf16" else W.F32, gate_bank=z["bank"],
-                  attn_impl=W.ATTN_SIMT, topk_budget=topk)
+                  attn_impl=impl, topk_budget=topk)
     q, k, v = (z[x] for x in ("q", "k", "v"))
     tol = TOL[dtype]
     for l in range(L):
@@ -106,9 +108,12 @@ def _run_golden(W, path, dtype):
 
 
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
-@pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_golden_session(W, path, dtype):
-    _run_golden(W, path, dtype)
+@pytest.mark.parametrize("dtype,impl", [("f32", "simt"), ("bf16", "simt"), ("bf16", "auto")])
+def test_golden_session(W, path, dtype, impl):
+    """The reference's own session vectors through the SIMT kernels and, in
+    bf16, through the default (Blackwell) path: tcgen05 K3 where the geometry
+    allows (d = 128, even GQA group), K5 + the finish kernel for decode."""
+    _run_golden(W, path, dtype, W.ATTN_SIMT if impl == "simt" else W.ATTN_AUTO)
 
 
 # ------------------------------------------------ random sessions vs oracle --
