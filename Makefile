@@ -18,7 +18,7 @@ build/%.o: $(PKG)/csrc/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(PKG)/libwgkv_b200.so: $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -Xcompiler -fPIC
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -Xcompiler -fPIC -ldl
 
 oracle:
 	$(MAKE) -s -C oracle all

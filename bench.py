@@ -122,11 +122,23 @@ def pair_count(bits, window):
 
 
 # ------------------------------------------------------------ reference arm --
-def cpu_reference(cfg, sample_T=8192, steps=1):
-    """Time the reference's own prefill hot path (oracle/_ref) on one layer of
-    one sequence at T = sample_T, all heads, WGKV_THREADS = host cores, and
-    extrapolate phase by phase to the full workload: gate+mask per token,
-    vertical-slash attention per permitted pair, populate per token."""
+def _ref_session(O, ref, cfg, hq, hkv, T, bank):
+    return O.Session(ref, 1, hq, hkv, cfg["d"], cfg["hidden"], cfg["window"], tau=cfg["tau"],
+                     rope_base=cfg["rope_base"], page_size=cfg["page"], gate_bank=bank, max_tokens=T)
+
+
+def cpu_reference(cfg, sample_T=8192, steps=1, decode_steps=3, with_cfg0=True):
+    """The reference's own hot path (oracle/_ref: the unmodified reference
+    sources, fp64, WGKV_THREADS = host cores) on the host:
+      * prefill: one layer of one sequence at T = sample_T, all heads, timed
+        per phase and extrapolated per phase to the workload (gate + mask per
+        token, vertical-slash attention per permitted pair, populate per token);
+      * decode: the reference's decode step (gate_forward + local_write + gather
+        + attn_ragged, engine.cpp:291-327) timed on a cache built at the
+        workload's context length (HeadCache::prefill_populate at admission a),
+        2 of the kv heads, scaled to all heads, layers and sequences;
+      * configs[0] (1 layer, 32 q / 8 kv, 4K prefill + 256 decode steps) timed
+        in full -- measured, not extrapolated."""
     import numpy as np
 
     nthreads = os.cpu_count() or 1
@@ -150,8 +162,7 @@ def cpu_reference(cfg, sample_T=8192, steps=1):
         bank[0, h, -1] = math.log(cfg["tau"] / (1 - cfg["tau"])) - np.quantile(z, 1 - cfg["admit"])
     secs_all, pairs = np.zeros(3), 0
     for _ in range(steps):
-        s = O.Session(ref, 1, hq, hkv, d, hid, W, tau=cfg["tau"], rope_base=cfg["rope_base"], page_size=cfg["page"],
-                      gate_bank=bank, max_tokens=Ts)
+        s = _ref_session(O, ref, cfg, hq, hkv, Ts, bank)
         secs, pairs = s.prefill_layer_timed(0, q, k, v)
         secs_all += secs
         del s
@@ -162,13 +173,59 @@ def cpu_reference(cfg, sample_T=8192, steps=1):
     pairs_full = pairs_full_head * hq * B * L
     t_full = (secs_all[0] / Ts * Tf * B * L + secs_all[1] / pairs * pairs_full + secs_all[2] / Ts * Tf * B * L)
     tok_s = B * Tf / t_full
-    return dict(value=tok_s, unit="tok/s", cores=nthreads, kind="reference",
-                sample=(f"reference Session::prefill hot path (oracle/_ref, fp64) on 1 layer x 1 seq x {hq}q/{hkv}kv "
-                        f"heads at T={Ts} (admit {cfg['admit']}): gate {secs_all[0]:.2f}s, VS attention "
-                        f"{secs_all[1]:.2f}s for {pairs:.3g} pairs ({pairs / secs_all[1]:.3g} pairs/s), populate "
-                        f"{secs_all[2]:.3f}s; extrapolated per phase to {L} layers x {B} x {Tf} tokens "
-                        f"({pairs_full:.3g} pairs) = {t_full:.3g} s"),
-                sample_seconds=float(secs_all.sum()), pairs_per_s=pairs / secs_all[1])
+    out = dict(value=tok_s, unit="tok/s", cores=nthreads, kind="reference",
+               sample=(f"reference Session::prefill hot path (oracle/_ref, fp64) on 1 layer x 1 seq x {hq}q/{hkv}kv "
+                       f"heads at T={Ts} (admit {cfg['admit']}): gate {secs_all[0]:.2f}s, VS attention "
+                       f"{secs_all[1]:.2f}s for {pairs:.3g} pairs ({pairs / secs_all[1]:.3g} pairs/s), populate "
+                       f"{secs_all[2]:.3f}s; extrapolated per phase to {L} layers x {B} x {Tf} tokens "
+                       f"({pairs_full:.3g} pairs) = {t_full:.3g} s"),
+               sample_seconds=float(secs_all.sum()), pairs_per_s=pairs / secs_all[1])
+
+    # ---- decode at the workload's context: 2 kv heads (8 q heads), scaled -----
+    hk2, hq2 = min(2, hkv), min(2, hkv) * (hq // hkv)
+    kk = rng.standard_normal((Tf, hk2, d)).astype(np.float32).astype(np.float64)
+    vv = rng.standard_normal((Tf, hk2, d)).astype(np.float32).astype(np.float64)
+    gates = np.where(rng.random((hk2, Tf)) < a, 0.9, 0.05)
+    s = _ref_session(O, ref, cfg, hq2, hk2, Tf + decode_steps + 1, bank[:, :hk2])
+    s.populate_layer(0, kk, vv, gates)
+    del kk, vv
+    t0 = time.perf_counter()
+    for i in range(decode_steps):
+        s.decode_layer(0, rng.standard_normal((hq2, d)), rng.standard_normal((hk2, d)), rng.standard_normal((hk2, d)))
+    t_step = (time.perf_counter() - t0) / decode_steps * (hkv / hk2)  # one layer of one sequence, all heads
+    del s
+    out["decode"] = dict(value=1.0 / (t_step * L), unit="tok/s/GPU", cores=1, kind="reference",
+                         sample=(f"reference decode step (gate_forward + local_write + gather + attn_ragged, serial "
+                                 f"as engine.cpp:291-327) on a {Tf}-token cache (admit {a}) of {hk2} kv / {hq2} q heads, "
+                                 f"{decode_steps} steps, {t_step / (hkv / hk2) * 1e3:.1f} ms each; x{hkv // hk2} heads, "
+                                 f"x{L} layers per token; the batch's {B} sequences are sequential work"))
+    if with_cfg0:
+        out["configs0_measured"] = cpu_reference_cfg0(O, ref, cfg)
+    return out
+
+
+def cpu_reference_cfg0(O, ref, cfg):
+    """BASELINE configs[0] timed in full on the reference (no extrapolation)."""
+    import numpy as np
+
+    hq, hkv, d, hid, T, D = 32, 8, 128, 128, 4096, 256
+    c0 = dict(cfg, window=1024, T=T)
+    bank = ref.gate_random_init(1, hkv, d, hid, 77, 0.02, -0.5)
+    rng = np.random.default_rng(1)
+    q = rng.standard_normal((T + D, hq, d)).astype(np.float32).astype(np.float64)
+    k = rng.standard_normal((T + D, hkv, d)).astype(np.float32).astype(np.float64)
+    v = rng.standard_normal((T + D, hkv, d)).astype(np.float32).astype(np.float64)
+    s = _ref_session(O, ref, c0, hq, hkv, T + D, bank)
+    t0 = time.perf_counter()
+    s.prefill_layer(0, q[:T], k[:T], v[:T])
+    t1 = time.perf_counter()
+    for t in range(T, T + D):
+        s.decode_layer(0, q[t], k[t], v[t])
+    t2 = time.perf_counter()
+    return dict(prefill_tok_s=T / (t1 - t0), decode_tok_s=D / (t2 - t1), prefill_s=t1 - t0, decode_s=t2 - t1,
+                cores=os.cpu_count() or 1,
+                sample="BASELINE configs[0] in full on the reference (oracle/_ref, fp64): 1 layer, 32q/8kv, d=128, "
+                       "T=4096 prefill (parallel_for over heads) + 256 decode steps, W=1024")
 
 
 # ------------------------------------------------------------------ GPU arm --
@@ -184,10 +241,13 @@ def run_gpu(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("nccl", device_id=dev)  # plumbing only: barrier, max-over-ranks, the NCCL id
     L, Hq, Hkv, d, hid = cfg["layers"], cfg["q_heads"], cfg["kv_heads"], cfg["d"], cfg["hidden"]
-    assert Hkv % world == 0, "KV heads must divide the GPU count"
-    hkv, hq = Hkv // world, Hq // world
+    # N = the number of KV-head shards: the GPUs of the job, or --emulate-shard N
+    # on one GPU (rank 0's shard; the NVLink transfer itself is not emulated)
+    shards = world if world > 1 else max(1, args.emulate_shard)
+    assert Hkv % shards == 0, "KV heads must divide the shard count"
+    hkv, hq = Hkv // shards, Hq // shards
     T, B, Wn, D = cfg["T"], cfg["batch"], cfg["window"], cfg["decode_steps"]
     if args.tokens:
         T = args.tokens
@@ -202,6 +262,10 @@ def run_gpu(args, cfg):
     sess = W.Session(L, hq, hkv, d, hid, Wn, tau=cfg["tau"], rope_base=cfg["rope_base"], page_size=cfg["page"],
                      max_seqs=B, max_tokens=T + D, max_prefill_tokens=T, kv_head_offset=rank * hkv, device=local,
                      gate_bank=bank)
+    if world > 1:  # C1 through the C-ABI: NCCL communicator owned by the context
+        box = [W.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        sess.comm_init(box[0], world, rank)
     # ---- resident inputs: `slots` distinct layer-input sets ------------------
     slots = max(1, min(args.slots, L))
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
@@ -223,11 +287,15 @@ def run_gpu(args, cfg):
     qd = [qd_all[:, i] for i in range(slots)]
     kd = [kd_all[:, i] for i in range(slots)]
     vd = [vd_all[:, i] for i in range(slots)]
-    out = torch.empty(B, T, hq, d, dtype=torch.bfloat16, device=dev)
+    # head outputs: double-buffered when the all-gather of layer l runs on the
+    # comm stream while layer l+1's attention writes the other buffer
+    outs = [torch.empty(B, T, hq, d, dtype=torch.bfloat16, device=dev) for _ in range(2 if shards > 1 else 1)]
     dout = torch.empty(B, hq, d, dtype=torch.bfloat16, device=dev)
-    # rank-major head-shard blocks (concatenated along dim 0; see sharding.gather_heads)
-    gath = torch.empty(world * B, T, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
-    dgath = torch.empty(world * B, hq, d, dtype=torch.bfloat16, device=dev) if world > 1 else None
+    full = torch.empty(B, T, Hq, d, dtype=torch.bfloat16, device=dev) if shards > 1 else None
+    dfull = torch.empty(B, Hq, d, dtype=torch.bfloat16, device=dev) if shards > 1 else None
+    # emulated shard: the rank-major receive buffer NCCL would fill
+    stage = torch.zeros(shards, B * T, hq * d, dtype=torch.bfloat16, device=dev) if world == 1 and shards > 1 else None
+    dstage = torch.zeros(shards, B, hq * d, dtype=torch.bfloat16, device=dev) if stage is not None else None
 
     # ---- calibrate b2 per (layer, kv head) to admission a ---------------------
     ztau = math.log(cfg["tau"] / (1 - cfg["tau"]))
@@ -249,9 +317,21 @@ def run_gpu(args, cfg):
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     launches = {"n": 0}
 
+    def exchange_prefill(o_):
+        """C1 after a layer's attention: the all-gather of head outputs on the
+        context's comm stream (overlapping the next layer), or its local part
+        (the assembly) when one GPU emulates a shard."""
+        if world > 1:
+            sess.comm_join()  # the previous layer's exchange is done: its buffer may be rewritten
+            sess.allgather_heads(o_, full, async_=True)
+            launches["n"] += 1
+        elif stage is not None:
+            W.assemble_heads(stage, full, shards, B * T)
+            launches["n"] += 1
+
     def prefill_layer(l, k3_events=None, inputs=None, out_buf=None):
         qi, ki, vi = inputs if inputs is not None else (Q[l % slots], K[l % slots], V[l % slots])
-        o_ = out if out_buf is None else out_buf
+        o_ = outs[l % len(outs)] if out_buf is None else out_buf
         check(lib.wgkv_gate_score(h, l, B, T, 0, P(ki), None, P(kpost), P(g_ws), P(bits_ws), None, 0, None), "K1")
         check(lib.wgkv_admit_prefill(h, l, 0, B, T, P(kpost), P(vi), P(g_ws), P(bits_ws)), "K2")
         if k3_events is not None:
@@ -260,8 +340,8 @@ def run_gpu(args, cfg):
         if k3_events is not None:
             k3_events[1].record(stream)
         launches["n"] += 6  # rope table, gate, recheck, plan, scatter, vs
-        if world > 1:
-            dist.all_gather_into_tensor(gath, o_)  # rank-major head shards (C1)
+        if shards > 1:
+            exchange_prefill(o_)
 
     # One decode token-step over all layers, issued eagerly or replayed from a
     # CUDA graph captured once (kills per-kernel launch gaps); the step's new
@@ -271,14 +351,22 @@ def run_gpu(args, cfg):
     sk = [sk_all[i] for i in range(slots)]
     sv = [sv_all[i] for i in range(slots)]
 
-    def decode_token_step():
+    def exchange_decode(o_):
+        if world > 1:
+            sess.allgather_heads(o_, dfull)  # KB-sized: on the compute stream, inside the graph
+        elif dstage is not None:
+            W.assemble_heads(dstage, dfull, shards, B)
+
+    def decode_token_step(qs=None, ks=None, vs=None, os_=None):
         for l in range(L):
             sl = l % slots
-            check(lib.wgkv_decode_layer(h, l, 0, B, P(sq[sl]), P(sk[sl]), P(sv[sl]), None, P(dout), None, None),
-                  "decode")
-            if world > 1:
-                dist.all_gather_into_tensor(dgath, dout)
+            qi, ki, vi = (sq[sl], sk[sl], sv[sl]) if qs is None else (qs[l], ks[l], vs[l])
+            o_ = dout if os_ is None else os_[l]
+            check(lib.wgkv_decode_layer(h, l, 0, B, P(qi), P(ki), P(vi), None, P(o_), None, None), "decode")
+            if shards > 1:
+                exchange_decode(o_)
 
+    per_layer_dec = 2 + (1 if shards > 1 else 0)  # K5 + finish (merge, new token, K4) [+ C1]
     graph = {"g": None}
 
     def _capture(fn):
@@ -293,7 +381,7 @@ def run_gpu(args, cfg):
         stream.wait_stream(gs)
         return g_
 
-    def decode_all(step0=0):
+    def decode_all():
         for s_ in range(D):
             sq_all.copy_(qd_all[s_], non_blocking=True)
             sk_all.copy_(kd_all[s_], non_blocking=True)
@@ -302,7 +390,7 @@ def run_gpu(args, cfg):
                 graph["g"].replay()
             else:
                 decode_token_step()
-            launches["n"] += 2 * L  # per layer: K5 (attention over the pre-append cache) + finish (merge, new token, K4)
+            launches["n"] += per_layer_dec * L
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -310,12 +398,18 @@ def run_gpu(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def one_step(record):
-        e = [ev() for _ in range(3)]
+    def prefill_all(record):
         k3 = [(ev(), ev()) for _ in range(L)] if record else None
-        e[0].record(stream)
         for l in range(L):
             prefill_layer(l, k3[l] if k3 else None)
+        if world > 1:
+            sess.comm_join()  # the last layer's exchange belongs to the prefill
+        return k3
+
+    def one_step(record):
+        e = [ev() for _ in range(3)]
+        e[0].record(stream)
+        k3 = prefill_all(record)
         e[1].record(stream)
         decode_all()
         e[2].record(stream)
@@ -329,17 +423,11 @@ def run_gpu(args, cfg):
             for l in range(L):
                 prefill_layer(l)
                 pairs_layer.append(int(pair_count(bits_ws, Wn).sum().item()) * (hq // hkv))
+            if world > 1:
+                sess.comm_join()
             st0 = sess.stats(0, B)
             if not args.no_graphs:  # capture one token-step over all layers (recorded, not executed)
-                gstream = torch.cuda.Stream(dev)
-                gstream.wait_stream(stream)
-                sess.set_stream(gstream)
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=gstream):
-                    decode_token_step()
-                sess.set_stream(stream)
-                stream.wait_stream(gstream)
-                graph["g"] = g
+                graph["g"] = _capture(decode_token_step)
             decode_all()
             st1 = sess.stats(0, B)
             resident = (st0["resident_entries"], st1["resident_entries"])
@@ -377,25 +465,19 @@ def run_gpu(args, cfg):
     # ---- end to end through the public API, host buffers -----------------------
     e2e = None
     if not args.no_e2e:
-        hq_in = [torch.empty_like(Q[0], device="cpu").pin_memory() for _ in range(1)]
+        hq_in = torch.empty_like(Q[0], device="cpu").pin_memory()
         hk_in = torch.empty_like(K[0], device="cpu").pin_memory()
         hv_in = torch.empty_like(V[0], device="cpu").pin_memory()
-        hq_in[0].copy_(Q[0])
+        hq_in.copy_(Q[0])
         hk_in.copy_(K[0])
         hv_in.copy_(V[0])
-        h_out = torch.empty_like(out, device="cpu").pin_memory()
-        dq_h = torch.empty_like(qd[0], device="cpu").pin_memory()
-        dq_h.copy_(qd[0])
-        dk_h = torch.empty_like(kd[0], device="cpu").pin_memory()
-        dk_h.copy_(kd[0])
-        dv_h = torch.empty_like(vd[0], device="cpu").pin_memory()
-        dv_h.copy_(vd[0])
-        dout_h = torch.empty_like(dout, device="cpu").pin_memory()
+        h_out = torch.empty_like(outs[0], device="cpu").pin_memory()
         bufs = [(torch.empty_like(Q[0]), torch.empty_like(K[0]), torch.empty_like(V[0])) for _ in range(2)]
-        outs = [out, torch.empty_like(out)]
+        e_outs = [outs[0], outs[1] if len(outs) > 1 else torch.empty_like(outs[0])]
         # three-stage pipeline on three streams: H2D of layer l+1's inputs, the
-        # layer's kernels, and D2H of layer l-1's output run concurrently (PCIe
-        # is full duplex); inputs and outputs are double-buffered
+        # layer's kernels (+ C1), and D2H of layer l-1's output (this rank's
+        # heads) run concurrently (PCIe is full duplex); inputs and outputs are
+        # double-buffered
         h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ready = [torch.cuda.Event() for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
@@ -414,7 +496,7 @@ def run_gpu(args, cfg):
             with torch.cuda.stream(h2d_s):
                 if l >= 2:
                     h2d_s.wait_event(free[b_])  # layer l-2 has consumed this buffer
-                for dst, src in zip(bufs[b_], (hq_in[0], hk_in, hv_in)):
+                for dst, src in zip(bufs[b_], (hq_in, hk_in, hv_in)):
                     dst.copy_(src, non_blocking=True)
                 ready[b_].record(h2d_s)
 
@@ -426,35 +508,38 @@ def run_gpu(args, cfg):
             stream.wait_event(ready[b])
             if l >= 2:
                 stream.wait_event(drained[b])  # output of layer l-2 is on the host
-            prefill_layer(l, inputs=bufs[b], out_buf=outs[b])
+            prefill_layer(l, inputs=bufs[b], out_buf=e_outs[b])
             free[b].record(stream)
             computed[b].record(stream)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(computed[b])
-                h_out.copy_(outs[b], non_blocking=True)
+                h_out.copy_(e_outs[b], non_blocking=True)
                 drained[b].record(d2h_s)
             h2d += sum(x.numel() * x.element_size() for x in bufs[b])
-            d2h += out.numel() * out.element_size()
+            d2h += e_outs[b].numel() * e_outs[b].element_size()
+        if world > 1:
+            sess.comm_join()
         stream.wait_stream(d2h_s)
         stream.wait_stream(h2d_s)
         # decode: one CUDA graph per token-step (H2D of the step's q/k/v from a
-        # pinned staging slot, the 32 layers' kernels, D2H of the output), two
-        # graphs alternating over double-buffered staging slots
-        # per step: ONE H2D of every layer's q/k/v and ONE D2H of every layer's output
+        # pinned staging slot, the 32 layers' kernels (+ C1), D2H of the
+        # outputs), two graphs alternating over double-buffered staging slots
         dq_d = torch.empty((L,) + tuple(qd[0][0].shape), dtype=torch.bfloat16, device=dev)
         dk_d = torch.empty((L,) + tuple(kd[0][0].shape), dtype=torch.bfloat16, device=dev)
         dv_d = torch.empty((L,) + tuple(vd[0][0].shape), dtype=torch.bfloat16, device=dev)
         do_d = torch.empty((L,) + tuple(dout.shape), dtype=torch.bfloat16, device=dev)
-        stage = [[torch.empty_like(x, device="cpu").pin_memory() for x in (dq_d, dk_d, dv_d, do_d)] for _ in range(2)]
+        stage_h = [[torch.empty_like(x, device="cpu").pin_memory() for x in (dq_d, dk_d, dv_d, do_d)]
+                   for _ in range(2)]
+        dq_h = qd[0].cpu()
+        dk_h = kd[0].cpu()
+        dv_h = vd[0].cpu()
 
         def e2e_step(b):
-            sq_h, sk_h, sv_h, so_h = stage[b]
+            sq_h, sk_h, sv_h, so_h = stage_h[b]
             dq_d.copy_(sq_h, non_blocking=True)
             dk_d.copy_(sk_h, non_blocking=True)
             dv_d.copy_(sv_h, non_blocking=True)
-            for l in range(L):
-                check(lib.wgkv_decode_layer(h, l, 0, B, P(dq_d[l]), P(dk_d[l]), P(dv_d[l]), None, P(do_d[l]), None,
-                                            None), "dec")
+            decode_token_step(dq_d, dk_d, dv_d, do_d)
             so_h.copy_(do_d, non_blocking=True)
 
         e2e_graphs = [_capture(lambda b=b: e2e_step(b)) for b in range(2)] if not args.no_graphs else None
@@ -465,7 +550,7 @@ def run_gpu(args, cfg):
             b = s_ % 2
             if s_ >= 2:
                 step_done[b].synchronize()  # the slot's previous step has drained
-            for dst, src in zip(stage[b][:3], (dq_h[s_], dk_h[s_], dv_h[s_])):
+            for dst, src in zip(stage_h[b][:3], (dq_h[s_], dk_h[s_], dv_h[s_])):
                 dst.copy_(src.unsqueeze(0).expand_as(dst))  # this step's token inputs of every layer
             if e2e_graphs:
                 e2e_graphs[b].replay()
@@ -486,16 +571,17 @@ def run_gpu(args, cfg):
         e2e = {"value": B * T / e2e_pre, "unit": "tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "decode_tok_s_per_gpu": B * D / e2e_dec / world,
                "note": "one step through the C-ABI from pinned host buffers. Prefill: per layer H2D of Q/K/V and D2H "
-                       "of the attention output, on their own streams (PCIe full duplex) overlapping the layer "
-                       "kernels, inputs and outputs double-buffered. Decode: per token-step a CUDA graph of one H2D "
-                       "of the 32 layers' q/k/v, the layers' kernels and one D2H of their outputs, from "
-                       "double-buffered pinned staging slots the host fills each step"}
+                       "of this rank's attention output, on their own streams (PCIe full duplex) overlapping the "
+                       "layer kernels (and, N > 1, the head all-gather), inputs and outputs double-buffered. "
+                       "Decode: per token-step a CUDA graph of one H2D of the 32 layers' q/k/v, the layers' kernels "
+                       "(+ all-gather) and one D2H of their outputs, from double-buffered pinned staging slots the "
+                       "host fills each step"}
 
     if world > 1:
         dist.barrier()
     res = dict(pre_s=pre_s, dec_s=dec_s, k3_s=k3_s, tot_s=tot_s, wall_s=t_wall, pairs_layer=pairs_layer,
                resident=resident, clocks=clk.summary(), launches=launches["n"] // args.steps, e2e=e2e,
-               T=T, B=B, D=D, world=world, hq=hq, hkv=hkv)
+               T=T, B=B, D=D, world=world, shards=shards, hq=hq, hkv=hkv)
     if world > 1:
         dist.destroy_process_group()
     return rank, res
@@ -518,6 +604,9 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="issue decode kernels eagerly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-T", type=int, default=16384)
+    ap.add_argument("--emulate-shard", type=int, default=0,
+                    help="one GPU runs rank 0's KV-head shard of N GPUs (8/N kv heads) incl. the head all-gather's "
+                         "assembly; the NVLink transfer is not emulated and no scaling curve is measured")
     args = ap.parse_args()
     if args.config in ("serve", "1m"):
         import bench_configs
@@ -538,6 +627,8 @@ def main():
                 "heads": f"{cfg['q_heads']}q/{cfg['kv_heads']}kv", "head_dim": cfg["d"], "gate_hidden": cfg["hidden"],
                 "window": cfg["window"], "admission": cfg["admit"], "tau": cfg["tau"], "page_size": cfg["page"],
                 "parallelism": f"kv-head shard x{world}", "l2": "inputs larger than L2 (no flush)"}
+    if args.emulate_shard > 1 and world == 1:
+        base_cfg["parallelism"] = f"emulated: rank 0 of a kv-head shard x{args.emulate_shard}, on 1 GPU"
     metric = "WG-KV prefill tok/s @128K & decode tok/s/GPU, % of tensor/HBM roofline"
 
     if args.impl == "reference":
@@ -549,7 +640,9 @@ def main():
                 "steps": steps, "warmup": 0, "ms_per_step": 1000.0 * cb["sample_seconds"],
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": base_cfg,
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "decode",
+                                                    "configs0_measured") if k in cb},
+                "decode_tok_s_per_gpu": cb["decode"]["value"],
                 "e2e": {"value": cb["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -567,7 +660,11 @@ def main():
     dec_bytes = D * (avg_res * 2 * d * 2 + 2 * B * r["hq"] * d * 2 * L)
     dec_gbs = dec_bytes / r["dec_s"] / 1e9
     prefill_tok_s = B * T / r["pre_s"]
-    decode_tok_s_gpu = B * D / r["dec_s"] / world
+    shards = r["shards"]
+    if world == 1 and shards > 1:  # emulated shard: whole-job numbers as if every shard ran on its own GPU
+        decode_tok_s_gpu = B * D / r["dec_s"] / shards
+    else:
+        decode_tok_s_gpu = B * D / r["dec_s"] / world
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(tpath):
@@ -593,10 +690,17 @@ def main():
                             "note": "resident Global+Local K+V bytes (bf16) + q/out per token-step / decode time"},
         "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
     }
+    if world == 1 and shards > 1:
+        line["emulated_shard"] = {
+            "n": shards, "kv_heads_per_gpu": r["hkv"], "q_heads_per_gpu": r["hq"],
+            "note": "one GPU runs rank 0's shard (its heads of every token) plus the head all-gather's assembly "
+                    "kernel; 'value' is the whole-job prefill tok/s if every shard ran this fast on its own GPU, "
+                    "the NVLink transfer is NOT included and no scaling curve was measured"}
     if not args.no_cpu_baseline:
         try:
             cb = cpu_reference(cfg, args.cpu_sample_T, 1)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "decode",
+                                                       "configs0_measured") if k in cb}
         except Exception as exc:  # the reference build needs g++ on the host
             line["cpu_baseline"] = {"value": None, "unit": "tok/s", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"unavailable: {exc}"}

@@ -200,6 +200,30 @@ int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq);
 /* pool occupancy: out[0] = capacity, out[1] = free pages */
 int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out);
 
+/* ---- C1: head-output all-gather of KV-head sharding (no reference
+ * equivalent) -------------------------------------------
+ * N contexts (one per GPU, one process per GPU or one process driving all),
+ * rank r created with kv_head_offset = r * kv_heads, own the q heads
+ * [r * q_heads, (r + 1) * q_heads).  wgkv_allgather_heads rebuilds Session's
+ * concat layout on every rank: full_out[s][t][p][:] = q head p's output
+ * (engine.cpp:234-238), full_out [nseq][T][N * q_heads][d] (cfg.dtype), from
+ * each rank's local_out [nseq][T][q_heads][d] (wgkv_vs_prefill /
+ * wgkv_decode_layer output; decode: T = 1).  NCCL over NVLink into a staging
+ * buffer, then an assemble kernel.  async = 0: on the context stream;
+ * async = 1: on the context's comm stream after the work enqueued so far, so
+ * the caller's next layer overlaps it -- wgkv_comm_join orders the context
+ * stream after it (before full_out is read or local_out reused).  Without a
+ * communicator (single device) it is a copy.  NCCL is loaded at run time. */
+int wgkv_comm_unique_id(uint8_t* id128);                         /* ncclGetUniqueId, on one rank */
+int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank); /* ncclCommInitRank */
+int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank);   /* caller-owned ncclComm_t */
+int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out, void* full_out, int async);
+int wgkv_comm_join(wgkv_ctx* ctx);
+/* the assembly step alone: rank-major [world][rows][blk_bytes] -> [rows][world * blk_bytes]
+ * on `stream` (cudaStream_t); blk_bytes a multiple of 16 */
+int wgkv_assemble_heads(int world, long rows, size_t blk_bytes, const void* rank_major, void* full_out,
+                        void* stream);
+
 /* vs_mask_pair_count (attention.cpp:182-191) of one head's bits, computed in
  * closed form on the host: sum_i min(i+1, W) + C(i-W+1). */
 uint64_t wgkv_vs_pair_count(const uint8_t* bits, long T, long window);

@@ -258,6 +258,7 @@ class Ref(_Base):
         L.wr_session_select_topk.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_long, _lp, _lp]
         L.wr_session_snapshot.argtypes = [C.c_void_p, C.c_char_p, C.c_long, _lp]
         L.wr_session_cache_stats.argtypes = [C.c_void_p, _dp]
+        L.wr_session_populate_layer.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_long]
         L.wr_gate_save.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.wr_thread_budget.restype = C.c_int
         L.wr_policy_trace.argtypes = [C.c_int, C.c_long, C.c_long, _u8p, C.c_int, C.c_long, C.c_long, C.c_double,
@@ -435,6 +436,14 @@ class Session:
         _check(self.lib.wr_session_prefill_layer_timed(self.h, layer, _ptr(q_pre), _ptr(k_pre), _ptr(v),
                                                        q_pre.shape[0], _ptr(secs), C.byref(pairs)), "prefill_timed")
         return secs, pairs.value
+
+    def populate_layer(self, layer, k_pre, v, gates):
+        """Reference backend only: RoPE + HeadCache::prefill_populate of every kv
+        head with the given gates [kv_heads][t] (no attention) -- a cache state
+        for timing decode steps at long context."""
+        k_pre, v, gates = _f64(k_pre), _f64(v), _f64(gates)
+        _check(self.lib.wr_session_populate_layer(self.h, layer, _ptr(k_pre), _ptr(v), _ptr(gates), k_pre.shape[0]),
+               "populate")
 
     def decode_layer(self, layer, q_pre, k_pre, v, forced_gates=None):
         q_pre, k_pre, v = _f64(q_pre), _f64(k_pre), _f64(v)

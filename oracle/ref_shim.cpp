@@ -270,6 +270,34 @@ int wr_session_prefill_layer(void* sp, int layer, const double* q_pre, const dou
     }
 }
 
+// HeadCache::prefill_populate (kvstore.cpp:160-203) of every kv head of a
+// layer with given gates, no attention: builds a long-context cache state for
+// timing the reference's decode step (bench.py cpu_baseline).  k_pre, v
+// [t][kv_heads][d]; gates [kv_heads][t].
+int wr_session_populate_layer(void* sp, int layer, const double* k_pre, const double* v, const double* gates, long t) {
+    auto& s = *static_cast<RefSession*>(sp);
+    try {
+        const int d = s.d, hkv = s.kv_heads;
+        const RopeConfig rope{d, s.rope_base};
+        std::vector<Matrix> k_post(static_cast<size_t>(hkv), Matrix(t, d)), vv(static_cast<size_t>(hkv), Matrix(t, d));
+        parallel_for(hkv, [&](long lo, long hi) {
+            for (long h = lo; h < hi; ++h)
+                for (long i = 0; i < t; ++i) {
+                    std::memcpy(k_post[h].row(i).data(), k_pre + (i * hkv + h) * d, sizeof(double) * d);
+                    apply_rope_inplace(k_post[h].row(i), i, rope);
+                    std::memcpy(vv[h].row(i).data(), v + (i * hkv + h) * d, sizeof(double) * d);
+                }
+        });
+        for (int h = 0; h < hkv; ++h)
+            s.at(layer, h).prefill_populate(s.pool, k_post[h], vv[h],
+                                            std::vector<double>(gates + h * t, gates + (h + 1) * t),
+                                            Threshold{s.tau}, 0);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
 // engine.cpp:291-327 with the projections removed
 int wr_session_decode_layer(void* sp, int layer, const double* q_pre, const double* k_pre, const double* v,
                             const double* forced_gates, double* out, double* g_out, int* events, uint64_t* evals) {

@@ -76,6 +76,12 @@ SIGNATURES = {
     "wgkv_release": ([_vp, _i, _i], _i),
     "wgkv_pool_info": ([_vp, C.POINTER(C.c_int64)], _i),
     "wgkv_vs_pair_count": ([_vp, _l, _l], C.c_uint64),
+    "wgkv_comm_unique_id": ([_vp], _i),
+    "wgkv_comm_init": ([_vp, _vp, _i, _i], _i),
+    "wgkv_comm_attach": ([_vp, _vp, _i, _i], _i),
+    "wgkv_allgather_heads": ([_vp, _i, _l, _vp, _vp, _i], _i),
+    "wgkv_comm_join": ([_vp], _i),
+    "wgkv_assemble_heads": ([_i, _l, C.c_size_t, _vp, _vp, _vp], _i),
 }
 
 _LIB = None

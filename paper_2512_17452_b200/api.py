@@ -189,10 +189,46 @@ class Session:
     def release(self, seq0=0, nseq=1):
         check(self.lib.wgkv_release(self.h, seq0, nseq), "release")
 
+    # ---- C1: head-output all-gather (KV-head sharding) -------------------------
+    def comm_init(self, unique_id: bytes, world: int, rank: int):
+        """Join the NCCL world of KV-head shards (this context = rank `rank`,
+        created with kv_head_offset = rank * kv_heads)."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(self.lib.wgkv_comm_init(self.h, buf, world, rank), "comm_init")
+
+    def allgather_heads(self, local_out: torch.Tensor, full_out: torch.Tensor, async_: bool = False):
+        """local_out [nseq][T][q_heads][d] -> full_out [nseq][T][world*q_heads][d]
+        (the reference's concat layout, engine.cpp:234-238); decode: T = 1."""
+        nseq = local_out.shape[0]
+        T = local_out.shape[1] if local_out.dim() == 4 else 1
+        check(self.lib.wgkv_allgather_heads(self.h, nseq, T, _p(local_out), _p(full_out), int(async_)),
+              "allgather_heads")
+        return full_out
+
+    def comm_join(self):
+        check(self.lib.wgkv_comm_join(self.h), "comm_join")
+
     def pool_info(self) -> dict:
         v = (C.c_int64 * 2)()
         check(self.lib.wgkv_pool_info(self.h, v), "pool_info")
         return dict(capacity=v[0], free=v[1])
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (call on one rank, broadcast the 128 bytes)."""
+    buf = C.create_string_buffer(128)
+    check(_lib.load().wgkv_comm_unique_id(buf), "comm_unique_id")
+    return buf.raw
+
+
+def assemble_heads(rank_major: torch.Tensor, full_out: torch.Tensor, world: int, rows: int, stream=None):
+    """wgkv_assemble_heads: rank-major [world][rows][blk] -> [rows][world * blk]
+    (the assembly step of wgkv_allgather_heads, usable on its own)."""
+    blk = rank_major.numel() * rank_major.element_size() // (world * rows)
+    st = stream if stream is not None else torch.cuda.current_stream(rank_major.device)
+    check(_lib.load().wgkv_assemble_heads(world, rows, blk, _p(rank_major), _p(full_out), C.c_void_p(st.cuda_stream)),
+          "assemble_heads")
+    return full_out
 
 
 def vs_pair_count(bits: np.ndarray, window: int) -> int:

@@ -223,26 +223,29 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 }
 
 // ---------------------------------------------------------------------------
-// K4 standalone: one CTA per (seq, kv head) of the call (append.cuh)
+// K4 standalone: the split append's route + gate CTAs (append.cuh)
 // ---------------------------------------------------------------------------
 template <typename E>
 __global__ void __launch_bounds__(kAppendThreads) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
-                                                                        long W, const E* __restrict__ k_pre,
+                                                                        long W, int npairs,
+                                                                        const E* __restrict__ k_pre,
                                                                         const E* __restrict__ v,
                                                                         const float* __restrict__ forced_g,
-                                                                        DecodeTrace tr) {
+                                                                        DecodeTrace tr, AppendWork wk) {
     extern __shared__ __align__(16) uint8_t append_smem[];
-    append_token<E>(pv, ga, layer, seq0, blockIdx.x / pv.kv_heads, blockIdx.x % pv.kv_heads, W, k_pre, v, forced_g,
-                    tr, append_smem);
+    append_role<E>(pv, ga, layer, seq0, W, npairs, blockIdx.x, k_pre, v, forced_g, tr, wk, append_smem);
 }
 
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
-                         const E* k_pre, const E* v, const float* forced_g, const DecodeTrace& tr, cudaStream_t st) {
+                         const E* k_pre, const E* v, const float* forced_g, const DecodeTrace& tr,
+                         const AppendWork& wk, cudaStream_t st) {
     const size_t smem = append_smem_bytes(pv.head_dim, ga.hidden);
     if (ensure_smem(decode_append_kernel<E>, smem) != cudaSuccess) return WGKV_ECUDA;
-    decode_append_kernel<E><<<nseq * pv.kv_heads, kAppendThreads, smem, st>>>(pv, ga, layer, seq0, W, k_pre, v,
-                                                                               forced_g, tr);
+    const int npairs = nseq * pv.kv_heads;
+    const int grid = npairs * (1 + (forced_g ? 0 : gate_ctas_per_pair(ga.hidden)));
+    decode_append_kernel<E><<<grid, kAppendThreads, smem, st>>>(pv, ga, layer, seq0, W, npairs, k_pre, v, forced_g,
+                                                                 tr, wk);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -250,7 +253,7 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     template int launch_admit_prefill<E>(const PoolView&, int, int, int, long, long, const E*, const E*,          \
                                          const float*, const uint8_t*, int32_t*, cudaStream_t);                   \
     template int launch_decode_append<E>(const PoolView&, const GateArgs&, int, int, int, long, const E*, const E*, \
-                                         const float*, const DecodeTrace&, cudaStream_t);
+                                         const float*, const DecodeTrace&, const AppendWork&, cudaStream_t);
 INST(float)
 INST(__nv_bfloat16)
 #undef INST

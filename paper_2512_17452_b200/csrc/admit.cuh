@@ -13,6 +13,7 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 // K4 as its own launch (one CTA per (seq, kv head)), append.cuh
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
-                         const E* k_pre, const E* v, const float* forced_g, const DecodeTrace& tr, cudaStream_t st);
+                         const E* k_pre, const E* v, const float* forced_g, const DecodeTrace& tr,
+                         const AppendWork& wk, cudaStream_t st);
 
 }  // namespace wgkv

@@ -16,6 +16,7 @@
 #include "admit.cuh"
 #include "attn.cuh"
 #include "attn_tc.cuh"
+#include "comm.cuh"
 #include "gate.cuh"
 
 using namespace wgkv;
@@ -215,6 +216,7 @@ struct wgkv_ctx {
     float* ws_part = nullptr;
     int* ws_nchunks = nullptr;
     int* ws_tokpos = nullptr;  // [S*H] the new token's position per (seq, kv head) (deferred append)
+    AppendWork wk{};           // split-append scratch (append.cuh)
     float* ws_score = nullptr;  // K6: [S][Hq][n_gp] page scores
     int32_t* ws_sel = nullptr;  // K6: [S][Hq][n_gp] selected logical pages
     int32_t* ws_nsel = nullptr; // K6: [S][Hq]
@@ -225,6 +227,14 @@ struct wgkv_ctx {
     int* quest_full = nullptr;             // K6 Quest mode: [L][S][H] pages whose metadata is final
     int max_chunks = kMaxChunks;
     long near_cap = 0;
+    // C1 (comm.cu): head-output all-gather over a world of KV-head shards
+    void* comm = nullptr;
+    bool own_comm = false;
+    int world = 1, rank = 0;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_comm_in = nullptr, ev_comm_done = nullptr;
+    uint8_t* stage = nullptr;  // [world][stage_rows][q_heads * d] elements
+    long stage_rows = 0;
     // host mirrors for lifecycle checks and grid sizing
     std::vector<uint8_t> prefilled;  // [L][S]
     std::vector<long> tokens;        // [L][S] tokens seen
@@ -354,6 +364,11 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     // per-pair chunk counts | work-stealing counter | per-pair merge counters
     ctx->ws_nchunks = dalloc<int>(2 * (size_t)S * H + 1, o);
     ctx->ws_tokpos = dalloc<int>((size_t)S * H, o);
+    ctx->wk.terms = dalloc<double>((size_t)S * H * c.hidden, o);
+    ctx->wk.count = dalloc<int>((size_t)S * H, o);
+    ctx->wk.slot = dalloc<int>((size_t)S * H, o);
+    ctx->wk.event = dalloc<int>((size_t)S * H, o);
+    ctx->wk.next = dalloc<HeadState>((size_t)S * H, o);
     if (c.topk_budget > 0) {
         ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
         ctx->ws_sel = dalloc<int32_t>((size_t)S * c.q_heads * n_gp, o);
@@ -382,6 +397,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     cudaMemcpy(pv.err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
     cudaMemset(pv.state, 0, sizeof(HeadState) * (size_t)L * S * H);
     cudaMemset(ctx->ws_nchunks, 0, sizeof(int) * (2 * (size_t)S * H + 1));  // K5 work counter starts at 0
+    cudaMemset(ctx->wk.count, 0, sizeof(int) * (size_t)S * H);              // split-append arrivals
     // zeroed pages: K3/K5 may stream stale slots of a partially filled page
     // (masked out), which must at least be finite
     cudaMemset(pv.data, 0, (size_t)cap * 2 * ps * d * ctx->esz);
@@ -402,6 +418,11 @@ int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     if (!ctx) return WGKV_OK;
     DevGuard dg_(ctx->cfg.device);
     cudaDeviceSynchronize();
+    if (ctx->own_comm) comm_destroy(ctx->comm);
+    if (ctx->stage) cudaFree(ctx->stage);
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->ev_comm_in) cudaEventDestroy(ctx->ev_comm_in);
+    if (ctx->ev_comm_done) cudaEventDestroy(ctx->ev_comm_done);
     for (void* p : ctx->owned) cudaFree(p);
     delete ctx;
     return WGKV_OK;
@@ -676,10 +697,10 @@ static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, cons
     if (ctx->cfg.dtype == WGKV_BF16)
         st = launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
                                                  (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g, tr,
-                                                 ctx->stream);
+                                                 ctx->wk, ctx->stream);
     else
         st = launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
-                                         (const float*)v, forced_g, tr, ctx->stream);
+                                         (const float*)v, forced_g, tr, ctx->wk, ctx->stream);
     if (st) return fail(st, "decode append kernel failed");
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
     return WGKV_OK;
@@ -798,6 +819,7 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     fin.v_new = (const __nv_bfloat16*)v;
     fin.forced_g = forced_g;
     fin.tr = tr;
+    fin.wk = ctx->wk;
     st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, &fin);
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
@@ -971,6 +993,111 @@ int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out) {
     out[0] = ctx->pv.capacity;
     out[1] = top;
     return WGKV_OK;
+}
+
+// ---- C1: head-output all-gather (comm.cu) ------------------------------------
+int wgkv_comm_unique_id(uint8_t* id128) {
+    if (!id128) return fail(WGKV_EINVAL, "null argument");
+    const int st = comm_unique_id(id128);
+    if (st) {
+        std::string why;
+        nccl_available(&why);
+        return fail(st, "ncclGetUniqueId: " + why);
+    }
+    return WGKV_OK;
+}
+
+static int comm_setup(wgkv_ctx* ctx, int world, int rank) {
+    const auto& c = ctx->cfg;
+    if (c.kv_head_offset != rank * c.kv_heads)
+        return fail(WGKV_EINVAL, "comm: rank r must own kv heads [r*kv_heads, (r+1)*kv_heads) (kv_head_offset)");
+    if ((size_t)c.q_heads * c.head_dim * ctx->esz % 16 != 0)
+        return fail(WGKV_ENOTSUP, "comm: a rank's head block per token must be a multiple of 16 bytes");
+    ctx->world = world;
+    ctx->rank = rank;
+    // staging for one chunk of tokens from every rank (bounded: 8192 rows)
+    ctx->stage_rows = std::max<long>(1, std::min<long>(ctx->cfg.max_prefill_tokens, 8192));
+    const size_t bytes = (size_t)world * ctx->stage_rows * c.q_heads * c.head_dim * ctx->esz;
+    WGKV_CUDA_TRY(cudaMalloc(&ctx->stage, bytes));
+    WGKV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_comm_in, cudaEventDisableTiming));
+    WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_comm_done, cudaEventDisableTiming));
+    return WGKV_OK;
+}
+
+int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank) {
+    if (!ctx || !id128) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    if (ctx->comm) return fail(WGKV_ESTATE, "comm: already initialised");
+    if (world < 1 || rank < 0 || rank >= world) return fail(WGKV_EINVAL, "comm: bad world / rank");
+    int st = comm_setup(ctx, world, rank);
+    if (st) return st;
+    std::string err;
+    st = comm_init(&ctx->comm, id128, world, rank, &err);
+    if (st) return fail(st, err);
+    ctx->own_comm = true;
+    return WGKV_OK;
+}
+
+int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank) {
+    if (!ctx || !nccl_comm) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    if (ctx->comm) return fail(WGKV_ESTATE, "comm: already initialised");
+    if (world < 1 || rank < 0 || rank >= world) return fail(WGKV_EINVAL, "comm: bad world / rank");
+    std::string why;
+    if (!nccl_available(&why)) return fail(WGKV_ENOTSUP, why);
+    const int st = comm_setup(ctx, world, rank);
+    if (st) return st;
+    ctx->comm = nccl_comm;
+    return WGKV_OK;
+}
+
+int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out, void* full_out, int async) {
+    if (!ctx || !local_out || !full_out) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    const auto& c = ctx->cfg;
+    if (nseq < 1 || T < 1) return fail(WGKV_EINVAL, "allgather_heads: empty");
+    const size_t blk = (size_t)c.q_heads * c.head_dim * ctx->esz;  // one rank's heads of one token
+    if (!ctx->comm) {  // a single device owns every head: the layout is already the reference's
+        if (local_out != full_out)
+            WGKV_CUDA_TRY(cudaMemcpyAsync(full_out, local_out, (size_t)nseq * T * blk, cudaMemcpyDeviceToDevice,
+                                          ctx->stream));
+        return WGKV_OK;
+    }
+    cudaStream_t st = ctx->stream;
+    if (async) {  // on the comm stream, after everything enqueued so far on the compute stream
+        WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_comm_in, ctx->stream));
+        WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_comm_in, 0));
+        st = ctx->comm_stream;
+    }
+    const auto* src = static_cast<const uint8_t*>(local_out);
+    auto* dst = static_cast<uint8_t*>(full_out);
+    std::string err;
+    for (int s = 0; s < nseq; ++s)
+        for (long t0 = 0; t0 < T; t0 += ctx->stage_rows) {
+            const long n = std::min(ctx->stage_rows, T - t0);
+            const int r = comm_allgather_assemble(ctx->comm, src + ((size_t)s * T + t0) * blk, ctx->stage, n * blk,
+                                                  dst + ((size_t)s * T + t0) * blk * ctx->world, n, ctx->world, blk,
+                                                  blk * ctx->world, st, &err);
+            if (r) return fail(r, err.empty() ? std::string("assemble kernel failed") : err);
+        }
+    if (async) WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_comm_done, ctx->comm_stream));
+    return WGKV_OK;
+}
+
+int wgkv_comm_join(wgkv_ctx* ctx) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
+    if (ctx->comm_stream) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm_done, 0));
+    return WGKV_OK;
+}
+
+int wgkv_assemble_heads(int world, long rows, size_t blk_bytes, const void* rank_major, void* full_out,
+                        void* stream) {
+    if (world < 1 || rows < 0 || !rank_major || !full_out) return fail(WGKV_EINVAL, "bad argument");
+    const int st = launch_assemble(static_cast<const uint8_t*>(rank_major), static_cast<uint8_t*>(full_out), rows,
+                                   world, blk_bytes, blk_bytes * world, static_cast<cudaStream_t>(stream));
+    return st ? fail(st, "assemble_heads: blocks must be 16-byte multiples") : WGKV_OK;
 }
 
 // diagnostics (not part of the C-ABI contract): out[0] = tokens the last

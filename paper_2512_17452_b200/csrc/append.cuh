@@ -1,11 +1,24 @@
-// append.cuh -- K4: one decode token of one (seq, kv head) into the dual cache.
+// append.cuh -- K4: one decode token of each (seq, kv head) into the dual cache.
 //
 // HeadCache::local_write + promote (kvstore.cpp:102-158) fused with the
-// decode-time gate (gate_forward, gating.cpp:158-171, in the reference's exact
-// fp64 operation order) and RoPE (numerics.cpp:50-77), run by one 256-thread
-// CTA.  Used by the standalone append kernel (admit.cu) and by the decode
-// finish kernel (decode_finish.cu), which runs it beside the chunk merge of
-// the same layer.
+// decode-time gate (gate_forward, gating.cpp:158-171) and RoPE
+// (numerics.cpp:50-77).  One token per (seq, kv head) is a chain of dependent
+// memory round trips (state -> ring page -> victim bit -> page pop -> copies)
+// plus an fp64 gate whose weights (hidden x 2d doubles, 256 KB per head at
+// d = hidden = 128) one SM would need several microseconds to stream.  So a
+// pair's work is split over CTAs of one launch that run concurrently:
+//   * the route CTA: RoPE of the new key, the routing decision (lazy promotion
+//     of the ring victim on its stored bit, device page allocation), the
+//     victim's copy into Global and the new token's K/V into the ring slot;
+//   * ceil(hidden / 16) gate CTAs: 16 hidden units each, W1 rows staged
+//     through shared memory, every z1 a sequential fp64 dot in the reference's
+//     order (dot, numerics.cpp:94-99, no FMA) -> w2 * gelu(z1 + b1);
+//   * whichever CTA of the pair arrives last (an arrival counter) sums
+//     z2 = b2 + terms in order, applies sigmoid and the clamp, writes the
+//     token's gate and bit into its slot, publishes the new HeadState (only
+//     now, so every CTA of the pair saw the old one) and the GateTrace.
+// Used by the standalone append kernel (admit.cu) and by the decode finish
+// kernel (decode_finish.cu), which runs these CTAs beside the chunk merge.
 #pragma once
 #include "common.cuh"
 #include "gate.cuh"
@@ -21,38 +34,90 @@ struct DecodeTrace {
     int32_t* events;   // PromotionEvent of the ring victim: 0 none, 1 promoted, 2 dropped, -1 failed
 };
 
+// per-(seq, kv head) scratch of the split append, [max_seqs * kv_heads] (+ terms)
+struct AppendWork {
+    double* terms;       // [pair][hidden] w2 * gelu(z1 + b1) from the gate CTAs
+    int* count;          // arrivals of the pair's CTAs; the last one resets it to 0
+    int* slot;           // new token's pool slot (page * ps + slot) or -1
+    int* event;          // promotion event (0 none, 1 promoted, 2 dropped, -1 failed)
+    HeadState* next;     // the state after the append, published by the last arrival
+};
+
 constexpr int kAppendThreads = 256;
-// dynamic smem of append_token: xs [2d] + terms [hidden] doubles, kpost [d] floats
+constexpr int kGateUnits = 16;  // hidden units per gate CTA
+__host__ __device__ inline int gate_ctas_per_pair(int hidden) { return (hidden + kGateUnits - 1) / kGateUnits; }
+// dynamic smem of the roles: gate = feature [2d] + W1 rows [16][2d + 1] doubles
 __host__ __device__ inline size_t append_smem_bytes(int d, int hidden) {
-    return sizeof(double) * (2 * (size_t)d + (size_t)hidden) + sizeof(float) * (size_t)d;
+    return sizeof(double) * (2 * (size_t)d + (size_t)kGateUnits * (2 * d + 1)) + 16;
 }
 
-// s: call-relative sequence index (inputs are [nseq][kv_heads][d]); the cache
-// slot is seq0 + s.  Whole CTA (kAppendThreads threads), smem from the caller.
+// ---------------------------------------------------------------------------
+// the last arrival of a pair finishes the token (thread 0 only)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void append_finalize(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s,
+                                                int h, const float* __restrict__ forced_g, const DecodeTrace& tr,
+                                                const AppendWork& wk) {
+    __threadfence();  // acquire: the other CTAs' terms / slot / state
+    const int pair = (seq0 + s) * pv.kv_heads + h;
+    const int blk = layer * pv.kv_heads + h;
+    double g;
+    if (forced_g) {
+        g = (double)forced_g[(size_t)s * pv.kv_heads + h];
+    } else {  // z2 = b2 + sum_h terms, sequential (gating.cpp:162-166)
+        const volatile double* t = wk.terms + (size_t)pair * ga.hidden;
+        double z2 = ga.b2d[blk];
+        for (int u = 0; u < ga.hidden; ++u) z2 = __dadd_rn(z2, t[u]);
+        g = gate_from_z2(z2);
+    }
+    const uint8_t bit = g >= ga.tau ? 1 : 0;
+    const int sl = *(volatile int*)&wk.slot[pair];
+    const int ev = *(volatile int*)&wk.event[pair];
+    if (sl >= 0) {
+        pv.gate[sl] = (float)g;
+        pv.adm[sl] = bit;
+    }
+    if (ev >= 0) pv.state[pv.head_index(layer, seq0 + s, h)] = wk.next[pair];
+    const size_t o = (size_t)s * pv.kv_heads + h;
+    if (tr.g) tr.g[o] = (float)g;
+    if (tr.bits) tr.bits[o] = bit;
+    if (tr.near_tau) tr.near_tau[o] = fabs(g - ga.tau) < 1e-6 ? 1 : 0;
+    if (tr.events) tr.events[o] = ev;
+    wk.count[pair] = 0;  // ready for the next step
+}
+
+// every CTA of a pair calls this once its writes are issued (whole CTA)
+__device__ __forceinline__ void append_arrive(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s, int h,
+                                              const float* __restrict__ forced_g, const DecodeTrace& tr,
+                                              const AppendWork& wk, int arrivals) {
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // release this CTA's writes
+        last = atomicAdd(&wk.count[(seq0 + s) * pv.kv_heads + h], 1) == arrivals - 1;
+        if (last) append_finalize(pv, ga, layer, seq0, s, h, forced_g, tr, wk);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// route CTA: RoPE, lazy promotion, ring write (no gate)
+// ---------------------------------------------------------------------------
 template <typename E>
-__device__ __forceinline__ void append_token(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s, int h,
+__device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s, int h,
                                              long W, const E* __restrict__ k_pre, const E* __restrict__ v,
-                                             const float* __restrict__ forced_g, const DecodeTrace& tr,
-                                             uint8_t* smem) {
+                                             const AppendWork& wk) {
     const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
     const long hidx = pv.head_index(layer, seq0 + s, h);
-    double* xs = reinterpret_cast<double*>(smem);  // [2d] gate feature [k_pre ; RoPE(k_pre)] (fp64)
-    double* terms = xs + 2 * d;                    // [hidden]
-    float* kpost = reinterpret_cast<float*>(terms + ga.hidden);  // [d] RoPE'd key (fp32) for the cache
+    const int pair = (seq0 + s) * pv.kv_heads + h;
     __shared__ int vpage, vslot, gpage, gslot, npage, nslot, event;
-    __shared__ HeadState nst;
     const size_t in = ((size_t)s * pv.kv_heads + h) * d;
-    const int blk = layer * pv.kv_heads + h;
     E* pool = reinterpret_cast<E*>(pv.data);
-
-    // ---- phase A: inputs, state, speculative victim fetch, RoPE, feature ----
-    // (the new token's inputs do not depend on the cache state: loads first;
+    // the new token's inputs do not depend on the cache state: loads first;
     // every thread reads the state and the ring page under local_ptr itself, so
-    // the victim's K/V is fetched in the same round as its admission bit)
+    // the victim's K/V is fetched in the same round as its admission bit
     const bool kt = tid < d / 2, et = tid < d;
     const float x0 = kt ? to_f(k_pre[in + 2 * tid]) : 0.f, x1 = kt ? to_f(k_pre[in + 2 * tid + 1]) : 0.f;
     const E vnew = et ? v[in + tid] : E();
-    HeadState st = pv.state[hidx];
+    const HeadState st = pv.state[hidx];
     const long pos = st.tokens_seen;
     const int slot = st.local_ptr;
     const int lp0 = pv.lpt[hidx * pv.n_lp + slot / ps];
@@ -63,27 +128,13 @@ __device__ __forceinline__ void append_token(const PoolView& pv, const GateArgs&
         vk = ks[tid];
         vv = ks[tid + (size_t)ps * d];
     }
+    float y0 = 0.f, y1 = 0.f;  // the cached key: fp64 angle, fp32 rotation
     if (kt) {
         float c, sn;
-        rope_cs(ga.freq, tid, pos, c, sn);  // the cached key: fp64 angle, fp32 rotation
-        rope_pair_f32(x0, x1, c, sn, kpost[2 * tid], kpost[2 * tid + 1]);
-        if (!forced_g) {  // the gate feature in the reference's arithmetic (numerics.cpp:53-62)
-            const double a = x0, b = x1;
-            const double angle = __dmul_rn((double)pos, ga.freq[tid]);
-            const double cd = cos(angle), sd = sin(angle);
-            xs[2 * tid] = a;
-            xs[2 * tid + 1] = b;
-            xs[d + 2 * tid] = __dsub_rn(__dmul_rn(a, cd), __dmul_rn(b, sd));
-            xs[d + 2 * tid + 1] = __dadd_rn(__dmul_rn(a, sd), __dmul_rn(b, cd));
-        }
+        rope_cs(ga.freq, tid, pos, c, sn);
+        rope_pair_f32(x0, x1, c, sn, y0, y1);
     }
-    __syncthreads();
-
-    // ---- phase B: the gate's hidden units (threads 0-127) beside the routing
-    // decision (thread 128): lazy promotion inspects the VICTIM's stored bit
-    // (written W steps ago), never the new token's gate ----------------------
-    if (!forced_g) gate_terms_ref(ga.gd(), blk, xs, d, terms, 0, 128);
-    if (tid == 128) {
+    if (tid == 0) {
         int lp = lp0;
         int ev = 0, vp = -1, gp = -1, gs_ = 0;
         HeadState ns = st;
@@ -138,44 +189,101 @@ __device__ __forceinline__ void append_token(const PoolView& pv, const GateArgs&
         gslot = gs_;
         npage = lp;
         nslot = slot % ps;
-        nst = ns;
+        wk.next[pair] = ns;
+        wk.event[pair] = ev;
+        wk.slot[pair] = lp >= 0 ? lp * ps + slot % ps : -1;
+        if (ev == 1) {  // the victim's metadata, read before the new token overwrites the slot
+            const size_t a = (size_t)vp * ps + slot % ps, b = (size_t)gp * ps + gs_;
+            pv.gate[b] = pv.gate[a];
+            pv.pos[b] = pv.pos[a];
+            pv.adm[b] = pv.adm[a];
+        }
+        if (lp >= 0) pv.pos[(size_t)lp * ps + slot % ps] = (int32_t)pos;
     }
     __syncthreads();
-
-    // ---- phase C: promote the victim (K/V fetched in phase A; gate, pos, bit),
-    // write the new token into the ring slot, its gate, the state ------------
+    // promote the victim (K/V fetched above), then the new token into the ring
     if (event == 1 && et) {
         E* kd = pool + (size_t)gpage * pv.page_elems() + (size_t)gslot * d;
         kd[tid] = vk;
         kd[tid + (size_t)ps * d] = vv;
     }
-    if (npage >= 0 && et) {
+    if (npage >= 0) {
         E* kd = pool + (size_t)npage * pv.page_elems() + (size_t)nslot * d;
-        kd[tid] = from_f<E>(kpost[tid]);
-        kd[tid + (size_t)ps * d] = vnew;
-    }
-    if (tid == 0) {
-        if (event == 1) {  // the victim's metadata, read before the new token overwrites the slot
-            const size_t a = (size_t)vpage * ps + vslot, b = (size_t)gpage * ps + gslot;
-            pv.gate[b] = pv.gate[a];
-            pv.pos[b] = pv.pos[a];
-            pv.adm[b] = pv.adm[a];
+        if (kt) {
+            kd[2 * tid] = from_f<E>(y0);
+            kd[2 * tid + 1] = from_f<E>(y1);
         }
-        const double g = forced_g ? (double)forced_g[(size_t)s * pv.kv_heads + h] : gate_from_z2(gate_z2_ref(ga.gd(), blk, terms));
-        const uint8_t bit = g >= ga.tau ? 1 : 0;
-        if (npage >= 0) {
-            const size_t b = (size_t)npage * ps + nslot;
-            pv.gate[b] = (float)g;
-            pv.adm[b] = bit;
-            pv.pos[b] = (int32_t)pos;
-        }
-        if (event >= 0) pv.state[hidx] = nst;
-        const size_t o = (size_t)s * pv.kv_heads + h;
-        if (tr.g) tr.g[o] = (float)g;
-        if (tr.bits) tr.bits[o] = bit;
-        if (tr.near_tau) tr.near_tau[o] = fabs(g - ga.tau) < 1e-6 ? 1 : 0;
-        if (tr.events) tr.events[o] = event;
+        if (et) kd[tid + (size_t)ps * d] = vnew;
     }
+    (void)vpage;
+    (void)vslot;
+}
+
+// ---------------------------------------------------------------------------
+// gate CTA j of a pair: terms of hidden units [16 j, 16 j + 16)
+// ---------------------------------------------------------------------------
+template <typename E>
+__device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s,
+                                                 int h, int j, const E* __restrict__ k_pre, const AppendWork& wk,
+                                                 uint8_t* smem) {
+    const int tid = threadIdx.x, d = pv.head_dim, fd = 2 * d, hid = ga.hidden;
+    const int pair = (seq0 + s) * pv.kv_heads + h;
+    const int blk = layer * pv.kv_heads + h;
+    const int u0 = j * kGateUnits, nu = min(kGateUnits, hid - u0);
+    double* xs = reinterpret_cast<double*>(smem);  // [2d] feature [k_pre ; RoPE(k_pre)] (fp64)
+    double* ws = xs + fd;                          // [16][2d + 1] W1 rows (padded: conflict-free columns)
+    // the state is published only by the pair's last arrival: tokens_seen is the new token's position
+    const long pos = pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
+    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
+    const double* w1 = ga.w1d + ((size_t)blk * hid + u0) * fd;
+    // W1 rows, coalesced (16-byte vectors when 2d is even: it is)
+    for (int e = tid; e < nu * fd / 2; e += blockDim.x) {
+        const int r = e / (fd / 2), c2 = e % (fd / 2);
+        const double2 w = reinterpret_cast<const double2*>(w1 + (size_t)r * fd)[c2];
+        ws[r * (fd + 1) + 2 * c2] = w.x;
+        ws[r * (fd + 1) + 2 * c2 + 1] = w.y;
+    }
+    // the feature in the reference's arithmetic (numerics.cpp:53-62)
+    for (int i = tid; i < d / 2; i += blockDim.x) {
+        const double a = to_f(k_pre[in + 2 * i]), b = to_f(k_pre[in + 2 * i + 1]);
+        const double angle = __dmul_rn((double)pos, ga.freq[i]);
+        const double cd = cos(angle), sd = sin(angle);
+        xs[2 * i] = a;
+        xs[2 * i + 1] = b;
+        xs[d + 2 * i] = __dsub_rn(__dmul_rn(a, cd), __dmul_rn(b, sd));
+        xs[d + 2 * i + 1] = __dadd_rn(__dmul_rn(a, sd), __dmul_rn(b, cd));
+    }
+    __syncthreads();
+    if (tid < nu) {
+        const double* wr = ws + tid * (fd + 1);
+        double z1 = 0.0;  // dot (numerics.cpp:94-99)
+        for (int k = 0; k < fd; ++k) z1 = __dadd_rn(z1, __dmul_rn(wr[k], xs[k]));
+        const int u = u0 + tid;
+        wk.terms[(size_t)pair * hid + u] = __dmul_rn(ga.w2d[(size_t)blk * hid + u], gelu_ref(__dadd_rn(z1, ga.b1d[(size_t)blk * hid + u])));
+    }
+}
+
+// CTA role dispatch of the split append: r in [0, npairs) route CTAs, then
+// npairs * gate_ctas_per_pair gate CTAs (none with forced gates)
+template <typename E>
+__device__ __forceinline__ void append_role(const PoolView& pv, const GateArgs& ga, int layer, int seq0, long W,
+                                            int npairs, int r, const E* __restrict__ k_pre, const E* __restrict__ v,
+                                            const float* __restrict__ forced_g, const DecodeTrace& tr,
+                                            const AppendWork& wk, uint8_t* smem) {
+    const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
+    int pr, j = -1;
+    if (r < npairs) {
+        pr = r;
+    } else {
+        pr = (r - npairs) / gpp;
+        j = (r - npairs) % gpp;
+    }
+    const int s = pr / pv.kv_heads, h = pr % pv.kv_heads;
+    if (j < 0)
+        append_route<E>(pv, ga, layer, seq0, s, h, W, k_pre, v, wk);
+    else
+        append_gate_part<E>(pv, ga, layer, seq0, s, h, j, k_pre, wk, smem);
+    append_arrive(pv, ga, layer, seq0, s, h, forced_g, tr, wk, gpp + 1);
 }
 
 }  // namespace wgkv

@@ -62,6 +62,7 @@ struct FinishArgs {
     const __nv_bfloat16* v_new;  // [nseq][kv_heads][d]
     const float* forced_g;       // [nseq][kv_heads] or null
     DecodeTrace tr;
+    AppendWork wk;
 };
 
 // counter_reset_by_append: the kernel just before on the stream zeroed the work

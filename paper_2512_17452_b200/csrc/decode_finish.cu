@@ -10,9 +10,10 @@
 //   * combine CTAs, one per (seq, q head): merge K5's chunk partials and the
 //     new token itself (its logit from the RoPE'd q and k, value v), which is
 //     exactly the reference's attended set after local_write;
-//   * append CTAs, one per (seq, kv head): K4 (append.cuh) -- lazy promotion of
-//     the ring victim, the new token into the ring, its exact fp64 gate --
-//     which may only start once K5 has read the victim slot, i.e. now.
+//   * append CTAs: K4 (append.cuh) -- per (seq, kv head) a route CTA (lazy
+//     promotion of the ring victim, the new token into the ring) and gate CTAs
+//     (its exact fp64 gate) -- which may only start once K5 has read the
+//     victim slot, i.e. now.
 // Both roles run concurrently, so K4 costs no extra step on the layer's path.
 #include "attn.cuh"
 
@@ -29,10 +30,9 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     // K5 has finished: partials written, the ring's victim slots read
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int tid = threadIdx.x;
-    if ((int)blockIdx.x >= ncomb) {  // ---- append role: K4 for one (seq, kv head)
-        const int r = blockIdx.x - ncomb;
-        append_token<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, r / a.pv.kv_heads, r % a.pv.kv_heads, a.window,
-                                    fin.k_new, fin.v_new, fin.forced_g, fin.tr, fsm);
+    if ((int)blockIdx.x >= ncomb) {  // ---- append roles: K4 (route + gate CTAs, append.cuh)
+        append_role<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, a.window, a.n_pairs, blockIdx.x - ncomb,
+                                   fin.k_new, fin.v_new, fin.forced_g, fin.tr, fin.wk, fsm);
         return;
     }
     // ---- combine role: one (seq, q head) --------------------------------------
@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
 int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, const float* part, __nv_bfloat16* out,
                          const FinishArgs& fin, cudaStream_t st) {
     if (a.pv.head_dim != 128 || !a.tokpos || !a.counter || !a.nchunks) return WGKV_ENOTSUP;
-    const int ncomb = nseq * a.q_heads, napp = nseq * a.pv.kv_heads;
+    const int ncomb = nseq * a.q_heads;
+    const int napp = nseq * a.pv.kv_heads * (1 + (fin.forced_g ? 0 : gate_ctas_per_pair(fin.ga.hidden)));
     const size_t smem = std::max(append_smem_bytes(a.pv.head_dim, fin.ga.hidden),
                                  sizeof(float) * (2 * (kAppendThreads / 32) + (kAppendThreads / 32) * 128));
     if (ensure_smem(decode_finish_kernel, smem) != cudaSuccess) return WGKV_ECUDA;

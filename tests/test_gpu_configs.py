@@ -331,6 +331,12 @@ def test_virtual_shards_reproduce_unsharded(W, orc, pin):
             for r in range(N):
                 for h in range(hk):
                     assert np.array_equal(parts[r]["gpos"][b][h], full["gpos"][b][r * hk + h])
+        # C1's assembly step: the rank-major all-gather result -> the reference's
+        # concat layout (engine.cpp:234-238), bitwise the unsharded output
+        rank_major = torch.stack([p_["out"].reshape(B * T, -1) for p_ in parts])
+        full_out = torch.empty_like(full["out"])
+        W.assemble_heads(rank_major, full_out, N, B * T)
+        assert torch.equal(full_out, full["out"]), N
         dec = torch.cat([p_["dec"] for p_ in parts], dim=2)
         if pin:
             assert torch.equal(dec, full["dec"]), N
@@ -421,3 +427,29 @@ def test_decode_trace_near_tau_reported(W, orc):
     assert abs(gr - 0.1) < 1e-6
     assert tr["near_tau"].item() == 1
     assert tr["bits"].item() == (gr >= 0.1)  # the exact-order fp64 gate reproduces the reference's bit here
+
+
+def test_comm_world_one(W, orc):
+    """wgkv_comm_init / wgkv_allgather_heads through NCCL with a world of one
+    (the only world one GPU can host): prefill- and decode-shaped outputs come
+    back in the reference's layout, synchronously and on the comm stream."""
+    hq, hkv, d, T, B = 8, 2, 128, 300, 2
+    s = W.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=T, gate_bank=orc.gate_random_init(1, hkv, d, d, 3))
+    s.comm_init(W.nccl_unique_id(), 1, 0)
+    x = torch.randn(B, T, hq, d, device="cuda").to(torch.bfloat16)
+    full = torch.zeros_like(x)
+    s.allgather_heads(x, full)
+    s.sync()
+    assert torch.equal(full, x)
+    full2 = torch.zeros_like(x)
+    s.allgather_heads(x, full2, async_=True)
+    s.comm_join()
+    s.sync()
+    assert torch.equal(full2, x)
+    xd = torch.randn(B, hq, d, device="cuda").to(torch.bfloat16)
+    fd = torch.zeros_like(xd)
+    s.allgather_heads(xd, fd)
+    s.sync()
+    assert torch.equal(fd, xd)
+    with pytest.raises(ValueError):  # rank 1 of 2 must own kv heads [hkv, 2 hkv)
+        W.Session(1, hq, hkv, d, d, 64, max_tokens=T).comm_init(W.nccl_unique_id(), 2, 1)
