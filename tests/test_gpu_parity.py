@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
 import oracle as O  # noqa: E402
+import topk_check as TK  # noqa: E402
 
 # every reference-generated session: d = 128 (Llama head geometry) and the
 # reference's own default ModelConfig geometry (d = 16, session_small_l2)
@@ -304,28 +305,20 @@ def test_topk_decode_vs_oracle(W, orc, dtype, budget):
     s.prefill_layer(0, to_dev(q[:, :T], dt), to_dev(k[:, :T], dt), to_dev(v[:, :T], dt))
     r = O.Session(orc, 1, hq, hkv, d, d, Wn, gate_bank=bank, max_tokens=T + steps, topk_budget=budget)
     r.prefill_layer(0, q[0, :T], k[0, :T], v[0, :T])
-    near_ties = checks = 0
+    ties = checks = 0
+    rel = TK.BF16_KEY_REL if dtype == "bf16" else TK.FP32_ACC_REL
     for t in range(T, T + steps):
         o = s.decode_layer(0, to_dev(q[:, t], dt), to_dev(k[:, t], dt), to_dev(v[:, t], dt))
-        ro, _, _, _ = r.decode_layer(0, q[0, t], k[0, t], v[0, t])
+        r.decode_layer(0, q[0, t], k[0, t], v[0, t])
         o = o.float().cpu().numpy()[0]
         for p in range(hq):
-            checks += 1
-            if rel_err(o[p], ro[p]) < TOL[dtype]:
-                continue
-            # only a near-tie at the selection boundary may flip the discrete
-            # choice (bf16 keys vs the oracle's fp64 keys): verify it is one
-            assert dtype == "bf16", (t, p)
-            gk = r.gather(0, p // (hq // hkv))["global_k"]
+            c = r.gather(0, p // (hq // hkv))
+            gk, gv, lk, lv = (np.asarray(c[x], np.float64) for x in ("global_k", "global_v", "local_k", "local_v"))
             qr = orc.rope(q[0, t, p], t)
-            sc = np.array([np.max(gk[i:i + 16] @ qr) for i in range(0, gk.shape[0], 16)])
-            srt = np.sort(sc)[::-1]
-            kk = min(budget, len(srt))
-            assert kk < len(srt), (t, p)
-            gap = (srt[kk - 1] - srt[kk]) / max(abs(srt[kk - 1]), 1e-30)
-            assert gap < 3e-2, (t, p, gap)
-            near_ties += 1
-    assert near_ties <= checks // 4, (near_ties, checks)
+            sc, err = TK.maxdot_scores(gk, qr, rel)
+            ties += TK.check_selection(o[p], qr, gk, gv, lk, lv, sc, err, budget, TOL[dtype])
+            checks += 1
+    print(f"top-k {dtype} budget {budget}: {ties} of {checks} (step, q head) selections resolved as bounded ties")
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
@@ -377,7 +370,7 @@ def test_topk_quest_bound_vs_numpy(W, orc, budget):
     s = W.Session(1, hq, hkv, d, d, Wn, max_tokens=T + steps, gate_bank=bank, topk_budget=budget,
                   topk_mode=W.TOPK_QUEST)
     s.prefill_layer(0, to_dev(q[:, :T], dt), to_dev(k[:, :T], dt), to_dev(v[:, :T], dt))
-    near_ties = checks = 0
+    ties = checks = 0
     for t in range(T, T + steps):
         o = s.decode_layer(0, to_dev(q[:, t], dt), to_dev(k[:, t], dt), to_dev(v[:, t], dt)).float().cpu().numpy()[0]
         for h in range(hkv):
@@ -390,25 +383,11 @@ def test_topk_quest_bound_vs_numpy(W, orc, budget):
                 p = h * gs + g
                 qr = orc.rope(q[0, t, p], t)
                 bound = np.maximum(qr * mn, qr * mx).sum(1)
-                order = sorted(range(n), key=lambda i: (-bound[i], i))  # higher first, ties to older
-                kk = min(budget, n)
-                sel = sorted(order[:kk])
-                rows = np.concatenate([np.arange(16 * i, min(16 * i + 16, gk.shape[0])) for i in sel]) if sel else \
-                    np.zeros(0, int)
-                keys = np.concatenate([gk[rows], lk])
-                vals = np.concatenate([gv[rows], lv])
-                lg = keys @ qr / math.sqrt(d)
-                w = np.exp(lg - lg.max())
-                ref = (w[:, None] * vals).sum(0) / w.sum()
+                # keys are the device's own (exported): only fp32 accumulation differs
+                err = TK.FP32_ACC_REL * (np.abs(qr) * np.maximum(np.abs(mn), np.abs(mx))).sum(1)
+                ties += TK.check_selection(o[p], qr, gk, gv, lk, lv, bound, err, budget, TOL["bf16"])
                 checks += 1
-                if rel_err(o[p], ref) < TOL["bf16"]:
-                    continue
-                srt = sorted(bound, reverse=True)
-                assert kk < n, (t, p)
-                gap = (srt[kk - 1] - srt[kk]) / max(abs(srt[kk - 1]), 1e-30)
-                assert gap < 3e-2, (t, p, gap)
-                near_ties += 1
-    assert near_ties <= checks // 4, (near_ties, checks)
+    print(f"quest budget {budget}: {ties} of {checks} (step, q head) selections resolved as bounded ties")
 
 
 @pytest.mark.parametrize("topk", [0, 3])
@@ -448,10 +427,15 @@ def test_ragged_batch_decode(W, orc, topk):
             assert np.array_equal(ev[b], rev), (i, b)
             for p in range(hq):
                 checks += 1
-                if rel_err(o[b, p], ro[p]) >= TOL["bf16"]:
-                    assert topk, (i, b, p)  # only a top-k near-tie may flip a page (see test_topk_decode_vs_oracle)
-                    near += 1
-    assert near <= checks // 10, (near, checks)
+                if rel_err(o[b, p], ro[p]) < TOL["bf16"]:
+                    continue
+                assert topk, (i, b, p)  # only a top-k near-tie may flip a page
+                c = refs[b].gather(0, p // (hq // hkv))
+                gk, gv, lk, lv = (np.asarray(c[x], np.float64) for x in ("global_k", "global_v", "local_k", "local_v"))
+                qr = orc.rope(qs[b, p], lens[b] + i)
+                sc, err = TK.maxdot_scores(gk, qr, TK.BF16_KEY_REL)
+                near += TK.check_selection(o[b, p], qr, gk, gv, lk, lv, sc, err, topk, TOL["bf16"])
+    print(f"ragged top-k {topk}: {near} of {checks} selections resolved as bounded ties")
     for b in range(nseq):
         for h in range(hkv):
             a, r = s.gather(0, b, h), refs[b].gather(0, h)
