@@ -88,6 +88,43 @@ public:
         throw_on(wgkv_decode_layer(ctx_, layer, seq0, nseq, q, k_pre, v, forced_g, out, g, events),
                  "Session::decode_step");
     }
+    // decode_layer with the step's GateTrace (engine.cpp:300-305): g, g >= tau,
+    // the near-tau flag and the ring victim's promotion event, device pointers
+    void decode_layer(int layer, int seq0, int nseq, const void* q, const void* k_pre, const void* v, void* out,
+                      const float* forced_g, const wgkv_decode_trace& trace) {
+        throw_on(wgkv_decode_layer_traced(ctx_, layer, seq0, nseq, q, k_pre, v, forced_g, out, &trace),
+                 "Session::decode_step");
+    }
+    // HeadCache accessors + gather (kvstore.hpp:120-127, kvstore.cpp:205-241) of one
+    // (layer, seq, kv head), to host memory; with_kv = false copies positions and gates only
+    struct Gathered {
+        long local_len = 0, local_ptr = 0, global_len = 0, tokens_seen = 0, local_pages = 0, global_pages = 0;
+        std::vector<long> global_pos, local_pos;
+        std::vector<float> global_gate, local_gate;
+        std::vector<float> global_k, global_v, local_k, local_v;  // [rows][d] when with_kv
+    };
+    Gathered gather(int layer, int seq, int kv_head, int head_dim, bool with_kv = false) {
+        int64_t lens[6];
+        throw_on(wgkv_cache_state(ctx_, layer, seq, kv_head, lens), "HeadCache::gather");
+        Gathered g;
+        g.local_len = lens[0], g.local_ptr = lens[1], g.global_len = lens[2], g.tokens_seen = lens[3];
+        g.local_pages = lens[4], g.global_pages = lens[5];
+        std::vector<int64_t> gp(g.global_len), lp(g.local_len);
+        g.global_gate.resize(g.global_len);
+        g.local_gate.resize(g.local_len);
+        if (with_kv) {
+            g.global_k.resize(g.global_len * head_dim), g.global_v.resize(g.global_len * head_dim);
+            g.local_k.resize(g.local_len * head_dim), g.local_v.resize(g.local_len * head_dim);
+        }
+        throw_on(wgkv_cache_export(ctx_, layer, seq, kv_head, with_kv ? g.global_k.data() : nullptr,
+                                   with_kv ? g.global_v.data() : nullptr, gp.data(), g.global_gate.data(),
+                                   with_kv ? g.local_k.data() : nullptr, with_kv ? g.local_v.data() : nullptr,
+                                   lp.data(), g.local_gate.data()),
+                 "HeadCache::gather");
+        g.global_pos.assign(gp.begin(), gp.end());
+        g.local_pos.assign(lp.begin(), lp.end());
+        return g;
+    }
     // HeadCache::release (kvstore.cpp:243-251) for every head of the slots
     void release(int seq0, int nseq) { throw_on(wgkv_release(ctx_, seq0, nseq), "release"); }
     // cache_snapshot (kvstore.cpp:269-286) of one sequence slot (gate digits of the stored fp32 value)
