@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(kAppendThreads) decode_append_kernel(PoolView 
                                                                         const float* __restrict__ forced_g,
                                                                         DecodeTrace tr, AppendWork wk) {
     extern __shared__ __align__(16) uint8_t append_smem[];
-    append_role<E>(pv, ga, layer, seq0, W, npairs, blockIdx.x, k_pre, v, forced_g, tr, wk, append_smem);
+    const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
+    append_role<E>(pv, ga, layer, seq0, W, npairs, blockIdx.x, gpp, gpp + 1, k_pre, v, forced_g, tr, wk, append_smem);
 }
 
 template <typename E>

@@ -222,19 +222,22 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
 // ---------------------------------------------------------------------------
 // gate CTA j of a pair: terms of hidden units [16 j, 16 j + 16)
 // ---------------------------------------------------------------------------
+// pdl_wait: the CTA runs in the K5 launch, a programmatic dependent whose
+// predecessor may still own the pair's scratch and the head state: only the
+// W1 rows (gate parameters, unchanged while decoding) are staged before
+// griddepcontrol.wait.  In the finish kernel the gate CTAs need no wait: K5
+// (their primary) passed its own wait before releasing them, so every earlier
+// kernel -- the previous layer's finalize included -- has completed.
 template <typename E>
 __device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s,
                                                  int h, int j, const E* __restrict__ k_pre, const AppendWork& wk,
-                                                 uint8_t* smem) {
+                                                 uint8_t* smem, bool pdl_wait = false) {
     const int tid = threadIdx.x, d = pv.head_dim, fd = 2 * d, hid = ga.hidden;
     const int pair = (seq0 + s) * pv.kv_heads + h;
     const int blk = layer * pv.kv_heads + h;
     const int u0 = j * kGateUnits, nu = min(kGateUnits, hid - u0);
     double* xs = reinterpret_cast<double*>(smem);  // [2d] feature [k_pre ; RoPE(k_pre)] (fp64)
     double* ws = xs + fd;                          // [16][2d + 1] W1 rows (padded: conflict-free columns)
-    // the state is published only by the pair's last arrival: tokens_seen is the new token's position
-    const long pos = pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
-    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
     const double* w1 = ga.w1d + ((size_t)blk * hid + u0) * fd;
     // W1 rows, coalesced (16-byte vectors when 2d is even: it is)
     for (int e = tid; e < nu * fd / 2; e += blockDim.x) {
@@ -243,6 +246,10 @@ __device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateA
         ws[r * (fd + 1) + 2 * c2] = w.x;
         ws[r * (fd + 1) + 2 * c2 + 1] = w.y;
     }
+    if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the state is published only by the pair's last arrival: tokens_seen is the new token's position
+    const long pos = pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
+    const size_t in = ((size_t)s * pv.kv_heads + h) * d;
     // the feature in the reference's arithmetic (numerics.cpp:53-62)
     for (int i = tid; i < d / 2; i += blockDim.x) {
         const double a = to_f(k_pre[in + 2 * i]), b = to_f(k_pre[in + 2 * i + 1]);
@@ -264,13 +271,13 @@ __device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateA
 }
 
 // CTA role dispatch of the split append: r in [0, npairs) route CTAs, then
-// npairs * gate_ctas_per_pair gate CTAs (none with forced gates)
+// npairs * gpp gate CTAs of this launch (0 with forced gates, or when the K5
+// launch ran the pair's gate CTA); `arrivals` = CTAs per pair over both launches
 template <typename E>
 __device__ __forceinline__ void append_role(const PoolView& pv, const GateArgs& ga, int layer, int seq0, long W,
-                                            int npairs, int r, const E* __restrict__ k_pre, const E* __restrict__ v,
-                                            const float* __restrict__ forced_g, const DecodeTrace& tr,
-                                            const AppendWork& wk, uint8_t* smem) {
-    const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
+                                            int npairs, int r, int gpp, int arrivals, const E* __restrict__ k_pre,
+                                            const E* __restrict__ v, const float* __restrict__ forced_g,
+                                            const DecodeTrace& tr, const AppendWork& wk, uint8_t* smem) {
     int pr, j = -1;
     if (r < npairs) {
         pr = r;
@@ -283,7 +290,7 @@ __device__ __forceinline__ void append_role(const PoolView& pv, const GateArgs& 
         append_route<E>(pv, ga, layer, seq0, s, h, W, k_pre, v, wk);
     else
         append_gate_part<E>(pv, ga, layer, seq0, s, h, j, k_pre, wk, smem);
-    append_arrive(pv, ga, layer, seq0, s, h, forced_g, tr, wk, gpp + 1);
+    append_arrive(pv, ga, layer, seq0, s, h, forced_g, tr, wk, arrivals);
 }
 
 }  // namespace wgkv

@@ -44,6 +44,11 @@ struct DecArgs {
     int* tokpos;
     int* counter;  // K5 work-stealing counter, reset to 0 by the kernel that merges its partials
     int pin_cp;    // > 0: pages per chunk fixed (wgkv_config.decode_chunk_pages)
+    // deferred append with the MLP gate: the first n_gate_ctas CTAs of the K5
+    // launch are the append's gate CTAs (append.cuh), off the layer's critical
+    // path; the K5 work CTAs follow them
+    int n_gate_ctas;
+    int early_trigger;  // K5 releases its programmatic dependent right after its PDL wait
 };
 
 // K6: select_topk_pages + per-q-head attention over the selection (topk.cu).

@@ -27,19 +27,32 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     extern __shared__ __align__(16) uint8_t fsm[];
     // the next kernel on the stream may launch now; it waits for our completion
     asm volatile("griddepcontrol.launch_dependents;");
+    const int tid = threadIdx.x;
+    // grid: [gate CTAs of the append, when not in the K5 launch][combine CTAs][route CTAs]
+    const int gpp = (fin.forced_g || a.n_gate_ctas > 0) ? 0 : gate_ctas_per_pair(fin.ga.hidden);
+    const int ngate = a.n_pairs * gpp;
+    const int arrivals = fin.forced_g ? 1 : gate_ctas_per_pair(fin.ga.hidden) + 1;
+    if ((int)blockIdx.x < ngate) {
+        // gate CTAs first: they need nothing K5 produces (see append_gate_part),
+        // so they run in the slots K5's tail frees, without the PDL wait
+        const int pr = blockIdx.x / gpp, j = blockIdx.x % gpp;
+        const int s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
+        append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, fsm);
+        append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, arrivals);
+        return;
+    }
     // K5 has finished: partials written, the ring's victim slots read
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int tid = threadIdx.x;
-    if ((int)blockIdx.x >= ncomb) {  // ---- append roles: K4 (route + gate CTAs, append.cuh)
-        append_role<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, a.window, a.n_pairs, blockIdx.x - ncomb,
-                                   fin.k_new, fin.v_new, fin.forced_g, fin.tr, fin.wk, fsm);
+    if ((int)blockIdx.x >= ngate + ncomb) {  // ---- route CTAs of the append (K4, append.cuh)
+        append_role<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, a.window, a.n_pairs, blockIdx.x - ngate - ncomb,
+                                   0, arrivals, fin.k_new, fin.v_new, fin.forced_g, fin.tr, fin.wk, fsm);
         return;
     }
     // ---- combine role: one (seq, q head) --------------------------------------
     constexpr int NW = kAppendThreads / 32;
     constexpr int d = 128;
     const int gs = a.q_heads / a.pv.kv_heads;
-    const int sp = blockIdx.x, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
+    const int sp = blockIdx.x - ngate, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
     const int bh = s * a.pv.kv_heads + h;
     const int lane = tid & 31, warp = tid >> 5;
     const size_t pstride = (size_t)gs * (d + 2);
@@ -47,7 +60,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     float* wm = reinterpret_cast<float*>(fsm);  // [NW]
     float* wl = wm + NW;                         // [NW]
     float* wacc = wl + NW;                       // [NW][d]
-    if (blockIdx.x == 0 && tid == 0) *a.counter = 0;  // K5's work counter, for the next launch
+    if (sp == 0 && tid == 0) *a.counter = 0;  // K5's work counter, for the next launch
     const int nch = min(a.nchunks[bh], kMaxChunks);
     float m = -INFINITY, l = 0.f;
     float2 acc[2];  // columns 2*lane + 64*j
@@ -133,7 +146,9 @@ int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, con
                          const FinishArgs& fin, cudaStream_t st) {
     if (a.pv.head_dim != 128 || !a.tokpos || !a.counter || !a.nchunks) return WGKV_ENOTSUP;
     const int ncomb = nseq * a.q_heads;
-    const int napp = nseq * a.pv.kv_heads * (1 + (fin.forced_g ? 0 : gate_ctas_per_pair(fin.ga.hidden)));
+    // route CTAs, plus the gate CTAs unless K5 ran them (a.n_gate_ctas > 0)
+    const int napp = nseq * a.pv.kv_heads *
+                     (1 + ((fin.forced_g || a.n_gate_ctas > 0) ? 0 : gate_ctas_per_pair(fin.ga.hidden)));
     const size_t smem = std::max(append_smem_bytes(a.pv.head_dim, fin.ga.hidden),
                                  sizeof(float) * (2 * (kAppendThreads / 32) + (kAppendThreads / 32) * 128));
     if (ensure_smem(decode_finish_kernel, smem) != cudaSuccess) return WGKV_ECUDA;

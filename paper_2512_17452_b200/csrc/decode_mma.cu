@@ -13,6 +13,8 @@
 // merges its warps; decode_combine_kernel (attn_simt.cu) merges chunks.
 #include <cuda.h>
 
+#include <cstring>
+
 #include "attn.cuh"
 #include "tc.cuh"
 
@@ -37,6 +39,10 @@ constexpr int CPS = WGKV_K5_CPS;  // CTAs per SM
 constexpr int PAGE_B = 8192; // bf16 page of 16 tokens: K 4 KB | V 4 KB
 constexpr int QROW = 136;    // padded Q row (bf16 elements)
 constexpr int PID_CAP = kDecPidCap;  // pages per work item (staged page ids)
+#ifndef WGKV_GATE_K5_MAX
+#define WGKV_GATE_K5_MAX 64
+#endif
+constexpr int kGateInK5MaxCtas = WGKV_GATE_K5_MAX;  // gate CTAs carried by the K5 launch at most
 #ifndef WGKV_K5_IPC
 #define WGKV_K5_IPC 3  // work items per CTA (work stealing balance vs per-item fixed costs; 3 beats 2 by
                        // 1.5 % at 128K x 4 and 2.2 % on the serving mix with 6-warp CTAs)
@@ -89,7 +95,8 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                                                                       DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                       float* __restrict__ part,
                                                                       int* __restrict__ nchunks,
-                                                                      int* __restrict__ work_counter) {
+                                                                      int* __restrict__ work_counter,
+                                                                      const __grid_constant__ FinishArgs fin) {
     extern __shared__ uint8_t dsm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     constexpr int d = 128;
@@ -97,9 +104,24 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     const int gs = a.q_heads / a.pv.kv_heads;
     const int npairs = a.n_pairs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (!TOPK && (int)blockIdx.x < a.n_gate_ctas) {
+        // deferred append's gate CTAs (append.cuh): the new token's exact fp64
+        // gate (engine.cpp:300-303) is only consumed W steps later (when the
+        // token leaves the ring), so it runs beside the attention instead of
+        // behind it; W1 is staged before the PDL wait
+        const int gpp = gate_ctas_per_pair(fin.ga.hidden);
+        const int pr = blockIdx.x / gpp, j = blockIdx.x % gpp;
+        const int s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
+        append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, sm, true);
+        append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, gpp + 1);
+        return;
+    }
+    const int kcta = (int)blockIdx.x - a.n_gate_ctas, kgrid = (int)gridDim.x - a.n_gate_ctas;
     // launched as a programmatic dependent of the previous kernel (K4, or the
     // previous layer's finish kernel): wait for it (pages, tables, ring state)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // let the kernel that merges our partials launch now (it waits for our completion)
+    if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;");
     uint8_t* ring = sm;                                                                    // [DW][DNS][8 KB]
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm + DW * DNS * PAGE_B);          // [16][QROW]
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + DW * DNS * PAGE_B + 16 * QROW * 2);  // [DW][DNS]
@@ -124,7 +146,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
             const int np = ngv + (st.local_len + ps - 1) / ps;
             item_base[p] = np;
-            if (!TOPK && a.defer && blockIdx.x == 0) a.tokpos[p] = st.tokens_seen;  // the new token (finish kernel)
+            if (!TOPK && a.defer && kcta == 0) a.tokpos[p] = st.tokens_seen;  // the new token (finish kernel)
             tot += np;
             npmax = max(npmax, np);
         }
@@ -147,12 +169,12 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         }
         const long total = tot;
         // ~2 items per CTA, taken dynamically (work stealing) for balance
-        int cp = (int)((total + WGKV_K5_IPC * gridDim.x - 1) / (WGKV_K5_IPC * gridDim.x));
+        int cp = (int)((total + WGKV_K5_IPC * kgrid - 1) / (WGKV_K5_IPC * kgrid));
         cp = max(cp, WGKV_K5_MIN_PAGES);  // per-item fixed costs (page ids, ring fill, merge) amortised
 #if WGKV_K5_RULE == 1
         // few, long pairs (small batches): cap the chunks per pair near 24 (the
         // combine merges every chunk) while keeping >= grid/2 items in flight
-        cp = max(cp, (int)min((long)(npmax + WGKV_K5_CAPCH - 1) / WGKV_K5_CAPCH, (2 * total + gridDim.x - 1) / gridDim.x));
+        cp = max(cp, (int)min((long)(npmax + WGKV_K5_CAPCH - 1) / WGKV_K5_CAPCH, (2 * total + kgrid - 1) / kgrid));
 #endif
         if (a.pin_cp > 0) cp = a.pin_cp;  // pinned split: per-head arithmetic independent of the launch
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
@@ -173,7 +195,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         for (int p = p0; p < p1; ++p) {
             const int nc = max(1, (item_base[p] + cp - 1) / cp);
             item_base[p] = acc;
-            if (blockIdx.x == 0) nchunks[p] = nc;
+            if (kcta == 0) nchunks[p] = nc;
             acc += nc;
         }
         if (p1 == npairs && p0 < p1) {
@@ -466,8 +488,24 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     int* counter = nchunks + (size_t)a.pv.max_seqs * a.pv.kv_heads;
     a.counter = counter;
     if (!counter_reset_by_append) cudaMemsetAsync(counter, 0, sizeof(int), st);
+    // the deferred append's gate CTAs ride in this launch (see the kernel); the
+    // finish kernel then runs only the route CTAs
+    // Few gate CTAs (small batches): in this launch, where they cost K5 a few
+    // slots for ~2 us.  Many (large batches, where they would displace most of
+    // K5's first wave): first in the finish kernel's grid, which K5 releases
+    // early, so they fill the slots K5's tail frees and overlap it.
+    static const char* gp_env = getenv("WGKV_GATE_PLACE");  // A/B switch: "k5" | "finish"
+    static const int gate_k5_max = gp_env ? (strcmp(gp_env, "k5") == 0 ? 1 << 30 : 0) : kGateInK5MaxCtas;
+    static const bool no_trigger = getenv("WGKV_K5_NO_TRIGGER") != nullptr;  // A/B switch
+    FinishArgs fa{};
+    a.n_gate_ctas = 0;
+    if (fin && !fin->forced_g && a.n_pairs * gate_ctas_per_pair(fin->ga.hidden) <= gate_k5_max) {
+        a.n_gate_ctas = a.n_pairs * gate_ctas_per_pair(fin->ga.hidden);
+        fa = *fin;
+    }
+    a.early_trigger = fin && !no_trigger;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CPS * num_sms());
+    cfg.gridDim = dim3(a.n_gate_ctas + CPS * num_sms());
     cfg.blockDim = dim3(DW * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -476,7 +514,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = counter_reset_by_append ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kern, tp, a, q, part, nchunks, counter);
+    cudaLaunchKernelEx(&cfg, kern, tp, a, q, part, nchunks, counter, fa);
     a.nchunks = nchunks;
     if (fin) return launch_decode_finish(a, nseq, q, part, out, *fin, st);
     extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);

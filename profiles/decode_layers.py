@@ -25,8 +25,10 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
     args = ap.parse_args()
-    B, T, L, Hq, Hkv, d = args.batch, args.T, args.layers, 32, 8, 128
+    B, T, L, Hq, Hkv, d = args.batch, args.T, args.layers, args.hq, args.hkv, 128
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(0)
     bank = np.zeros((L, Hkv, d * 2 * d + 2 * d + 1))
@@ -48,7 +50,7 @@ def main():
     out = torch.empty_like(qd)
     P = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
     lib, h = s.lib, s.h
-    res = {"T": T, "batch": B, "layers": L}
+    res = {"T": T, "batch": B, "layers": L, "hq": Hq, "hkv": Hkv}
     for name, fg in (("fp64_gate", None), ("forced_gate", fz)):
         def step():
             for l in range(L):
