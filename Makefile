@@ -30,5 +30,6 @@ clean:
 # (load with WGKV_LIB=build/var/libwgkv_x.so; not a product artefact)
 variant: $(OBJ)
 	@mkdir -p build/var/$(NAME)
-	$(NVCC) $(NVFLAGS) $(DEFS) -I$(PKG)/csrc -c $(or $(SRCF),$(PKG)/csrc/attn_tc.cu) -o build/var/$(NAME)/attn_tc.o 2> build/var/$(NAME)/ptxas.log || (cat build/var/$(NAME)/ptxas.log; false)
-	$(NVCC) $(ARCH) -shared -o build/var/libwgkv_$(NAME).so $(filter-out build/attn_tc.o,$(OBJ)) build/var/$(NAME)/attn_tc.o -Xcompiler -fPIC
+	$(NVCC) $(NVFLAGS) $(DEFS) -I$(PKG)/csrc -c $(or $(SRCF),$(PKG)/csrc/attn_tc.cu) -o build/var/$(NAME)/$(VOBJ) 2> build/var/$(NAME)/ptxas.log || (cat build/var/$(NAME)/ptxas.log; false)
+	$(NVCC) $(ARCH) -shared -o build/var/libwgkv_$(NAME).so $(filter-out build/$(VOBJ),$(OBJ)) build/var/$(NAME)/$(VOBJ) -Xcompiler -fPIC -ldl
+VOBJ = $(notdir $(patsubst %.cu,%.o,$(or $(SRCF),$(PKG)/csrc/attn_tc.cu)))

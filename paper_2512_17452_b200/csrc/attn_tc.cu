@@ -37,6 +37,11 @@
 #ifndef WGKV_K3_WARP_ISSUE
 #define WGKV_K3_WARP_ISSUE 1
 #endif
+// each 8-MMA group as one asm block (one elect, descriptors advanced by
+// immediates): halves the issue instructions, measured neutral (r2_k3_notes.md)
+#ifndef WGKV_K3_MMA8
+#define WGKV_K3_MMA8 0
+#endif
 // waits with a suspend-time hint (spinning warps give their issue slots to the
 // softmax warps of the same SM sub-partition): bit 0 producers, 1 MMA issuer, 2 softmax
 #ifndef WGKV_K3_SLEEP
@@ -114,6 +119,31 @@ __device__ __forceinline__ float2 ex2_emu2(float x0, float x1) {
     const int r0 = max(__float_as_int(p.x) + (__float_as_int(t.x) << 23), 0);
     const int r1 = max(__float_as_int(p.y) + (__float_as_int(t.y) << 23), 0);
     return make_float2(__int_as_float(r0), __int_as_float(r1));
+}
+
+#ifndef WGKV_EMU_PACK_INT
+#define WGKV_EMU_PACK_INT 0
+#endif
+// emulated pair straight to bf16x2 (no F2FP on the MUFU pipe): the same cubic,
+// the exponent add and a round-half-up bias folded into one IADD3 per value,
+// the two high halves joined by one PRMT.  x is clamped at -126 so the biased
+// exponent never goes negative (masked -inf keys give a ~1e-38 weight, zero at
+// bf16 resolution of any row sum they join).  *s0 / *s1 receive the fp32 values
+// (bias excluded) for the row sum.
+__device__ __forceinline__ uint32_t ex2_emu2_bf16(float x0, float x1, float& s0, float& s1) {
+    const float2 xc = make_float2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+    const float2 big = make_float2(12582912.f, 12582912.f);
+    const float2 t = __fadd2_rn(xc, big);
+    const float2 tb = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(tb, make_float2(-1.f, -1.f), xc);
+    float2 p = __ffma2_rn(f, make_float2(0.05517161f, 0.05517161f), make_float2(0.24261111f, 0.24261111f));
+    p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+    p = __ffma2_rn(p, f, make_float2(0.99992806f, 0.99992806f));
+    const uint32_t e0 = (uint32_t)__float_as_int(t.x) << 23, e1 = (uint32_t)__float_as_int(t.y) << 23;
+    const uint32_t r0 = (uint32_t)__float_as_int(p.x) + e0, r1 = (uint32_t)__float_as_int(p.y) + e1;
+    s0 = __uint_as_float(r0);
+    s1 = __uint_as_float(r1);
+    return __byte_perm(r0 + 0x8000u, r1 + 0x8000u, 0x7632);
 }
 
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_saddr, int kk) {
@@ -278,16 +308,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t qa = sbase + OFF_Q + t * TILE_BYTES;
                 const uint32_t ka = sbase + OFF_KV + st * STAGE_BYTES;
                 const uint32_t d = tmem + 256 * t + 128;
+#if WGKV_K3_MMA8
+                tc::mma8_ss_kmajor_w(d, kmajor_desc(qa, 0), kmajor_desc(ka, 0), idS, 0);
+#else
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) K3_MMA_SS(d, kmajor_desc(qa, kk), kmajor_desc(ka, kk), idS, kk > 0);
+#endif
             };
             auto issue_PV = [&](int t, int st, bool acc) {
                 const uint32_t va = sbase + OFF_KV + st * STAGE_BYTES + TILE_BYTES;
                 const uint32_t d = tmem + 256 * t, pa = tmem + 256 * t + 128;
+#if WGKV_K3_MMA8
+                tc::mma8_ts_vmn_w(d, pa, tc::smem_desc_sw128(va, SUB_BYTES, 1024), idPV, acc ? 1u : 0u);
+#else
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
                     K3_MMA_TS(d, pa + 8 * kk, tc::smem_desc_sw128(va + kk * 2048u, SUB_BYTES, 1024), idPV,
                                (acc || kk > 0) ? 1u : 0u);
+#endif
             };
             tc::mbar_wait(&bar->q_ready, 0);
             tc::mbar_wait(&bar->k_full[0], 0);
@@ -449,6 +487,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const float2 xd = __fadd2_rn(make_float2(__uint_as_float(x[2 * e]), __uint_as_float(x[2 * e + 1])), nmu);
                     // selected pairs on the FMA pipe, the rest on the MUFU
                     float e0, e1;
+                    if (WGKV_EMU_PACK_INT && ((WGKV_EMU_MASK >> e) & 1)) {
+                        pa[off + e] = ex2_emu2_bf16(xd.x, xd.y, e0, e1);
+                        lsv[e & 3] = __fadd2_rn(lsv[e & 3], make_float2(e0, e1));
+                        continue;
+                    }
                     if ((WGKV_EMU_MASK >> e) & 1) {
                         const float2 ee = ex2_emu2(xd.x, xd.y);
                         e0 = ee.x;

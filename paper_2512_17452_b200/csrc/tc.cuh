@@ -213,3 +213,91 @@ int make_tmap_4d_bf16(CUtensorMap* map, const void* base, const uint64_t dims[4]
 int make_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_bytes,
                       uint64_t stride2_bytes, uint32_t box0, uint32_t box1, uint32_t box2);
 }
+
+namespace wgkv {
+namespace tc {
+// One K = 128 group of 8 warp-issued MMAs (K step 16 each) in a single asm
+// block: one elect.sync, descriptors advanced by immediates inside the block
+// (start-address field, units of 16 bytes), so the issue costs ~2 instructions
+// per MMA instead of recomputing and re-broadcasting every operand.
+//   SS: a_desc(kk) = a0 + a_step(kk), b_desc(kk) = b0 + b_step(kk); accumulate from kk > 0 or acc
+//   TS: A from TMEM at a_tmem + 8 kk
+// K-major SW128 [128][64] sub-tile pairs step {0,2,4,6,1024,1026,1028,1030}
+// (32 bytes per k16 inside a 128-byte row, next sub-tile at +16 KB);
+// MN-major V sub-tiles of 16 rows step 128 (2 KB) per k16.
+__device__ __forceinline__ void mma8_ss_kmajor_w(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                                 uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\n.reg .b64 a, b;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "add.s64 a, %1, 2;\n add.s64 b, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 4;\n add.s64 b, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 6;\n add.s64 b, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 1024;\n add.s64 b, %2, 1024;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 1026;\n add.s64 b, %2, 1026;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 1028;\n add.s64 b, %2, 1028;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 1030;\n add.s64 b, %2, 1030;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a0), "l"(b0), "r"(idesc), "r"(acc));
+}
+// TS with B K-major (S = Q K^T, Q in TMEM)
+__device__ __forceinline__ void mma8_ts_kmajor_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b0, uint32_t idesc,
+                                                 uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\n.reg .b64 b;\n.reg .b32 a;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "add.s32 a, %1, 8;\n add.s64 b, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 16;\n add.s64 b, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 24;\n add.s64 b, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 32;\n add.s64 b, %2, 1024;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 40;\n add.s64 b, %2, 1026;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 48;\n add.s64 b, %2, 1028;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 56;\n add.s64 b, %2, 1030;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b0), "r"(idesc), "r"(acc));
+}
+// TS with B MN-major V sub-tiles (O += P V): b_desc(kk) = b0 + 128 kk
+__device__ __forceinline__ void mma8_ts_vmn_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b0, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\n.reg .b64 b;\n.reg .b32 a;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "add.s32 a, %1, 8;\n add.s64 b, %2, 128;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 16;\n add.s64 b, %2, 256;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 24;\n add.s64 b, %2, 384;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 32;\n add.s64 b, %2, 512;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 40;\n add.s64 b, %2, 640;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 48;\n add.s64 b, %2, 768;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 56;\n add.s64 b, %2, 896;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b0), "r"(idesc), "r"(acc));
+}
+}  // namespace tc
+}  // namespace wgkv
