@@ -219,6 +219,17 @@ int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank); /*
 int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank);   /* caller-owned ncclComm_t */
 int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out, void* full_out, int async);
 int wgkv_comm_join(wgkv_ctx* ctx);
+/* ---- f3: output projection overlapped with the head all-gather -----------
+ * Session's x[t] += Wo . concat[t] (engine.cpp:243-245 prefill, :331 decode)
+ * on top of wgkv_allgather_heads: local_out [nseq][T][q_heads][d] (bf16, this
+ * rank's heads), wo [dim][world * q_heads * d] bf16 row-major
+ * (LayerWeights::wo, model.hpp), x [nseq][T][dim] fp32 residual stream,
+ * updated in place.  With a communicator the rows go in chunks: the NCCL
+ * all-gather + assembly of chunk c+1 (comm stream) overlaps the Wo GEMM of
+ * chunk c (cuBLAS, bf16 tensor cores, fp32 accumulation; context stream).
+ * Without one the local heads are the concat and only the GEMM runs.
+ * bf16 contexts only (WGKV_ENOTSUP otherwise). */
+int wgkv_output_proj(wgkv_ctx* ctx, int nseq, long T, const void* local_out, const void* wo, int dim, float* x);
 /* the assembly step alone: rank-major [world][rows][blk_bytes] -> [rows][world * blk_bytes]
  * on `stream` (cudaStream_t); blk_bytes a multiple of 16 */
 int wgkv_assemble_heads(int world, long rows, size_t blk_bytes, const void* rank_major, void* full_out,

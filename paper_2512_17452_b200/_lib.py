@@ -81,6 +81,7 @@ SIGNATURES = {
     "wgkv_comm_attach": ([_vp, _vp, _i, _i], _i),
     "wgkv_allgather_heads": ([_vp, _i, _l, _vp, _vp, _i], _i),
     "wgkv_comm_join": ([_vp], _i),
+    "wgkv_output_proj": ([_vp, _i, _l, _vp, _vp, _i, _vp], _i),
     "wgkv_assemble_heads": ([_i, _l, C.c_size_t, _vp, _vp, _vp], _i),
 }
 

@@ -208,6 +208,18 @@ class Session:
     def comm_join(self):
         check(self.lib.wgkv_comm_join(self.h), "comm_join")
 
+    def output_proj(self, local_out: torch.Tensor, wo: torch.Tensor, x: torch.Tensor):
+        """f3: x += concat . wo^T (engine.cpp:243-245 / :331) where concat is
+        the all-gathered head output; local_out [nseq][T][q_heads][d] (decode:
+        [nseq][q_heads][d]) bf16, wo [dim][world*q_heads*d] bf16, x fp32
+        [nseq][T][dim] updated in place.  The gather of the next row chunk
+        overlaps the GEMM of the current one."""
+        nseq = local_out.shape[0]
+        T = local_out.shape[1] if local_out.dim() == 4 else 1
+        assert wo.dtype == torch.bfloat16 and x.dtype == torch.float32 and x.is_contiguous()
+        check(self.lib.wgkv_output_proj(self.h, nseq, T, _p(local_out), _p(wo), wo.shape[0], _p(x)), "output_proj")
+        return x
+
     def pool_info(self) -> dict:
         v = (C.c_int64 * 2)()
         check(self.lib.wgkv_pool_info(self.h, v), "pool_info")

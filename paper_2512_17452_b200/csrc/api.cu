@@ -17,6 +17,7 @@
 #include "attn.cuh"
 #include "attn_tc.cuh"
 #include "comm.cuh"
+#include "outproj.cuh"
 #include "gate.cuh"
 
 using namespace wgkv;
@@ -235,6 +236,11 @@ struct wgkv_ctx {
     cudaEvent_t ev_comm_in = nullptr, ev_comm_done = nullptr;
     uint8_t* stage = nullptr;  // [world][stage_rows][q_heads * d] elements
     long stage_rows = 0;
+    // f3 (outproj.cu): cuBLAS handle and the two-slot concat ring of the chunked Wo
+    void* blas = nullptr;
+    uint8_t* cring = nullptr;  // [2][cring_rows][world * q_heads * d] elements
+    long cring_rows = 0;
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_gemm[2] = {nullptr, nullptr};
     // host mirrors for lifecycle checks and grid sizing
     std::vector<uint8_t> prefilled;  // [L][S]
     std::vector<long> tokens;        // [L][S] tokens seen
@@ -421,6 +427,12 @@ int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     if (ctx->own_comm) comm_destroy(ctx->comm);
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    blas_destroy(ctx->blas);
+    if (ctx->cring) cudaFree(ctx->cring);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->ev_ready[b]) cudaEventDestroy(ctx->ev_ready[b]);
+        if (ctx->ev_gemm[b]) cudaEventDestroy(ctx->ev_gemm[b]);
+    }
     if (ctx->ev_comm_in) cudaEventDestroy(ctx->ev_comm_in);
     if (ctx->ev_comm_done) cudaEventDestroy(ctx->ev_comm_done);
     for (void* p : ctx->owned) cudaFree(p);
@@ -1022,6 +1034,14 @@ static int comm_setup(wgkv_ctx* ctx, int world, int rank) {
     WGKV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
     WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_comm_in, cudaEventDisableTiming));
     WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_comm_done, cudaEventDisableTiming));
+    // f3: the chunked Wo's concat ring (chunks of <= 1024 rows: a 1024 x 4096 x 4096
+    // GEMM chunk is ~25 us, enough to hide the next chunk's 8 MB exchange)
+    ctx->cring_rows = std::min<long>(ctx->stage_rows, kOutProjChunkRows);
+    WGKV_CUDA_TRY(cudaMalloc(&ctx->cring, 2 * (size_t)ctx->cring_rows * world * c.q_heads * c.head_dim * ctx->esz));
+    for (int b = 0; b < 2; ++b) {
+        WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_ready[b], cudaEventDisableTiming));
+        WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_gemm[b], cudaEventDisableTiming));
+    }
     return WGKV_OK;
 }
 
@@ -1082,6 +1102,46 @@ int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out,
             if (r) return fail(r, err.empty() ? std::string("assemble kernel failed") : err);
         }
     if (async) WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_comm_done, ctx->comm_stream));
+    return WGKV_OK;
+}
+
+int wgkv_output_proj(wgkv_ctx* ctx, int nseq, long T, const void* local_out, const void* wo, int dim, float* x) {
+    if (!ctx || !local_out || !wo || !x) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    const auto& c = ctx->cfg;
+    if (nseq < 1 || T < 1 || dim < 1) return fail(WGKV_EINVAL, "output_proj: empty");
+    if (c.dtype != WGKV_BF16) return fail(WGKV_ENOTSUP, "output_proj: bf16 contexts only");
+    const size_t blk = (size_t)c.q_heads * c.head_dim * ctx->esz;  // one rank's heads of one token
+    const int K = ctx->world * c.q_heads * c.head_dim;               // Session's concat width
+    const long rows = (long)nseq * T;
+    std::string err;
+    int st = blas_handle(&ctx->blas, &err);
+    if (st) return fail(st, "output_proj: " + err);
+    if (!ctx->comm) {  // one device owns every head: local_out is the concat
+        st = gemm_rows_wt(ctx->blas, ctx->stream, rows, dim, K, local_out, wo, x, &err);
+        return st ? fail(st, "output_proj: " + err) : WGKV_OK;
+    }
+    // chunk c: gather + assemble on the comm stream into ring slot c % 2 (after
+    // the GEMM of chunk c - 2 released it), then its GEMM on the compute stream
+    WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_comm_in, ctx->stream));
+    WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_comm_in, 0));
+    const auto* src = static_cast<const uint8_t*>(local_out);
+    const size_t slot = (size_t)ctx->cring_rows * blk * ctx->world;
+    long ci = 0;
+    for (long r0 = 0; r0 < rows; r0 += ctx->cring_rows, ++ci) {
+        const int b = (int)(ci & 1);
+        const long n = std::min(ctx->cring_rows, rows - r0);
+        uint8_t* buf = ctx->cring + b * slot;
+        if (ci >= 2) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_gemm[b], 0));
+        st = comm_allgather_assemble(ctx->comm, src + r0 * blk, ctx->stage, n * blk, buf, n, ctx->world, blk,
+                                     blk * ctx->world, ctx->comm_stream, &err);
+        if (st) return fail(st, err.empty() ? std::string("output_proj: assemble kernel failed") : err);
+        WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_ready[b], ctx->comm_stream));
+        WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_ready[b], 0));
+        st = gemm_rows_wt(ctx->blas, ctx->stream, n, dim, K, buf, wo, x + r0 * dim, &err);
+        if (st) return fail(st, "output_proj: " + err);
+        WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_gemm[b], ctx->stream));
+    }
     return WGKV_OK;
 }
 

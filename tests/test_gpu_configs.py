@@ -453,3 +453,34 @@ def test_comm_world_one(W, orc):
     assert torch.equal(fd, xd)
     with pytest.raises(ValueError):  # rank 1 of 2 must own kv heads [hkv, 2 hkv)
         W.Session(1, hq, hkv, d, d, 64, max_tokens=T).comm_init(W.nccl_unique_id(), 2, 1)
+
+
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_output_proj_overlapped(W, orc, with_comm):
+    """f3 (engine.cpp:243-245): x += concat . Wo^T after the head all-gather.
+    With a communicator the rows go through the chunked gather -> GEMM
+    pipeline (3 chunks of <= 1024 rows here, both ring slots reused); without
+    one the local heads are the concat.  Checked against an fp64 product of the
+    same bf16 operands (fp32 accumulation: 1e-5 of the output scale)."""
+    hq, hkv, d, T, B, dim = 8, 2, 128, 1300, 2, 512
+    s = W.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=T,
+                  gate_bank=orc.gate_random_init(1, hkv, d, d, 3))
+    if with_comm:
+        s.comm_init(W.nccl_unique_id(), 1, 0)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    lo = torch.randn(B, T, hq, d, device="cuda", generator=g).to(torch.bfloat16)
+    wo = (torch.randn(dim, hq * d, device="cuda", generator=g) / (hq * d) ** 0.5).to(torch.bfloat16)
+    x0 = torch.randn(B, T, dim, device="cuda", generator=g)
+    x = x0.clone()
+    s.output_proj(lo, wo, x)
+    s.sync()
+    ref = x0.double() + lo.reshape(B, T, hq * d).double() @ wo.double().T
+    err = (x.double() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
+    # decode shape: one token per sequence
+    xd0 = torch.randn(B, dim, device="cuda", generator=g)
+    xd = xd0.clone()
+    s.output_proj(lo[:, 0].contiguous(), wo, xd)
+    s.sync()
+    refd = xd0.double() + lo[:, 0].reshape(B, hq * d).double() @ wo.double().T
+    assert (xd.double() - refd).abs().max().item() / refd.abs().max().item() < 1e-5
