@@ -125,6 +125,19 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
                     void* k_post_out, float* g_out, uint8_t* bits_out, int64_t* near_idx, int near_cap,
                     int* near_count);
 
+/* f1: wgkv_gate_score with the key projection fused in (engine.cpp:190-205:
+ * k_pre = Wk_h . a, k_post = RoPE(k_pre), gate, binarize): one tcgen05 kernel
+ * projects each 128-token tile into TMEM, rounds it to bf16 and feeds it
+ * straight to the gate GEMM, so k_pre is not re-read from HBM.
+ *   x  [nseq][T][dm]     bf16 layer input (after the RMSNorm, engine.cpp:178-182)
+ *   wk [kv_heads][d][dm] bf16 this context's rows of LayerWeights::wk
+ *   k_pre_out [nseq][T][kv_heads][d] bf16(x . wk^T) (fp32 accumulation) -- the
+ *   k_pre the gate was evaluated on; the rest as wgkv_gate_score.  bf16
+ *   contexts with d = hidden = 128 and dm a multiple of 64 (WGKV_ENOTSUP). */
+int wgkv_gate_score_proj(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const void* x, const void* wk, int dm,
+                         void* k_pre_out, void* k_post_out, float* g_out, uint8_t* bits_out, int64_t* near_idx,
+                         int near_cap, int* near_count);
+
 /* ---- K2: HeadCache::prefill_populate (kvstore.cpp:160-203) ---------------
  * Warp-scan compaction: admitted rows j < T-W appended to the paged Global
  * cache in ascending order, rows [T-W, T) into the Local ring slots 0.. .

@@ -62,6 +62,7 @@ SIGNATURES = {
     "wgkv_gate_set": ([_vp, _vp, _i, _i], _i),
     "wgkv_gate_load": ([_vp, C.c_char_p], _i),
     "wgkv_gate_score": ([_vp, _i, _i, _l, _l, _vp, _vp, _vp, _vp, _vp, _vp, _i, C.POINTER(_i)], _i),
+    "wgkv_gate_score_proj": ([_vp, _i, _i, _l, _l, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, C.POINTER(_i)], _i),
     "wgkv_admit_prefill": ([_vp, _i, _i, _i, _l, _vp, _vp, _vp, _vp], _i),
     "wgkv_vs_prefill": ([_vp, _i, _i, _i, _l, _vp, _vp, _vp, _vp, _vp], _i),
     "wgkv_prefill_layer": ([_vp, _i, _i, _i, _l, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),

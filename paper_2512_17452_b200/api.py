@@ -110,6 +110,23 @@ class Session:
                                        _p(bits), _p(near), near.numel(), C.byref(n)), "gate_forward_batch")
         return k_post, g, bits, near[: min(n.value, near.numel())].cpu().numpy()
 
+    def gate_forward_batch_proj(self, layer: int, x: torch.Tensor, wk: torch.Tensor, pos0: int = 0):
+        """f1 (engine.cpp:190-205): x [nseq][T][dm] layer input, wk [kv_heads][d][dm]
+        (this context's Wk rows), bf16 -> (k_pre = bf16(x . wk^T), k_post, g, bits,
+        near flat indices); the projection is fused into the gate kernel."""
+        nseq, T, dm = x.shape
+        H, d = self.cfg.kv_heads, self.cfg.head_dim
+        k_pre = torch.empty((nseq, T, H, d), dtype=torch.bfloat16, device=self.device)
+        k_post = torch.empty_like(k_pre)
+        g = torch.empty((nseq, H, T), dtype=torch.float32, device=self.device)
+        bits = torch.empty((nseq, H, T), dtype=torch.uint8, device=self.device)
+        near = torch.empty(1 << 16, dtype=torch.int64, device=self.device)
+        n = C.c_int(0)
+        check(self.lib.wgkv_gate_score_proj(self.h, layer, nseq, T, pos0, _p(x), _p(wk), dm, _p(k_pre), _p(k_post),
+                                            _p(g), _p(bits), _p(near), near.numel(), C.byref(n)),
+              "gate_forward_batch_proj")
+        return k_pre, k_post, g, bits, near[: min(n.value, near.numel())].cpu().numpy()
+
     # ---- prefill -----------------------------------------------------------
     def prefill_layer(self, layer, q, k_pre, v, seq0=0, forced_gates=None, out=None, want_gates=False):
         """q [nseq][T][q_heads][d], k_pre/v [nseq][T][kv_heads][d] (device, dtype)."""

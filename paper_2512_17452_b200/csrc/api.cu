@@ -604,6 +604,38 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
     return WGKV_OK;
 }
 
+int wgkv_gate_score_proj(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const void* x, const void* wk, int dm,
+                         void* k_pre_out, void* k_post_out, float* g_out, uint8_t* bits_out, int64_t* near_idx,
+                         int near_cap, int* near_count) {
+    if (!ctx || !x || !wk || !k_pre_out || !k_post_out || !g_out || !bits_out) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    int st = check_slots(ctx, layer, 0, nseq, T);
+    if (st) return st;
+    if (!ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
+    if (ctx->cfg.dtype != WGKV_BF16 || !ctx->w1split)
+        return fail(WGKV_ENOTSUP, "gate_score_proj: bf16 contexts with d = hidden = 128 only");
+    if (dm < 64 || dm % 64 != 0) return fail(WGKV_ENOTSUP, "gate_score_proj: model dim must be a multiple of 64");
+    if (T == 0) return WGKV_OK;
+    GateArgs a = ctx->gate_args(layer, T, pos0);
+    int64_t* nidx = near_idx ? near_idx : ctx->ws_near;
+    const int ncap = near_idx ? near_cap : (int)ctx->near_cap;
+    WGKV_CUDA_TRY(cudaMemsetAsync(ctx->ws_cnt + 1, 0, sizeof(int), ctx->stream));
+    WGKV_CUDA_TRY(cudaMemsetAsync(ctx->ws_pcnt, 0, sizeof(int) * nseq * ctx->cfg.kv_heads, ctx->stream));
+    st = launch_gate_proj_tc(a, nseq, (const __nv_bfloat16*)x, (const __nv_bfloat16*)wk, dm, (__nv_bfloat16*)k_pre_out,
+                             (__nv_bfloat16*)k_post_out, g_out, bits_out, (int32_t*)ctx->ws_cand, ctx->ws_pcnt,
+                             ctx->w1split, (long)ctx->cfg.layers * ctx->cfg.kv_heads * 4, ctx->ws_rope, ctx->stream);
+    if (!st)
+        st = launch_gate_recheck<__nv_bfloat16>(a, nseq, (const __nv_bfloat16*)k_pre_out, g_out, bits_out,
+                                                (int32_t*)ctx->ws_cand, ctx->ws_pcnt, nidx, ncap, ctx->ws_cnt + 1,
+                                                ctx->stream);
+    if (st) return fail(st, std::string("gate_proj kernels: ") + cudaGetErrorString(cudaGetLastError()));
+    if (near_count) {
+        WGKV_CUDA_TRY(cudaMemcpyAsync(near_count, ctx->ws_cnt + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    return WGKV_OK;
+}
+
 int wgkv_admit_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const void* k_post, const void* v,
                        const float* g, const uint8_t* bits) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");

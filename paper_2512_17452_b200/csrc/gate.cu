@@ -370,6 +370,14 @@ int launch_gate_prefill(const GateArgs& a, int nseq, const T* k_pre, T* k_post, 
         dim3 grid((unsigned)((a.T + GT_TOK - 1) / GT_TOK), a.kv_heads, nseq);
         gate_prefill_kernel<T><<<grid, 256, smem, st>>>(a, k_pre, k_post, g, bits, cand, pcnt);
     }
+    return launch_gate_recheck<T>(a, nseq, k_pre, g, bits, cand, pcnt, near_idx, near_cap, near_cnt, st);
+}
+
+// the fp64 recheck of the listed tokens (reference operation order), bits overwritten
+template <typename T>
+int launch_gate_recheck(const GateArgs& a, int nseq, const T* k_pre, float* g, uint8_t* bits, int32_t* cand,
+                        int* pcnt, int64_t* near_idx, int near_cap, int* near_cnt, cudaStream_t st) {
+    const int npairs = nseq * a.kv_heads;
     if (a.d == 128 && a.hidden == 128) {
         if (ensure_smem(gate_recheck_gemm_kernel<T>, RC_SMEM) != cudaSuccess) return WGKV_ECUDA;
         gate_recheck_gemm_kernel<T><<<num_sms(), 256, RC_SMEM, st>>>(a, npairs, k_pre, g, bits, cand, pcnt, near_idx,
@@ -421,6 +429,8 @@ int launch_forced_gate(const GateArgs& a, int nseq, const void* k_pre, void* k_p
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
+template int launch_gate_recheck<__nv_bfloat16>(const GateArgs&, int, const __nv_bfloat16*, float*, uint8_t*,
+                                                int32_t*, int*, int64_t*, int, int*, cudaStream_t);
 template int launch_gate_prefill<float>(const GateArgs&, int, const float*, float*, float*, uint8_t*, int32_t*, int*,
                                         int64_t*, int, int*, const __nv_bfloat16*, long, float2*, cudaStream_t);
 template int launch_gate_prefill<__nv_bfloat16>(const GateArgs&, int, const __nv_bfloat16*, __nv_bfloat16*, float*,

@@ -152,4 +152,15 @@ int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv
                    uint8_t* bits, int32_t* cand, int* pcnt, const __nv_bfloat16* w1split, long n_wtiles,
                    float2* rope_ws, cudaStream_t st);
 
+// cos/sin table of one call's positions (gate_tc.cu), [T][d/2] float2
+void launch_rope_table(const double* freq, long pos0, long T, int hp, float2* out, cudaStream_t st);
+// f1 (gate_proj.cu): the key projection fused into K1 -- x [nseq][T][dm], wk [kv_heads][128][dm]
+// bf16; writes k_pre (bf16 of the fp32 projection), k_post, g, bits and the recheck list
+int launch_gate_proj_tc(const GateArgs& a, int nseq, const __nv_bfloat16* x, const __nv_bfloat16* wk, int dm,
+                        __nv_bfloat16* k_pre, __nv_bfloat16* k_post, float* g, uint8_t* bits, int32_t* cand, int* pcnt,
+                        const __nv_bfloat16* w1split, long n_wtiles, float2* rope_ws, cudaStream_t st);
+template <typename T>
+int launch_gate_recheck(const GateArgs& a, int nseq, const T* k_pre, float* g, uint8_t* bits, int32_t* cand,
+                        int* pcnt, int64_t* near_idx, int near_cap, int* near_cnt, cudaStream_t st);
+
 }  // namespace wgkv

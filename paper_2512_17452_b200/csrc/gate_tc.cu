@@ -359,6 +359,10 @@ __global__ void rope_table_kernel(const double* __restrict__ freq, long pos0, lo
     }
 }
 
+void launch_rope_table(const double* freq, long pos0, long T, int hp, float2* out, cudaStream_t st) {
+    rope_table_kernel<<<num_sms() * 8, 256, 0, st>>>(freq, pos0, T, hp, out);
+}
+
 int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv_bfloat16* k_post, float* g,
                    uint8_t* bits, int32_t* cand, int* pcnt, const __nv_bfloat16* w1split, long n_wtiles,
                    float2* rope_ws, cudaStream_t st) {

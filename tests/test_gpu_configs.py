@@ -484,3 +484,37 @@ def test_output_proj_overlapped(W, orc, with_comm):
     s.sync()
     refd = xd0.double() + lo[:, 0].reshape(B, hq * d).double() @ wo.double().T
     assert (xd.double() - refd).abs().max().item() / refd.abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("dm,T", [(512, 700), (4096, 300)])
+def test_gate_proj_fused(W, orc, dm, T):
+    """f1 (engine.cpp:190-205): the key projection fused into K1.  k_pre must be
+    the bf16 rounding of x . Wk^T (fp32 accumulation may land a value on the
+    other side of a bf16 rounding boundary: at most one ulp, rarely), and given
+    that k_pre, k_post / g / bits / near list must be exactly what K1
+    (wgkv_gate_score, itself pinned to the oracle) produces."""
+    hq, hkv, d, B = 8, 2, 128, 2
+    bank = orc.gate_random_init(1, hkv, d, d, 17, 0.1, -2.2)
+    s = W.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=T, rope_base=5e5, gate_bank=bank)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(B, T, dm, device="cuda", generator=g).to(torch.bfloat16)
+    wk = (torch.randn(hkv, d, dm, device="cuda", generator=g) / dm ** 0.5).to(torch.bfloat16)
+    k_pre, k_post, gg, bits, near = s.gate_forward_batch_proj(0, x, wk, pos0=5)
+    s.sync()
+    ref = torch.einsum("btk,hdk->bthd", x.double(), wk.double())
+    ref_bf = ref.to(torch.bfloat16)
+    diff = k_pre != ref_bf
+    frac = diff.float().mean().item()
+    assert frac < 1e-2, frac  # grows with dm (fp32 accumulation error vs a bf16 ulp)
+    if diff.any():  # only rounding-boundary cases: one bf16 ulp plus the fp32 accumulation error
+        kd, rd = k_pre[diff].double(), ref[diff]
+        mag = torch.einsum("btk,hdk->bthd", x.double().abs(), wk.double().abs())[diff]
+        assert ((kd - rd).abs() <= rd.abs() * 2.0 ** -7 + 2 * dm * 2.0 ** -24 * mag).all()
+    k_post2, g2, bits2, near2 = s.gate_forward_batch(0, k_pre, pos0=5)
+    s.sync()
+    assert torch.equal(k_post, k_post2)
+    assert torch.equal(bits, bits2)
+    assert torch.equal(gg, g2)
+    assert sorted(near.tolist()) == sorted(near2.tolist())
+    print(f"gate_proj dm={dm}: {frac:.2e} of k_pre on the other side of a bf16 rounding boundary, "
+          f"{int(bits.sum())} admitted")
