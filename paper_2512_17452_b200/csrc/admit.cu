@@ -225,28 +225,35 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 // ---------------------------------------------------------------------------
 // K4 standalone: the split append's route + gate CTAs (append.cuh)
 // ---------------------------------------------------------------------------
+// mode 0: route + gate CTAs in one launch; 1: route CTAs only (the gate CTAs
+// follow in a mode-2 launch on a side stream, overlapping the attention)
 template <typename E>
 __global__ void __launch_bounds__(kAppendThreads) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
                                                                         long W, int npairs,
                                                                         const E* __restrict__ k_pre,
                                                                         const E* __restrict__ v,
                                                                         const float* __restrict__ forced_g,
-                                                                        DecodeTrace tr, AppendWork wk) {
+                                                                        DecodeTrace tr, AppendWork wk, int mode) {
     extern __shared__ __align__(16) uint8_t append_smem[];
     const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
-    append_role<E>(pv, ga, layer, seq0, W, npairs, blockIdx.x, gpp, gpp + 1, k_pre, v, forced_g, tr, wk, append_smem);
+    const int r = mode == 2 ? npairs + (int)blockIdx.x : (int)blockIdx.x;
+    append_role<E>(pv, ga, layer, seq0, W, npairs, r, gpp, gpp + 1, k_pre, v, forced_g, tr, wk, append_smem);
 }
 
 template <typename E>
 int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int nseq, long W,
                          const E* k_pre, const E* v, const float* forced_g, const DecodeTrace& tr,
-                         const AppendWork& wk, cudaStream_t st) {
+                         const AppendWork& wk0, cudaStream_t st, int mode) {
     const size_t smem = append_smem_bytes(pv.head_dim, ga.hidden);
     if (ensure_smem(decode_append_kernel<E>, smem) != cudaSuccess) return WGKV_ECUDA;
     const int npairs = nseq * pv.kv_heads;
-    const int grid = npairs * (1 + (forced_g ? 0 : gate_ctas_per_pair(ga.hidden)));
-    decode_append_kernel<E><<<grid, kAppendThreads, smem, st>>>(pv, ga, layer, seq0, W, npairs, k_pre, v, forced_g,
-                                                                 tr, wk);
+    const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
+    AppendWork wk = wk0;
+    wk.early_state = mode != 0;
+    const int grid = mode == 0 ? npairs * (1 + gpp) : (mode == 1 ? npairs : npairs * gpp);
+    if (grid > 0)
+        decode_append_kernel<E><<<grid, kAppendThreads, smem, st>>>(pv, ga, layer, seq0, W, npairs, k_pre, v, forced_g,
+                                                                     tr, wk, mode);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
@@ -254,7 +261,7 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     template int launch_admit_prefill<E>(const PoolView&, int, int, int, long, long, const E*, const E*,          \
                                          const float*, const uint8_t*, int32_t*, cudaStream_t);                   \
     template int launch_decode_append<E>(const PoolView&, const GateArgs&, int, int, int, long, const E*, const E*, \
-                                         const float*, const DecodeTrace&, const AppendWork&, cudaStream_t);
+                                         const float*, const DecodeTrace&, const AppendWork&, cudaStream_t, int);
 INST(float)
 INST(__nv_bfloat16)
 #undef INST

@@ -218,6 +218,11 @@ struct wgkv_ctx {
     int* ws_nchunks = nullptr;
     int* ws_tokpos = nullptr;  // [S*H] the new token's position per (seq, kv head) (deferred append)
     AppendWork wk{};           // split-append scratch (append.cuh)
+    // non-deferred decode: the append's gate CTAs run on gate_stream, forked after
+    // the route kernel and joined after the attention of the same layer call
+    cudaStream_t gate_stream = nullptr;
+    cudaEvent_t ev_route = nullptr, ev_gate = nullptr;
+    bool gate_join = false;
     float* ws_score = nullptr;  // K6: [S][Hq][n_gp] page scores
     int32_t* ws_sel = nullptr;  // K6: [S][Hq][n_gp] selected logical pages
     int32_t* ws_nsel = nullptr; // K6: [S][Hq]
@@ -375,6 +380,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->wk.slot = dalloc<int>((size_t)S * H, o);
     ctx->wk.event = dalloc<int>((size_t)S * H, o);
     ctx->wk.next = dalloc<HeadState>((size_t)S * H, o);
+    ctx->wk.pos = dalloc<int>((size_t)S * H, o);
     if (c.topk_budget > 0) {
         ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
         ctx->ws_sel = dalloc<int32_t>((size_t)S * c.q_heads * n_gp, o);
@@ -427,6 +433,9 @@ int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     if (ctx->own_comm) comm_destroy(ctx->comm);
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->gate_stream) cudaStreamDestroy(ctx->gate_stream);
+    if (ctx->ev_route) cudaEventDestroy(ctx->ev_route);
+    if (ctx->ev_gate) cudaEventDestroy(ctx->ev_gate);
     blas_destroy(ctx->blas);
     if (ctx->cring) cudaFree(ctx->cring);
     for (int b = 0; b < 2; ++b) {
@@ -727,8 +736,11 @@ static int decode_check(wgkv_ctx* ctx, int layer, int seq0, int nseq) {
     return WGKV_OK;
 }
 
+// split = true (decode_layer, non-deferred path): the route CTAs on the context
+// stream, the gate CTAs forked onto gate_stream -- their g / bit is consumed
+// only when the token leaves the ring -- and joined after the layer's attention
 static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* k_pre, const void* v,
-                              const float* forced_g, const DecodeTrace& tr) {
+                              const float* forced_g, const DecodeTrace& tr, bool split = false) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
     int st = decode_check(ctx, layer, seq0, nseq);
@@ -737,14 +749,34 @@ static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, cons
         if (ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] >= ctx->cfg.max_tokens)
             return fail(WGKV_EINVAL, "sequence exceeds max_tokens");
     if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
+    static const bool no_split = getenv("WGKV_APPEND_NOSPLIT") != nullptr;  // A/B switch
+    split = split && !forced_g && !no_split;
+    if (split && !ctx->gate_stream) {
+        WGKV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->gate_stream, cudaStreamNonBlocking));
+        WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_route, cudaEventDisableTiming));
+        WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_gate, cudaEventDisableTiming));
+    }
     GateArgs ga = ctx->gate_args(layer, 1, 0);
-    if (ctx->cfg.dtype == WGKV_BF16)
-        st = launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
-                                                 (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v, forced_g, tr,
-                                                 ctx->wk, ctx->stream);
-    else
-        st = launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
-                                         (const float*)v, forced_g, tr, ctx->wk, ctx->stream);
+    auto launch = [&](cudaStream_t sm, int mode) {
+        if (ctx->cfg.dtype == WGKV_BF16)
+            return launch_decode_append<__nv_bfloat16>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window,
+                                                       (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v,
+                                                       forced_g, tr, ctx->wk, sm, mode);
+        return launch_decode_append<float>(ctx->pv, ga, layer, seq0, nseq, ctx->cfg.window, (const float*)k_pre,
+                                           (const float*)v, forced_g, tr, ctx->wk, sm, mode);
+    };
+    if (split) {
+        st = launch(ctx->stream, 1);
+        if (!st) {
+            WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_route, ctx->stream));
+            WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->gate_stream, ctx->ev_route, 0));
+            st = launch(ctx->gate_stream, 2);
+            WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_gate, ctx->gate_stream));
+            ctx->gate_join = true;
+        }
+    } else {
+        st = launch(ctx->stream, 0);
+    }
     if (st) return fail(st, "decode append kernel failed");
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
     return WGKV_OK;
@@ -847,9 +879,14 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     DecodeTrace tr{};
     if (trace) tr = DecodeTrace{trace->g, trace->bits, trace->near_tau, trace->events};
     if (!defer_append(ctx->cfg)) {
-        int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, tr);
+        int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, tr, true);
         if (st) return st;
-        return decode_attn_impl(ctx, layer, seq0, nseq, q, out, nullptr);
+        st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, nullptr);
+        if (ctx->gate_join) {  // the append's gate CTAs ran beside the attention
+            WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_gate, 0));
+            ctx->gate_join = false;
+        }
+        return st;
     }
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;

@@ -41,6 +41,11 @@ struct AppendWork {
     int* slot;           // new token's pool slot (page * ps + slot) or -1
     int* event;          // promotion event (0 none, 1 promoted, 2 dropped, -1 failed)
     HeadState* next;     // the state after the append, published by the last arrival
+    int* pos;            // the new token's position (split launch: route kernel -> gate kernel)
+    // split launch (route CTAs, then the gate CTAs in a kernel on a side stream
+    // that overlaps the attention): the route CTA publishes the head state
+    // itself -- the attention reads it -- and leaves the position in `pos`
+    int early_state;
 };
 
 constexpr int kAppendThreads = 256;
@@ -76,7 +81,7 @@ __device__ __forceinline__ void append_finalize(const PoolView& pv, const GateAr
         pv.gate[sl] = (float)g;
         pv.adm[sl] = bit;
     }
-    if (ev >= 0) pv.state[pv.head_index(layer, seq0 + s, h)] = wk.next[pair];
+    if (ev >= 0 && !wk.early_state) pv.state[pv.head_index(layer, seq0 + s, h)] = wk.next[pair];
     const size_t o = (size_t)s * pv.kv_heads + h;
     if (tr.g) tr.g[o] = (float)g;
     if (tr.bits) tr.bits[o] = bit;
@@ -102,9 +107,15 @@ __device__ __forceinline__ void append_arrive(const PoolView& pv, const GateArgs
 // route CTA: RoPE, lazy promotion, ring write (no gate)
 // ---------------------------------------------------------------------------
 template <typename E>
+// pdl_wait (the decode finish kernel, a programmatic dependent of K5): every
+// read, the routing decision, page pops, page-table and metadata writes happen
+// before griddepcontrol.wait -- K5 reads none of them (new pages lie past the
+// attended ones; a promoted victim lands past the tail page's valid rows) --
+// and only the K/V stores into the victim's ring slot, which K5 is streaming,
+// wait for K5 to complete.
 __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s, int h,
                                              long W, const E* __restrict__ k_pre, const E* __restrict__ v,
-                                             const AppendWork& wk) {
+                                             const AppendWork& wk, bool pdl_wait = false) {
     const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
     const long hidx = pv.head_index(layer, seq0 + s, h);
     const int pair = (seq0 + s) * pv.kv_heads + h;
@@ -191,6 +202,10 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
         nslot = slot % ps;
         wk.next[pair] = ns;
         wk.event[pair] = ev;
+        if (wk.early_state) {
+            wk.pos[pair] = (int)pos;
+            if (ev >= 0) pv.state[hidx] = ns;
+        }
         wk.slot[pair] = lp >= 0 ? lp * ps + slot % ps : -1;
         if (ev == 1) {  // the victim's metadata, read before the new token overwrites the slot
             const size_t a = (size_t)vp * ps + slot % ps, b = (size_t)gp * ps + gs_;
@@ -201,6 +216,7 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
         if (lp >= 0) pv.pos[(size_t)lp * ps + slot % ps] = (int32_t)pos;
     }
     __syncthreads();
+    if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     // promote the victim (K/V fetched above), then the new token into the ring
     if (event == 1 && et) {
         E* kd = pool + (size_t)gpage * pv.page_elems() + (size_t)gslot * d;
@@ -248,7 +264,8 @@ __device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateA
     }
     if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     // the state is published only by the pair's last arrival: tokens_seen is the new token's position
-    const long pos = pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
+    // (split launch: the route CTA published it already and left the position in wk.pos)
+    const long pos = wk.early_state ? (long)wk.pos[pair] : pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
     const size_t in = ((size_t)s * pv.kv_heads + h) * d;
     // the feature in the reference's arithmetic (numerics.cpp:53-62)
     for (int i = tid; i < d / 2; i += blockDim.x) {
@@ -277,7 +294,8 @@ template <typename E>
 __device__ __forceinline__ void append_role(const PoolView& pv, const GateArgs& ga, int layer, int seq0, long W,
                                             int npairs, int r, int gpp, int arrivals, const E* __restrict__ k_pre,
                                             const E* __restrict__ v, const float* __restrict__ forced_g,
-                                            const DecodeTrace& tr, const AppendWork& wk, uint8_t* smem) {
+                                            const DecodeTrace& tr, const AppendWork& wk, uint8_t* smem,
+                                            bool pdl_wait = false) {
     int pr, j = -1;
     if (r < npairs) {
         pr = r;
@@ -287,7 +305,7 @@ __device__ __forceinline__ void append_role(const PoolView& pv, const GateArgs& 
     }
     const int s = pr / pv.kv_heads, h = pr % pv.kv_heads;
     if (j < 0)
-        append_route<E>(pv, ga, layer, seq0, s, h, W, k_pre, v, wk);
+        append_route<E>(pv, ga, layer, seq0, s, h, W, k_pre, v, wk, pdl_wait);
     else
         append_gate_part<E>(pv, ga, layer, seq0, s, h, j, k_pre, wk, smem);
     append_arrive(pv, ga, layer, seq0, s, h, forced_g, tr, wk, arrivals);

@@ -21,6 +21,7 @@ constexpr int kMaxChunks = 512;
 // K5 pages per work item (staged page ids); max_tokens per head is bounded by
 // kMaxChunks * kDecPidCap pages (checked at context creation)
 constexpr int kDecPidCap = 2048;
+constexpr int kDecSmemStatePairs = 512;  // K5 caches per-pair head state in smem up to this many pairs
 
 struct DecArgs {
     PoolView pv;
@@ -49,6 +50,7 @@ struct DecArgs {
     // path; the K5 work CTAs follow them
     int n_gate_ctas;
     int early_trigger;  // K5 releases its programmatic dependent right after its PDL wait
+    int state_in_smem;  // K5 keeps every pair's HeadState in shared memory (fits for <= kDecSmemStatePairs)
 };
 
 // K6: select_topk_pages + per-q-head attention over the selection (topk.cu).

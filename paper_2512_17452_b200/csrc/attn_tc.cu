@@ -79,6 +79,14 @@ struct Bars {
     int C;
 };
 
+#ifndef WGKV_K3_MAX3
+#define WGKV_K3_MAX3 0
+#endif
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -449,6 +457,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     cut(s1, 2 * c + 1);
                 }
             }
+#if WGKV_K3_MAX3
+            // three-input FMNMX3: 32 instead of 64 max instructions per row half
+            float pm[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pm[e] = max3f(__uint_as_float(s0[e]), __uint_as_float(s0[e + 8]), __uint_as_float(s0[e + 16]));
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pm[e] = max3f(pm[e], __uint_as_float(s0[e + 24]), __uint_as_float(s1[e]));
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pm[e] = max3f(pm[e], __uint_as_float(s1[e + 8]), __uint_as_float(s1[e + 16]));
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pm[e] = fmaxf(pm[e], __uint_as_float(s1[e + 24]));
+            float mx = max3f(max3f(pm[0], pm[1], pm[2]), max3f(pm[3], pm[4], pm[5]), fmaxf(pm[6], pm[7]));
+#else
             float pm[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
             auto rmax = [&](const uint32_t(&x)[32]) {
 #pragma unroll
@@ -458,6 +479,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             rmax(s1);
             float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                              fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+#endif
             // both halves hold their S in registers past this barrier, so the
             // P stores below may overwrite any S column
             if (lane == 0 && c == 0 && wq == 0) K3_TR(t, j, 1);

@@ -41,11 +41,10 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, arrivals);
         return;
     }
-    // K5 has finished: partials written, the ring's victim slots read
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     if ((int)blockIdx.x >= ngate + ncomb) {  // ---- route CTAs of the append (K4, append.cuh)
+        // reads and routing run while K5 streams; the ring-slot stores wait for it
         append_role<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, a.window, a.n_pairs, blockIdx.x - ngate - ncomb,
-                                   0, arrivals, fin.k_new, fin.v_new, fin.forced_g, fin.tr, fin.wk, fsm);
+                                   0, arrivals, fin.k_new, fin.v_new, fin.forced_g, fin.tr, fin.wk, fsm, true);
         return;
     }
     // ---- combine role: one (seq, q head) --------------------------------------
@@ -60,6 +59,8 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     float* wm = reinterpret_cast<float*>(fsm);  // [NW]
     float* wl = wm + NW;                         // [NW]
     float* wacc = wl + NW;                       // [NW][d]
+    // K5 has finished: partials written
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (sp == 0 && tid == 0) *a.counter = 0;  // K5's work counter, for the next launch
     const int nch = min(a.nchunks[bh], kMaxChunks);
     float m = -INFINITY, l = 0.f;
@@ -90,7 +91,9 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     }
     if (warp == NW - 1) {
         // the new token at its position: logit = RoPE(q) . bf16(RoPE(k)) / sqrt(d)
-        // (the key as it will be cached), weight on v
+        // (the key as it will be cached), weight on v.  (Not hoisted above the
+        // wait: tokpos comes from K5, and the head state may already hold the
+        // next position once this kernel's append has finalised.)
         const long pos = a.tokpos[bh];
         const size_t qo = ((size_t)s * a.q_heads + p) * d, ko = ((size_t)s * a.pv.kv_heads + h) * d;
         float dotp = 0.f;
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
             float q0, q1, k0, k1;
             rope_pair_f32(__bfloat162float(q[qo + 2 * i]), __bfloat162float(q[qo + 2 * i + 1]), c, sn, q0, q1);
             rope_pair_f32(__bfloat162float(fin.k_new[ko + 2 * i]), __bfloat162float(fin.k_new[ko + 2 * i + 1]), c, sn,
-                      k0, k1);
+                          k0, k1);
             k0 = __bfloat162float(__float2bfloat16_rn(k0));
             k1 = __bfloat162float(__float2bfloat16_rn(k1));
             dotp = fmaf(q0, k0, fmaf(q1, k1, dotp));

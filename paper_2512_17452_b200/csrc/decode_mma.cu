@@ -128,6 +128,9 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     float* red = reinterpret_cast<float*>(ring);  // [DW][16][d + 2], aliases the idle ring at merge time
     int* item_base = reinterpret_cast<int*>(full + DW * DNS);                              // [npairs + 1]
     int* pids = item_base + npairs + 1;                                                    // [PID_CAP]
+    // per-pair head state, loaded once by the planning pass (an item then needs
+    // no dependent global round trip before its page ids)
+    HeadState* sst = reinterpret_cast<HeadState*>(pids + PID_CAP);                         // [npairs]
     __shared__ int s_cp, s_items;
 
     // ---- device-side split: uniform chunk size from the actual page counts --
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         int npmax = 0;
         for (int p = p0; p < p1; ++p) {
             const HeadState st = a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)];
+            if (a.state_in_smem) sst[p] = st;
             const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
             const int np = ngv + (st.local_len + ps - 1) / ps;
             item_base[p] = np;
@@ -214,8 +218,10 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     uint32_t kq = 0;  // pages this warp has issued / consumed so far (ring position + parity)
 
     __shared__ int s_item;
-    for (;;) {
-        if (tid == 0) s_item = atomicAdd(work_counter, 1);
+    // first item static (kcta): no atomic round trip in front of it; later items
+    // are stolen from kgrid on (the merging kernel resets the counter to 0)
+    for (int first = 1;; first = 0) {
+        if (tid == 0) s_item = first ? kcta : kgrid + atomicAdd(work_counter, 1);
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) break;
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         const int chunk = item - item_base[bh];
         const int s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
         const long hidx = a.pv.head_index(a.layer, a.seq0 + s, h);
-        const HeadState st = a.pv.state[hidx];
+        const HeadState st = a.state_in_smem ? sst[bh] : a.pv.state[hidx];
         // the query's position: after the append (K4 ran first) or, deferred, the
         // token about to be appended
         const long pos = (!TOPK && a.defer) ? st.tokens_seen : st.tokens_seen - 1;
@@ -476,8 +482,9 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         tp_cap = a.pv.capacity;
     }
     a.n_pairs = nseq * a.pv.kv_heads;
-    const size_t smem =
-        1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
+    a.state_in_smem = a.n_pairs <= kDecSmemStatePairs;
+    const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) +
+                        4 * PID_CAP + (a.state_in_smem ? sizeof(HeadState) * (size_t)a.n_pairs : 0);
     if (smem > (size_t)(228 / CPS - 1) * 1024) return WGKV_ENOTSUP;
     const bool topk = a.sel != nullptr;
     auto kern = topk ? decode_attn_mma_kernel<true> : decode_attn_mma_kernel<false>;
