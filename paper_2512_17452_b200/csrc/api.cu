@@ -223,6 +223,11 @@ struct wgkv_ctx {
     cudaStream_t gate_stream = nullptr;
     cudaEvent_t ev_route = nullptr, ev_gate = nullptr;
     bool gate_join = false;
+    // K5's work before its PDL wait is only safe when the kernel in front of it
+    // is the finish kernel of ANOTHER layer: every API call bumps api_gen, and
+    // a deferred decode_layer records its own generation and layer when done
+    uint64_t api_gen = 0, finish_gen = 0;
+    int finish_layer = -1;
     float* ws_score = nullptr;  // K6: [S][Hq][n_gp] page scores
     int32_t* ws_sel = nullptr;  // K6: [S][Hq][n_gp] selected logical pages
     int32_t* ws_nsel = nullptr; // K6: [S][Hq]
@@ -429,6 +434,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
 int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     if (!ctx) return WGKV_OK;
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     cudaDeviceSynchronize();
     if (ctx->own_comm) comm_destroy(ctx->comm);
     if (ctx->stage) cudaFree(ctx->stage);
@@ -452,6 +458,7 @@ int wgkv_ctx_destroy(wgkv_ctx* ctx) {
 int wgkv_set_stream(wgkv_ctx* ctx, void* stream) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     ctx->stream = static_cast<cudaStream_t>(stream);
     return WGKV_OK;
 }
@@ -459,6 +466,7 @@ int wgkv_set_stream(wgkv_ctx* ctx, void* stream) {
 int wgkv_sync(wgkv_ctx* ctx) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     int32_t err = 0;
     WGKV_CUDA_TRY(cudaMemcpy(&err, ctx->pv.err, sizeof(err), cudaMemcpyDeviceToHost));
@@ -475,6 +483,7 @@ int wgkv_sync(wgkv_ctx* ctx) {
 int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_heads) {
     if (!ctx || !bank) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (bank_layers != c.layers || bank_heads < c.kv_head_offset + c.kv_heads)
         return fail(WGKV_EINVAL, "Session: gate bank shape does not match model");
@@ -550,6 +559,7 @@ int wgkv_gate_set(wgkv_ctx* ctx, const double* bank, int bank_layers, int bank_h
 int wgkv_gate_load(wgkv_ctx* ctx, const char* path) {
     if (!ctx || !path) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     std::ifstream is(path, std::ios::binary);
     if (!is) return fail(WGKV_ERUNTIME, std::string("GateBank::load: cannot open ") + path);
     char magic[4];
@@ -582,6 +592,7 @@ int wgkv_gate_score(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, const
                     int* near_count) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = check_slots(ctx, layer, 0, nseq, T);
     if (st) return st;
     if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
@@ -618,6 +629,7 @@ int wgkv_gate_score_proj(wgkv_ctx* ctx, int layer, int nseq, long T, long pos0, 
                          int near_cap, int* near_count) {
     if (!ctx || !x || !wk || !k_pre_out || !k_post_out || !g_out || !bits_out) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = check_slots(ctx, layer, 0, nseq, T);
     if (st) return st;
     if (!ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
@@ -649,6 +661,7 @@ int wgkv_admit_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, con
                        const float* g, const uint8_t* bits) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = check_slots(ctx, layer, seq0, nseq, T);
     if (st) return st;
     if (T < 1) return fail(WGKV_EINVAL, "Session::prefill: empty prompt");
@@ -678,6 +691,7 @@ int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const 
                     const void* v, const uint8_t* bits, void* out) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = check_slots(ctx, layer, seq0, nseq, T);
     if (st) return st;
     VsArgs a{};
@@ -711,6 +725,7 @@ int wgkv_prefill_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, con
                        const void* v, const float* forced_g, void* out, float* g_out, uint8_t* bits_out) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = check_slots(ctx, layer, seq0, nseq, T);
     if (st) return st;
     if (T < 1) return fail(WGKV_EINVAL, "Session::prefill: empty prompt");
@@ -743,6 +758,7 @@ static int decode_append_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, cons
                               const float* forced_g, const DecodeTrace& tr, bool split = false) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s)
@@ -800,6 +816,7 @@ static int decode_attn_impl(wgkv_ctx* ctx, int layer, int seq0, int nseq, const 
                             const FinishArgs* fin) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
     const auto& c = ctx->cfg;
@@ -876,6 +893,7 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
                              const void* v, const float* forced_g, void* out, const wgkv_decode_trace* trace) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     DecodeTrace tr{};
     if (trace) tr = DecodeTrace{trace->g, trace->bits, trace->near_tau, trace->events};
     if (!defer_append(ctx->cfg)) {
@@ -894,7 +912,9 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
         if (ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] >= ctx->cfg.max_tokens)
             return fail(WGKV_EINVAL, "sequence exceeds max_tokens");
     if (!forced_g && !ctx->gates_set) return fail(WGKV_ESTATE, "gate parameters not set");
+    const bool prewait = ctx->finish_layer >= 0 && ctx->finish_layer != layer && ctx->finish_gen + 1 == ctx->api_gen;
     FinishArgs fin{};
+    fin.prewait = prewait;
     fin.ga = ctx->gate_args(layer, 1, 0);
     fin.k_new = (const __nv_bfloat16*)k_pre;
     fin.v_new = (const __nv_bfloat16*)v;
@@ -904,6 +924,8 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, &fin);
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
+    ctx->finish_gen = ctx->api_gen;
+    ctx->finish_layer = layer;
     return WGKV_OK;
 }
 
@@ -916,6 +938,7 @@ int wgkv_decode_layer(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* 
 int wgkv_cache_state(wgkv_ctx* ctx, int layer, int seq, int kv_head, int64_t* lens) {
     if (!ctx || !lens) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (layer < 0 || layer >= c.layers || seq < 0 || seq >= c.max_seqs || kv_head < 0 || kv_head >= c.kv_heads)
         return fail(WGKV_EINVAL, "index out of range");
@@ -939,6 +962,7 @@ int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk,
     int st = wgkv_cache_state(ctx, layer, seq, kv_head, lens);
     if (st) return st;
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     const int d = c.head_dim;
     const long G = lens[2], Lc = lens[0], rows = G + Lc;
@@ -988,6 +1012,7 @@ int wgkv_cache_export(wgkv_ctx* ctx, int layer, int seq, int kv_head, float* gk,
 int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* len) {
     if (!ctx || !len) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (seq < 0 || seq >= c.max_seqs) return fail(WGKV_EINVAL, "seq out of range");
     std::string text;
@@ -1024,6 +1049,7 @@ int wgkv_cache_snapshot(wgkv_ctx* ctx, int seq, char* buf, size_t cap, size_t* l
 int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -1049,6 +1075,7 @@ int wgkv_cache_stats(wgkv_ctx* ctx, int seq0, int nseq, int64_t* out) {
 int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (seq0 < 0 || nseq < 1 || seq0 + nseq > c.max_seqs) return fail(WGKV_EINVAL, "sequence slots out of range");
     release_kernel<<<c.layers * nseq * c.kv_heads, 256, 0, ctx->stream>>>(ctx->pv, c.layers, seq0, nseq);
@@ -1068,6 +1095,7 @@ int wgkv_release(wgkv_ctx* ctx, int seq0, int nseq) {
 int wgkv_pool_info(wgkv_ctx* ctx, int64_t* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     int32_t top = 0;
     WGKV_CUDA_TRY(cudaMemcpy(&top, ctx->pv.free_top, sizeof(top), cudaMemcpyDeviceToHost));
@@ -1117,6 +1145,7 @@ static int comm_setup(wgkv_ctx* ctx, int world, int rank) {
 int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank) {
     if (!ctx || !id128) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     if (ctx->comm) return fail(WGKV_ESTATE, "comm: already initialised");
     if (world < 1 || rank < 0 || rank >= world) return fail(WGKV_EINVAL, "comm: bad world / rank");
     int st = comm_setup(ctx, world, rank);
@@ -1131,6 +1160,7 @@ int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank) {
 int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank) {
     if (!ctx || !nccl_comm) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     if (ctx->comm) return fail(WGKV_ESTATE, "comm: already initialised");
     if (world < 1 || rank < 0 || rank >= world) return fail(WGKV_EINVAL, "comm: bad world / rank");
     std::string why;
@@ -1144,6 +1174,7 @@ int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank) {
 int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out, void* full_out, int async) {
     if (!ctx || !local_out || !full_out) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (nseq < 1 || T < 1) return fail(WGKV_EINVAL, "allgather_heads: empty");
     const size_t blk = (size_t)c.q_heads * c.head_dim * ctx->esz;  // one rank's heads of one token
@@ -1177,6 +1208,7 @@ int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out,
 int wgkv_output_proj(wgkv_ctx* ctx, int nseq, long T, const void* local_out, const void* wo, int dim, float* x) {
     if (!ctx || !local_out || !wo || !x) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     const auto& c = ctx->cfg;
     if (nseq < 1 || T < 1 || dim < 1) return fail(WGKV_EINVAL, "output_proj: empty");
     if (c.dtype != WGKV_BF16) return fail(WGKV_ENOTSUP, "output_proj: bf16 contexts only");
@@ -1217,6 +1249,7 @@ int wgkv_output_proj(wgkv_ctx* ctx, int nseq, long T, const void* local_out, con
 int wgkv_comm_join(wgkv_ctx* ctx) {
     if (!ctx) return fail(WGKV_EINVAL, "null ctx");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     if (ctx->comm_stream) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm_done, 0));
     return WGKV_OK;
 }
@@ -1234,6 +1267,7 @@ int wgkv_assemble_heads(int world, long rows, size_t blk_bytes, const void* rank
 extern "C" int wgkv_dbg_gate_counts(wgkv_ctx* ctx, int* out) {
     if (!ctx || !out) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
     WGKV_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     std::vector<int> pc((size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads);
     WGKV_CUDA_TRY(cudaMemcpy(pc.data(), ctx->ws_pcnt, sizeof(int) * pc.size(), cudaMemcpyDeviceToHost));

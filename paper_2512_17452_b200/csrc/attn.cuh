@@ -51,6 +51,7 @@ struct DecArgs {
     int n_gate_ctas;
     int early_trigger;  // K5 releases its programmatic dependent right after its PDL wait
     int state_in_smem;  // K5 keeps every pair's HeadState in shared memory (fits for <= kDecSmemStatePairs)
+    int prewait;        // K5's predecessor is another layer's finish kernel: plan before the PDL wait
 };
 
 // K6: select_topk_pages + per-q-head attention over the selection (topk.cu).
@@ -70,6 +71,7 @@ struct FinishArgs {
     const float* forced_g;       // [nseq][kv_heads] or null
     DecodeTrace tr;
     AppendWork wk;
+    bool prewait;  // K5 may plan and start its first loads before the PDL wait (see api.cu)
 };
 
 // counter_reset_by_append: the kernel just before on the stream zeroed the work

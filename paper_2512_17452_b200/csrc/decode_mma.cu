@@ -117,11 +117,25 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         return;
     }
     const int kcta = (int)blockIdx.x - a.n_gate_ctas, kgrid = (int)gridDim.x - a.n_gate_ctas;
-    // launched as a programmatic dependent of the previous kernel (K4, or the
-    // previous layer's finish kernel): wait for it (pages, tables, ring state)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    // let the kernel that merges our partials launch now (it waits for our completion)
-    if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;");
+    // Launched as a programmatic dependent of the previous kernel (K4, the
+    // previous layer's finish kernel, or K6's compaction).  Deferred path: the
+    // predecessor (finish of another layer) owns only the shared workspace
+    // (partials, chunk counts, work counter) and its own layer's pages, so the
+    // planning pass, the first item's page ids and its first TMA loads -- this
+    // layer's state and pages -- run before griddepcontrol.wait; q (a caller
+    // input) and every workspace write come after it.  Only when the host saw
+    // that the kernel in front is ANOTHER layer's finish kernel (a.prewait):
+    // the same layer's finish publishes the state and writes the ring.  Top-k:
+    // the selection is the predecessor's output, so everything waits.
+    bool waited = false;
+    auto pdl_wait = [&]() {
+        if (waited) return;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        // let the kernel that merges our partials launch now (it waits for our completion)
+        if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;");
+        waited = true;
+    };
+    if (TOPK || !a.defer || !a.prewait) pdl_wait();
     uint8_t* ring = sm;                                                                    // [DW][DNS][8 KB]
     __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm + DW * DNS * PAGE_B);          // [16][QROW]
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + DW * DNS * PAGE_B + 16 * QROW * 2);  // [DW][DNS]
@@ -150,7 +164,6 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             const int ngv = TOPK ? a.nsel[p] : (st.global_len + ps - 1) / ps;
             const int np = ngv + (st.local_len + ps - 1) / ps;
             item_base[p] = np;
-            if (!TOPK && a.defer && kcta == 0) a.tokpos[p] = st.tokens_seen;  // the new token (finish kernel)
             tot += np;
             npmax = max(npmax, np);
         }
@@ -199,7 +212,6 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         for (int p = p0; p < p1; ++p) {
             const int nc = max(1, (item_base[p] + cp - 1) / cp);
             item_base[p] = acc;
-            if (kcta == 0) nchunks[p] = nc;
             acc += nc;
         }
         if (p1 == npairs && p0 < p1) {
@@ -217,14 +229,35 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     const uint32_t wring = smem_u32(ring) + warp * DNS * PAGE_B;
     uint32_t kq = 0;  // pages this warp has issued / consumed so far (ring position + parity)
 
+    // after the PDL wait: the plan's chunk counts and (deferred) the new tokens'
+    // positions for the merging kernel -- the workspace the predecessor read
+    bool published = false;
+    auto publish_plan = [&]() {
+        pdl_wait();
+        if (published) return;
+        published = true;
+        if (kcta != 0) return;
+        for (int p = tid; p < npairs; p += blockDim.x) {
+            nchunks[p] = item_base[p + 1] - item_base[p];
+            if (!TOPK && a.defer)
+                a.tokpos[p] = a.state_in_smem
+                                  ? sst[p].tokens_seen
+                                  : a.pv.state[a.pv.head_index(a.layer, a.seq0 + p / a.pv.kv_heads, p % a.pv.kv_heads)]
+                                        .tokens_seen;
+        }
+    };
     __shared__ int s_item;
     // first item static (kcta): no atomic round trip in front of it; later items
-    // are stolen from kgrid on (the merging kernel resets the counter to 0)
+    // are stolen from kgrid on (the merging kernel resets the counter to 0 --
+    // only read after the PDL wait, which the first item passes)
     for (int first = 1;; first = 0) {
         if (tid == 0) s_item = first ? kcta : kgrid + atomicAdd(work_counter, 1);
         __syncthreads();
         const int item = s_item;
-        if (item >= nitems) break;
+        if (item >= nitems) {
+            publish_plan();
+            break;
+        }
         // pair of this item: the last bh with item_base[bh] <= item (binary search)
         int bh = 0;
         for (int lo = 0, hi = npairs - 1; lo <= hi;) {
@@ -318,6 +351,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             tc::fence_proxy_async_smem();
             for (int k = 0; k < min(DNS, nmine); ++k) issue(k);
         }
+        publish_plan();
         // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d); rows >= gs are zero
         // (computed while the first pages of the item are in flight)
         for (int e = tid; e < 16 * (d / 2); e += blockDim.x) {
@@ -511,6 +545,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         fa = *fin;
     }
     a.early_trigger = fin && !no_trigger;
+    a.prewait = fin && fin->prewait;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.n_gate_ctas + CPS * num_sms());
     cfg.blockDim = dim3(DW * 32);
