@@ -516,10 +516,12 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         tp_cap = a.pv.capacity;
     }
     a.n_pairs = nseq * a.pv.kv_heads;
-    a.state_in_smem = a.n_pairs <= kDecSmemStatePairs;
-    const size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) +
-                        4 * PID_CAP + (a.state_in_smem ? sizeof(HeadState) * (size_t)a.n_pairs : 0);
-    if (smem > (size_t)(228 / CPS - 1) * 1024) return WGKV_ENOTSUP;
+    const size_t smem_cap = (size_t)(228 / CPS - 1) * 1024;
+    size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
+    if (smem > smem_cap) return WGKV_ENOTSUP;
+    // per-pair state cached in smem when it still fits CPS CTAs per SM
+    a.state_in_smem = a.n_pairs <= kDecSmemStatePairs && smem + sizeof(HeadState) * (size_t)a.n_pairs <= smem_cap;
+    if (a.state_in_smem) smem += sizeof(HeadState) * (size_t)a.n_pairs;
     const bool topk = a.sel != nullptr;
     auto kern = topk ? decode_attn_mma_kernel<true> : decode_attn_mma_kernel<false>;
     if (ensure_smem(kern, smem) != cudaSuccess) return WGKV_ECUDA;

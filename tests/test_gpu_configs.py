@@ -518,3 +518,46 @@ def test_gate_proj_fused(W, orc, dm, T):
     assert sorted(near.tolist()) == sorted(near2.tolist())
     print(f"gate_proj dm={dm}: {frac:.2e} of k_pre on the other side of a bf16 rounding boundary, "
           f"{int(bits.sum())} admitted")
+
+
+def test_decode_many_pairs(W, orc):
+    """configs[3]-like batch geometry: 64 sequence slots x 4 kv heads = 256
+    (seq, kv head) pairs in one decode launch (K5's per-pair state no longer
+    fits its shared memory next to two CTAs per SM and is read from HBM), each
+    slot at its own length; sampled slots checked against their own oracle
+    sessions (outputs, promotion events, Global positions)."""
+    d = hid = 128
+    hq, hkv, Wn, steps, nseq = 16, 4, 64, 3, 64
+    rng = np.random.default_rng(5)
+    lens = [int(x) for x in rng.integers(80, 260, nseq)]
+    bank = orc.gate_random_init(1, hkv, d, hid, 61, 0.1, -1.8)
+    mx = max(lens) + steps
+    s = W.Session(1, hq, hkv, d, hid, Wn, max_seqs=nseq, max_tokens=mx, gate_bank=bank)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = torch.randn(nseq, mx, hq, d, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(nseq, mx, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(nseq, mx, hkv, d, device="cuda", generator=g).to(torch.bfloat16)
+    for b, T in enumerate(lens):
+        s.prefill_layer(0, q[b:b + 1, :T], k[b:b + 1, :T], v[b:b + 1, :T], seq0=b)
+    check = [0, 17, 42, 63]
+    refs = {}
+    for b in check:
+        r = O.Session(orc, 1, hq, hkv, d, hid, Wn, gate_bank=bank, max_tokens=mx)
+        f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+        r.prefill_layer(0, f(q[b, :lens[b]]), f(k[b, :lens[b]]), f(v[b, :lens[b]]))
+        refs[b] = r
+    for i in range(steps):
+        idx = torch.tensor([lens[b] + i for b in range(nseq)], device="cuda")
+        ar = torch.arange(nseq, device="cuda")
+        qs, ks, vs = q[ar, idx].contiguous(), k[ar, idx].contiguous(), v[ar, idx].contiguous()
+        o, _, ev = s.decode_layer(0, qs, ks, vs, want_events=True)
+        o, ev = o.float().cpu().numpy(), ev.cpu().numpy()
+        for b in check:
+            f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
+            ro, _, rev, _ = refs[b].decode_layer(0, f(qs[b]), f(ks[b]), f(vs[b]))
+            assert np.array_equal(ev[b], rev), (i, b)
+            for p in range(hq):
+                assert rel_err(o[b, p], ro[p]) < TOL["bf16"], (i, b, p)
+    for b in check:
+        for h in range(hkv):
+            assert np.array_equal(s.gather(0, b, h)["global_pos"], refs[b].gather(0, h)["global_pos"])
