@@ -226,7 +226,8 @@ int launch_admit_prefill(const PoolView& pv, int layer, int seq0, int nseq, long
 // K4 standalone: the split append's route + gate CTAs (append.cuh)
 // ---------------------------------------------------------------------------
 // mode 0: route + gate CTAs in one launch; 1: route CTAs only (the gate CTAs
-// follow in a mode-2 launch on a side stream, overlapping the attention)
+// follow in a mode-2 launch on a side stream, overlapping the attention);
+// 3: gate CTAs only, beside a deferred decode whose finish kernel routes
 template <typename E>
 __global__ void __launch_bounds__(kAppendThreads) decode_append_kernel(PoolView pv, GateArgs ga, int layer, int seq0,
                                                                         long W, int npairs,
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_append_kernel(PoolView 
                                                                         DecodeTrace tr, AppendWork wk, int mode) {
     extern __shared__ __align__(16) uint8_t append_smem[];
     const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
-    const int r = mode == 2 ? npairs + (int)blockIdx.x : (int)blockIdx.x;
+    const int r = mode >= 2 ? npairs + (int)blockIdx.x : (int)blockIdx.x;
     append_role<E>(pv, ga, layer, seq0, W, npairs, r, gpp, gpp + 1, k_pre, v, forced_g, tr, wk, append_smem);
 }
 
@@ -249,7 +250,7 @@ int launch_decode_append(const PoolView& pv, const GateArgs& ga, int layer, int 
     const int npairs = nseq * pv.kv_heads;
     const int gpp = forced_g ? 0 : gate_ctas_per_pair(ga.hidden);
     AppendWork wk = wk0;
-    wk.early_state = mode != 0;
+    wk.early_state = mode == 1 || mode == 2;
     const int grid = mode == 0 ? npairs * (1 + gpp) : (mode == 1 ? npairs : npairs * gpp);
     if (grid > 0)
         decode_append_kernel<E><<<grid, kAppendThreads, smem, st>>>(pv, ga, layer, seq0, W, npairs, k_pre, v, forced_g,

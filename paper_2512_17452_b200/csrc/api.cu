@@ -921,7 +921,25 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     fin.forced_g = forced_g;
     fin.tr = tr;
     fin.wk = ctx->wk;
+    // the append's gate CTAs on a side stream forked before K5 and joined after
+    // the finish kernel (WGKV_GATE_PLACE=side): they need nothing K5 produces
+    static const char* gp_env = getenv("WGKV_GATE_PLACE");
+    fin.gate_side = !forced_g && gp_env && strcmp(gp_env, "side") == 0;
+    if (fin.gate_side) {
+        if (!ctx->gate_stream) {
+            WGKV_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->gate_stream, cudaStreamNonBlocking));
+            WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_route, cudaEventDisableTiming));
+            WGKV_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_gate, cudaEventDisableTiming));
+        }
+        WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_route, ctx->stream));
+        WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->gate_stream, ctx->ev_route, 0));
+        st = launch_decode_append<__nv_bfloat16>(ctx->pv, fin.ga, layer, seq0, nseq, ctx->cfg.window, fin.k_new,
+                                                 fin.v_new, nullptr, tr, ctx->wk, ctx->gate_stream, 3);
+        if (st) return fail(st, "decode gate kernel failed");
+        WGKV_CUDA_TRY(cudaEventRecord(ctx->ev_gate, ctx->gate_stream));
+    }
     st = decode_attn_impl(ctx, layer, seq0, nseq, q, out, &fin);
+    if (fin.gate_side) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_gate, 0));
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
     ctx->finish_gen = ctx->api_gen;

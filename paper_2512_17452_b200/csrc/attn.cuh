@@ -72,6 +72,7 @@ struct FinishArgs {
     DecodeTrace tr;
     AppendWork wk;
     bool prewait;  // K5 may plan and start its first loads before the PDL wait (see api.cu)
+    bool gate_side;  // the append's gate CTAs run in their own launch on a side stream
 };
 
 // counter_reset_by_append: the kernel just before on the stream zeroed the work

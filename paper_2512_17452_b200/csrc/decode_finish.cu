@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     asm volatile("griddepcontrol.launch_dependents;");
     const int tid = threadIdx.x;
     // grid: [gate CTAs of the append, when not in the K5 launch][combine CTAs][route CTAs]
-    const int gpp = (fin.forced_g || a.n_gate_ctas > 0) ? 0 : gate_ctas_per_pair(fin.ga.hidden);
+    const int gpp = (fin.forced_g || a.n_gate_ctas > 0 || fin.gate_side) ? 0 : gate_ctas_per_pair(fin.ga.hidden);
     const int ngate = a.n_pairs * gpp;
     const int arrivals = fin.forced_g ? 1 : gate_ctas_per_pair(fin.ga.hidden) + 1;
     if ((int)blockIdx.x < ngate) {
@@ -151,7 +151,7 @@ int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, con
     const int ncomb = nseq * a.q_heads;
     // route CTAs, plus the gate CTAs unless K5 ran them (a.n_gate_ctas > 0)
     const int napp = nseq * a.pv.kv_heads *
-                     (1 + ((fin.forced_g || a.n_gate_ctas > 0) ? 0 : gate_ctas_per_pair(fin.ga.hidden)));
+                     (1 + ((fin.forced_g || a.n_gate_ctas > 0 || fin.gate_side) ? 0 : gate_ctas_per_pair(fin.ga.hidden)));
     const size_t smem = std::max(append_smem_bytes(a.pv.head_dim, fin.ga.hidden),
                                  sizeof(float) * (2 * (kAppendThreads / 32) + (kAppendThreads / 32) * 128));
     if (ensure_smem(decode_finish_kernel, smem) != cudaSuccess) return WGKV_ECUDA;

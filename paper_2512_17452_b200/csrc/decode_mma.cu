@@ -542,7 +542,7 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     static const bool no_trigger = getenv("WGKV_K5_NO_TRIGGER") != nullptr;  // A/B switch
     FinishArgs fa{};
     a.n_gate_ctas = 0;
-    if (fin && !fin->forced_g && a.n_pairs * gate_ctas_per_pair(fin->ga.hidden) <= gate_k5_max) {
+    if (fin && !fin->forced_g && !fin->gate_side && a.n_pairs * gate_ctas_per_pair(fin->ga.hidden) <= gate_k5_max) {
         a.n_gate_ctas = a.n_pairs * gate_ctas_per_pair(fin->ga.hidden);
         fa = *fin;
     }
