@@ -343,6 +343,20 @@ def run_gpu(args, cfg):
         if shards > 1:
             exchange_prefill(o_)
 
+    def prefill_layer_seq(l, s_, inputs, out_buf):
+        """The same layer body for sequence slot s_ alone (e2e: the first layer
+        starts on sequence 0 while the other sequences' inputs are still on PCIe,
+        the last layer's outputs drain per sequence)."""
+        qi, ki, vi = (x[s_:s_ + 1] for x in inputs)
+        o_ = out_buf[s_:s_ + 1]
+        check(lib.wgkv_gate_score(h, l, 1, T, 0, P(ki), None, P(kpost[s_:s_ + 1]), P(g_ws[s_:s_ + 1]),
+                                  P(bits_ws[s_:s_ + 1]), None, 0, None), "K1")
+        check(lib.wgkv_admit_prefill(h, l, s_, 1, T, P(kpost[s_:s_ + 1]), P(vi), P(g_ws[s_:s_ + 1]),
+                                     P(bits_ws[s_:s_ + 1])), "K2")
+        check(lib.wgkv_vs_prefill(h, l, s_, 1, T, P(qi), P(kpost[s_:s_ + 1]), P(vi), P(bits_ws[s_:s_ + 1]), P(o_)),
+              "K3")
+        launches["n"] += 6
+
     # One decode token-step over all layers, issued eagerly or replayed from a
     # CUDA graph captured once (kills per-kernel launch gaps); the step's new
     # q/k/v are copied into static buffers first, so every replay is a real step.
@@ -491,13 +505,26 @@ def run_gpu(args, cfg):
         d2h_s.wait_stream(stream)
         h2d = d2h = 0
 
+        # the first layer's inputs and the last layer's outputs have nothing to
+        # overlap with but the layer itself: they move (and are processed) one
+        # sequence at a time (single-GPU runs; with C1 the layer is one call)
+        per_seq = shards == 1 and B > 1
+        ready0 = [torch.cuda.Event() for _ in range(B)]
+        done_last = [torch.cuda.Event() for _ in range(B)]
+
         def load(l):
             b_ = l % 2
             with torch.cuda.stream(h2d_s):
                 if l >= 2:
                     h2d_s.wait_event(free[b_])  # layer l-2 has consumed this buffer
-                for dst, src in zip(bufs[b_], (hq_in, hk_in, hv_in)):
-                    dst.copy_(src, non_blocking=True)
+                if l == 0 and per_seq:
+                    for s_ in range(B):
+                        for dst, src in zip(bufs[b_], (hq_in, hk_in, hv_in)):
+                            dst[s_].copy_(src[s_], non_blocking=True)
+                        ready0[s_].record(h2d_s)
+                else:
+                    for dst, src in zip(bufs[b_], (hq_in, hk_in, hv_in)):
+                        dst.copy_(src, non_blocking=True)
                 ready[b_].record(h2d_s)
 
         load(0)
@@ -505,16 +532,38 @@ def run_gpu(args, cfg):
             b = l % 2
             if l + 1 < L:
                 load(l + 1)
-            stream.wait_event(ready[b])
             if l >= 2:
                 stream.wait_event(drained[b])  # output of layer l-2 is on the host
-            prefill_layer(l, inputs=bufs[b], out_buf=e_outs[b])
-            free[b].record(stream)
-            computed[b].record(stream)
-            with torch.cuda.stream(d2h_s):
-                d2h_s.wait_event(computed[b])
-                h_out.copy_(e_outs[b], non_blocking=True)
-                drained[b].record(d2h_s)
+            if per_seq and l in (0, L - 1):
+                if l != 0:
+                    stream.wait_event(ready[b])
+                for s_ in range(B):
+                    if l == 0:
+                        stream.wait_event(ready0[s_])
+                    prefill_layer_seq(l, s_, bufs[b], e_outs[b])
+                    if l == L - 1:
+                        done_last[s_].record(stream)
+                        with torch.cuda.stream(d2h_s):
+                            d2h_s.wait_event(done_last[s_])
+                            h_out[s_].copy_(e_outs[b][s_], non_blocking=True)
+                free[b].record(stream)
+                if l == L - 1:
+                    drained[b].record(d2h_s)
+                else:
+                    computed[b].record(stream)
+                    with torch.cuda.stream(d2h_s):
+                        d2h_s.wait_event(computed[b])
+                        h_out.copy_(e_outs[b], non_blocking=True)
+                        drained[b].record(d2h_s)
+            else:
+                stream.wait_event(ready[b])
+                prefill_layer(l, inputs=bufs[b], out_buf=e_outs[b])
+                free[b].record(stream)
+                computed[b].record(stream)
+                with torch.cuda.stream(d2h_s):
+                    d2h_s.wait_event(computed[b])
+                    h_out.copy_(e_outs[b], non_blocking=True)
+                    drained[b].record(d2h_s)
             h2d += sum(x.numel() * x.element_size() for x in bufs[b])
             d2h += e_outs[b].numel() * e_outs[b].element_size()
         if world > 1:
