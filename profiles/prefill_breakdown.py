@@ -70,7 +70,8 @@ def main():
         s.release(0, B)
     if args.trace:
         buf = np.zeros((4, 4096, 8), np.uint64)
-        fn = lib.wgkv_dbg_k3_trace1 if os.environ.get("WGKV_TRACE_V1") else lib.wgkv_dbg_k3_trace
+        fn = getattr(lib, os.environ.get("WGKV_TRACE_FN", "wgkv_dbg_k3_trace1" if os.environ.get("WGKV_TRACE_V1")
+                                         else "wgkv_dbg_k3_trace"))
         check(fn(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes)))
         np.save(args.trace, buf)
     ii = torch.arange(T, device=dev)
