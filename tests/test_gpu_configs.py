@@ -561,3 +561,27 @@ def test_decode_many_pairs(W, orc):
     for b in check:
         for h in range(hkv):
             assert np.array_equal(s.gather(0, b, h)["global_pos"], refs[b].gather(0, h)["global_pos"])
+
+
+def test_comm_world_one_in_cuda_graph(W, orc):
+    """The decode-shaped head all-gather through NCCL captured inside a CUDA
+    graph (bench.py captures one token step, C1 included) and replayed: the
+    output follows the inputs of each replay."""
+    hq, hkv, d, B = 8, 2, 128, 2
+    s = W.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=64, gate_bank=orc.gate_random_init(1, hkv, d, d, 3))
+    s.comm_init(W.nccl_unique_id(), 1, 0)
+    xd = torch.zeros(B, hq, d, device="cuda", dtype=torch.bfloat16)
+    fd = torch.zeros_like(xd)
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    s.set_stream(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        s.allgather_heads(xd, fd)
+    s.set_stream(torch.cuda.current_stream())
+    torch.cuda.current_stream().wait_stream(st)
+    for i in range(3):
+        xd.copy_(torch.randn(B, hq, d, device="cuda").to(torch.bfloat16))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(fd, xd), i
