@@ -97,6 +97,11 @@ struct GateProjArgs {
     GateArgs g;
     int nseq, dm;
     long tiles_per_pair, total_tiles;
+    // head-interleaved schedule (head_sched = 1): CTA k takes kv head k % H and the
+    // (k / H)-th of gridDim / H contiguous ranges of token tiles, so the H CTAs of
+    // a range stream the same layer-input tiles at the same time (one HBM read,
+    // the other heads hit L2) while each CTA keeps one head's W1 resident
+    int head_sched;
     const float2* rope;  // [T][d/2] (cos, sin) of position pos0 + t
 };
 
@@ -122,8 +127,22 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
     __nv_bfloat16* xxs = reinterpret_cast<__nv_bfloat16*>(sm + GP_OFF_XX);
     const GateArgs& a = A.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long t_begin = A.total_tiles * blockIdx.x / gridDim.x;
-    const long t_end = A.total_tiles * (blockIdx.x + 1) / gridDim.x;
+    long t_begin, t_end;
+    int hsched = 0;  // this CTA's kv head (head-interleaved schedule)
+    if (A.head_sched) {
+        const int R = (int)gridDim.x / a.kv_heads, r = (int)blockIdx.x / a.kv_heads;
+        hsched = (int)blockIdx.x % a.kv_heads;
+        const long ntt = (long)A.nseq * A.tiles_per_pair;  // token tiles over all sequences
+        t_begin = ntt * r / R;
+        t_end = ntt * (r + 1) / R;
+    } else {
+        t_begin = A.total_tiles * blockIdx.x / gridDim.x;
+        t_end = A.total_tiles * (blockIdx.x + 1) / gridDim.x;
+    }
+    // tile -> (seq * kv_heads + head, first token)
+    auto pair_of = [&](long tile) -> int {
+        return A.head_sched ? (int)(tile / A.tiles_per_pair) * a.kv_heads + hsched : (int)(tile / A.tiles_per_pair);
+    };
     const int nk = A.dm / 64;  // projection K steps of 64
     if (threadIdx.x == 0) {
         tc::mbar_init(b_full, 1);
@@ -154,7 +173,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
         const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16) + COL_P + 64u * half;
         for (long tile = t_begin; tile < t_end; ++tile) {
             const int it = (int)(tile - t_begin);
-            const int pair = (int)(tile / A.tiles_per_pair);
+            const int pair = pair_of(tile);
             const long t0 = (tile % A.tiles_per_pair) * 128;
             const int s = pair / a.kv_heads, h = pair % a.kv_heads;
             const long t = t0 + r;
@@ -235,7 +254,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
         };
         for (long tile = t_begin; tile < t_end; ++tile) {
             const int it = (int)(tile - t_begin);
-            const int pair = (int)(tile / A.tiles_per_pair);
+            const int pair = pair_of(tile);
             const long t0 = (tile % A.tiles_per_pair) * 128;
             const int s = pair / a.kv_heads, h = pair % a.kv_heads;
             const int blk = a.layer * a.kv_heads + h;
@@ -304,7 +323,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
         const float u_eff = 3.0e-5f;
         for (long tile = t_begin + grp; tile < t_end; tile += 2) {
             const int it = (int)(tile - t_begin);
-            const int pair = (int)(tile / A.tiles_per_pair);
+            const int pair = pair_of(tile);
             const long t0 = (tile % A.tiles_per_pair) * 128;
             const int s = pair / a.kv_heads, h = pair % a.kv_heads;
             const int blk = a.layer * a.kv_heads + h;
@@ -374,7 +393,9 @@ int launch_gate_proj_tc(const GateArgs& a, int nseq, const __nv_bfloat16* x, con
     A.tiles_per_pair = (a.T + 127) / 128;
     A.total_tiles = A.tiles_per_pair * nseq * a.kv_heads;
     A.rope = rope_ws;
-    const int grid = (int)std::min<long>(num_sms(), A.total_tiles);
+    const int R = num_sms() / a.kv_heads;  // token-tile ranges per head
+    A.head_sched = R >= 1 && (long)nseq * A.tiles_per_pair >= R;
+    const int grid = A.head_sched ? R * a.kv_heads : (int)std::min<long>(num_sms(), A.total_tiles);
     gate_proj_kernel<<<grid, GP_THREADS, GP_SMEM, st>>>(tw, ta, twk, A, k_pre, k_post, g, bits, cand, pcnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
