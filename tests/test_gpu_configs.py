@@ -585,3 +585,25 @@ def test_comm_world_one_in_cuda_graph(W, orc):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(fd, xd), i
+
+
+def test_f1_f3_argument_errors(W, orc):
+    """The f1 / f3 entry points reject what they do not implement the way the
+    rest of the C-ABI does (ENOTSUP / EINVAL, no kernel launched)."""
+    from paper_2512_17452_b200._lib import NotSupported
+
+    hq, hkv, d = 8, 2, 128
+    bank = orc.gate_random_init(1, hkv, d, d, 3)
+    s32 = W.Session(1, hq, hkv, d, d, 64, max_tokens=64, dtype=W.F32, gate_bank=bank)
+    lo = torch.zeros(1, 8, hq, d, device="cuda")
+    wo = torch.zeros(256, hq * d, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(NotSupported):  # bf16 contexts only
+        s32.output_proj(lo, wo, torch.zeros(1, 8, 256, device="cuda"))
+    s = W.Session(1, hq, hkv, d, d, 64, max_tokens=64, gate_bank=bank)
+    x = torch.zeros(1, 8, 100, device="cuda", dtype=torch.bfloat16)
+    wk = torch.zeros(hkv, d, 100, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(NotSupported):  # model dim must be a multiple of 64
+        s.gate_forward_batch_proj(0, x, wk)
+    with pytest.raises(ValueError):  # T beyond max_prefill_tokens
+        s.gate_forward_batch_proj(0, torch.zeros(1, 65, 128, device="cuda", dtype=torch.bfloat16),
+                                  torch.zeros(hkv, d, 128, device="cuda", dtype=torch.bfloat16))
