@@ -53,6 +53,9 @@ constexpr int kGateInK5MaxCtas = WGKV_GATE_K5_MAX;  // gate CTAs carried by the 
 #ifndef WGKV_K5_CAPCH
 #define WGKV_K5_CAPCH 24  // chunks per (seq, kv head) pair the few-long-pairs rule aims at
 #endif
+#ifndef WGKV_K5_ITEMS_DIV
+#define WGKV_K5_ITEMS_DIV 2  // the few-long-pairs cap keeps >= grid / ITEMS_DIV items
+#endif
 #ifndef WGKV_K5_MIN_PAGES
 #define WGKV_K5_MIN_PAGES 8
 #endif
@@ -191,7 +194,8 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
 #if WGKV_K5_RULE == 1
         // few, long pairs (small batches): cap the chunks per pair near 24 (the
         // combine merges every chunk) while keeping >= grid/2 items in flight
-        cp = max(cp, (int)min((long)(npmax + WGKV_K5_CAPCH - 1) / WGKV_K5_CAPCH, (2 * total + kgrid - 1) / kgrid));
+        cp = max(cp, (int)min((long)(npmax + WGKV_K5_CAPCH - 1) / WGKV_K5_CAPCH,
+                              (WGKV_K5_ITEMS_DIV * total + kgrid - 1) / kgrid));
 #endif
         if (a.pin_cp > 0) cp = a.pin_cp;  // pinned split: per-head arithmetic independent of the launch
         cp = max(cp, (npmax + a.max_chunks - 1) / a.max_chunks);
