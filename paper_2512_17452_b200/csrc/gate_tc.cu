@@ -100,7 +100,8 @@ struct GateTcArgs {
 };
 
 __global__ void __launch_bounds__(G_THREADS, 1)
-    gate_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tk, GateTcArgs A, const __nv_bfloat16* __restrict__ k_pre,
+    gate_tc_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tk,
+                   const __grid_constant__ CUtensorMap tpost, GateTcArgs A, const __nv_bfloat16* __restrict__ k_pre,
                    __nv_bfloat16* __restrict__ k_post, float* __restrict__ g_out, uint8_t* __restrict__ bits_out,
                    int32_t* __restrict__ cand, int* __restrict__ pcnt) {
     extern __shared__ uint8_t gsm_raw[];
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     uint64_t* b_full = bars + 0;
     uint64_t* t_full = bars + 3;    // [2]
     uint64_t* t_empty = bars + 5;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);  // (bars + 13: st_read)
     __nv_bfloat16* xxs = reinterpret_cast<__nv_bfloat16*>(sm + G_OFF_XX);
     const GateArgs& a = A.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     uint64_t* hl_full = bars + 9;   // producers wrote the hi / lo tiles
     uint64_t* hl_empty = bars + 10; // MMAs of segments 3-5 (hi / lo operands) done
     uint64_t* pre_read = bars + 11; // producers hold the k_pre tile in registers
+    uint64_t* st_read = bars + 13;  // the k_post (= hi) tile's TMA store has read shared memory
     if (threadIdx.x == 0) {
         tc::mbar_init(b_full, 1);
         tc::mbar_init(pre_full, 1);
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         tc::mbar_init(hl_full, G_PROD);
         tc::mbar_init(hl_empty, 1);
         tc::mbar_init(pre_read, G_PROD);
+        tc::mbar_init(st_read, 1);
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&t_full[b], 1);
             tc::mbar_init(&t_empty[b], G_EPI / 2);
@@ -168,7 +171,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             for (int u = 0; u < 8; ++u)
                 raw8[u] = *reinterpret_cast<const uint4*>(sm + G_OFF_A + (uint32_t)half * GT_SUB + tc::sw128_off(r, u));
             tc::mbar_arrive(pre_read);
-            if (it > 0) tc::mbar_wait_sleep(hl_empty, (it - 1) & 1);  // previous tile's hi / lo consumed
+            if (it > 0) {
+                tc::mbar_wait_sleep(hl_empty, (it - 1) & 1);  // previous tile's hi / lo consumed by the MMAs
+                tc::mbar_wait_sleep(st_read, (it - 1) & 1);   // and the hi tile read by its k_post store
+            }
             float xx = 0.f;
 #pragma unroll
             for (int u4 = 0; u4 < 8; u4 += 2) {
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                     const uint4 hv = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                     *reinterpret_cast<uint4*>(sm + G_OFF_A + GT_TILE + so) = hv;
                     *reinterpret_cast<uint4*>(sm + G_OFF_A + 2 * GT_TILE + so) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                    if (valid) dpost[u] = hv;
+                    (void)dpost;
                 }
             }
             xx += __shfl_xor_sync(0xffffffffu, xx, 1);
@@ -269,6 +275,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 }
                 tc::mbar_wait(hl_full, it & 1);
                 tc::fence_after_sync();
+                // k_post = the hi tile: one TMA store per 64-dim half (full lines, rows
+                // past the sequence's T clipped by the 4-D map) instead of every
+                // producer's strided 16-byte stores
+                if (lane == 0) {
+                    const int s = pair / a.kv_heads, h = pair % a.kv_heads;
+                    const int t0 = (int)((tile % A.tiles_per_pair) * 128);
+                    for (int hh = 0; hh < 2; ++hh)
+                        tc::tma_store_4d(&tpost, sm + G_OFF_A + GT_TILE + hh * GT_SUB, hh * 64, h, t0, s);
+                    tc::bulk_commit_group();
+                }
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Ahi, kk), kdesc(Bqh, kk), idG, 1u);
 #pragma unroll
@@ -277,7 +293,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 for (int kk = 0; kk < 8; ++kk) tc::mma_ss_w(dt, kdesc(Alo, kk), kdesc(Bqh, kk), idG, 1u);
                 tc::mma_commit_w(hl_empty);
                 tc::mma_commit_w(&t_full[buf]);
+                if (lane == 0) {  // the hi tile may be rewritten once the store has read it
+                    tc::bulk_wait_group_read0();
+                    tc::mbar_arrive(st_read);
+                }
+                __syncwarp();
             }
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // k_post written
         }
         __syncwarp();
     } else {
@@ -372,6 +394,13 @@ int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv
     if (make_tmap_3d_bf16(&tk, k_pre, 128, (uint64_t)a.kv_heads, (uint64_t)nseq * a.T, 256, (uint64_t)a.kv_heads * 256,
                           64, 1, 128))
         return WGKV_ECUDA;
+    CUtensorMap tpost;  // k_post [nseq][T][kv_heads][128] as {128, kv_heads, T, nseq}
+    {
+        const uint64_t dims[4] = {128, (uint64_t)a.kv_heads, (uint64_t)a.T, (uint64_t)nseq};
+        const uint64_t strides[3] = {256, (uint64_t)a.kv_heads * 256, (uint64_t)a.T * a.kv_heads * 256};
+        const uint32_t box[4] = {64, 1, 128, 1};
+        if (make_tmap_4d_bf16(&tpost, k_post, dims, strides, box)) return WGKV_ECUDA;
+    }
     if (ensure_smem(gate_tc_kernel, G_SMEM) != cudaSuccess) return WGKV_ECUDA;
     rope_table_kernel<<<num_sms() * 8, 256, 0, st>>>(a.freq, a.pos0, a.T, a.d / 2, rope_ws);
     GateTcArgs A;
@@ -381,7 +410,7 @@ int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv
     A.total_tiles = A.tiles_per_pair * nseq * a.kv_heads;
     A.rope = rope_ws;
     const int grid = (int)std::min<long>(num_sms(), A.total_tiles);
-    gate_tc_kernel<<<grid, G_THREADS, G_SMEM, st>>>(tw, tk, A, k_pre, k_post, g, bits, cand, pcnt);
+    gate_tc_kernel<<<grid, G_THREADS, G_SMEM, st>>>(tw, tk, tpost, A, k_pre, k_post, g, bits, cand, pcnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
