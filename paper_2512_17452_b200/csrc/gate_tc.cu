@@ -94,6 +94,7 @@ __device__ __forceinline__ uint16_t bf16_bits(float x) {
 struct GateTcArgs {
     GateArgs g;
     int nseq;
+    int head_sched;
     long tiles_per_pair;
     long total_tiles;
     const float2* rope;  // [T][d/2] (cos, sin) of position pos0 + t
@@ -115,8 +116,25 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     __nv_bfloat16* xxs = reinterpret_cast<__nv_bfloat16*>(sm + G_OFF_XX);
     const GateArgs& a = A.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long t_begin = A.total_tiles * blockIdx.x / gridDim.x;
-    const long t_end = A.total_tiles * (blockIdx.x + 1) / gridDim.x;
+    // head-interleaved schedule (head_sched): CTA k takes kv head k % H and the
+    // (k / H)-th of gridDim / H ranges of token tiles, so the H CTAs of a range
+    // walk the same positions together (the cos/sin table rows are shared in L2)
+    // and each keeps its head's W1 resident
+    long t_begin, t_end;
+    int hsched = 0;
+    if (A.head_sched) {
+        const int R = (int)gridDim.x / a.kv_heads, r = (int)blockIdx.x / a.kv_heads;
+        hsched = (int)blockIdx.x % a.kv_heads;
+        const long ntt = (long)A.nseq * A.tiles_per_pair;
+        t_begin = ntt * r / R;
+        t_end = ntt * (r + 1) / R;
+    } else {
+        t_begin = A.total_tiles * blockIdx.x / gridDim.x;
+        t_end = A.total_tiles * (blockIdx.x + 1) / gridDim.x;
+    }
+    auto pair_of = [&](long tile) -> int {
+        return A.head_sched ? (int)(tile / A.tiles_per_pair) * a.kv_heads + hsched : (int)(tile / A.tiles_per_pair);
+    };
     uint64_t* pre_full = bars + 7;  // k_pre tile landed (TMA)
     uint64_t* pre_empty = bars + 8; // MMAs of segments 1-2 (the k_pre operand) done
     uint64_t* hl_full = bars + 9;   // producers wrote the hi / lo tiles
@@ -152,7 +170,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         const int r = threadIdx.x >> 1, half = threadIdx.x & 1;  // adjacent lanes share a row
         for (long tile = t_begin; tile < t_end; ++tile) {
             const int it = (int)(tile - t_begin);
-            const int pair = (int)(tile / A.tiles_per_pair);
+            const int pair = pair_of(tile);
             const long t0 = (tile % A.tiles_per_pair) * 128;
             const int s = pair / a.kv_heads, h = pair % a.kv_heads;
             const long t = t0 + r;
@@ -229,7 +247,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             const uint32_t Bph = sbase + G_OFF_B, Bqh = Bph + GT_TILE, Bpl = Bph + 2 * GT_TILE,
                            Bql = Bph + 3 * GT_TILE;
             auto load_pre = [&](long tile) {
-                const int pair = (int)(tile / A.tiles_per_pair);
+                const int pair = pair_of(tile);
                 const int t0 = (int)((tile % A.tiles_per_pair) * 128);
                 const int s = pair / a.kv_heads, h = pair % a.kv_heads;
                 if (lane == 0) {
@@ -242,7 +260,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             if (t_begin < t_end) load_pre(t_begin);
             for (long tile = t_begin; tile < t_end; ++tile) {
                 const int it = (int)(tile - t_begin);
-                const int pair = (int)(tile / A.tiles_per_pair);
+                const int pair = pair_of(tile);
                 const int blk = a.layer * a.kv_heads + pair % a.kv_heads;
                 if (blk != cur_blk) {  // (re)load W1's split tiles once the previous MMAs are done with B
                     if (it > 0) tc::mbar_wait(hl_empty, (it - 1) & 1);
@@ -315,7 +333,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         const float u_eff = 3.0e-5f;
         for (long tile = t_begin + grp; tile < t_end; tile += 2) {
             const int it = (int)(tile - t_begin);
-            const int pair = (int)(tile / A.tiles_per_pair);
+            const int pair = pair_of(tile);
             const long t0 = (tile % A.tiles_per_pair) * 128;
             const int s = pair / a.kv_heads, h = pair % a.kv_heads;
             const int blk = a.layer * a.kv_heads + h;
@@ -409,7 +427,9 @@ int launch_gate_tc(const GateArgs& a, int nseq, const __nv_bfloat16* k_pre, __nv
     A.tiles_per_pair = (a.T + 127) / 128;
     A.total_tiles = A.tiles_per_pair * nseq * a.kv_heads;
     A.rope = rope_ws;
-    const int grid = (int)std::min<long>(num_sms(), A.total_tiles);
+    const int R = num_sms() / a.kv_heads;  // token-tile ranges per head
+    A.head_sched = R >= 1 && (long)nseq * A.tiles_per_pair >= R;
+    const int grid = A.head_sched ? R * a.kv_heads : (int)std::min<long>(num_sms(), A.total_tiles);
     gate_tc_kernel<<<grid, G_THREADS, G_SMEM, st>>>(tw, tk, tpost, A, k_pre, k_post, g, bits, cand, pcnt);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
