@@ -324,3 +324,52 @@ __device__ __forceinline__ void mma8_ts_vmn_w(uint32_t d_tmem, uint32_t a_tmem, 
 }
 }  // namespace tc
 }  // namespace wgkv
+
+namespace wgkv {
+namespace tc {
+// 8 K16 steps of an SS MMA over a K = 128 operand pair whose SW128 K-major
+// sub-tiles (64 of K) are `a_sub16` / `b_sub16` descriptor units (16 bytes)
+// apart: one elect.sync, descriptors advanced by immediates; accumulate from
+// the second step (the first step overwrites D)
+template <int A_SUB16, int B_SUB16>
+__device__ __forceinline__ void mma8_ss_k128_w(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc) {
+    asm volatile(
+        "{\n.reg .pred e;\n.reg .b64 a, b;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n"
+        "add.s64 a, %1, 2;\n add.s64 b, %2, 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 4;\n add.s64 b, %2, 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, 6;\n add.s64 b, %2, 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, %4;\n add.s64 b, %2, %5;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, %4 + 2;\n add.s64 b, %2, %5 + 2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, %4 + 4;\n add.s64 b, %2, %5 + 4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "add.s64 a, %1, %4 + 6;\n add.s64 b, %2, %5 + 6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a0), "l"(b0), "r"(idesc), "n"(A_SUB16), "n"(B_SUB16));
+}
+// 4 K16 steps of a TS MMA: A from TMEM at a_tmem + 8 kk, B MN-major advancing 128 units (2 KB) per step
+__device__ __forceinline__ void mma4_ts_vmn_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b0, uint32_t idesc,
+                                              uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred e, p;\n.reg .b64 b;\n.reg .b32 a;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "add.s32 a, %1, 8;\n add.s64 b, %2, 128;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 16;\n add.s64 b, %2, 256;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "add.s32 a, %1, 24;\n add.s64 b, %2, 384;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b0), "r"(idesc), "r"(acc));
+}
+}  // namespace tc
+}  // namespace wgkv
