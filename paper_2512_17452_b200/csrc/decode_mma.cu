@@ -356,9 +356,12 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             for (int k = 0; k < min(DNS, nmine); ++k) issue(k);
         }
         publish_plan();
-        // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d); rows >= gs are zero
+        // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d), split q = hi + lo into two
+        // bf16 halves (to ~2^-17 relative): row r < 8 holds hi, row r + 8 its lo, so
+        // the one m16 S MMA yields both halves' dots (gs <= 8) and the only score
+        // rounding left is the cache's own bf16 k; rows >= gs are zero
         // (computed while the first pages of the item are in flight)
-        for (int e = tid; e < 16 * (d / 2); e += blockDim.x) {
+        for (int e = tid; e < 8 * (d / 2); e += blockDim.x) {
             const int r = e / (d / 2), i = e % (d / 2);
             float y0 = 0.f, y1 = 0.f;
             if (r < gs) {
@@ -369,11 +372,14 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                 y0 = (x0 * c - x1 * sn) * qs;
                 y1 = (x0 * sn + x1 * c) * qs;
             }
-            Qs[r * QROW + 2 * i] = __float2bfloat16_rn(y0);
-            Qs[r * QROW + 2 * i + 1] = __float2bfloat16_rn(y1);
+            const __nv_bfloat16 h0 = __float2bfloat16_rn(y0), h1 = __float2bfloat16_rn(y1);
+            Qs[r * QROW + 2 * i] = h0;
+            Qs[r * QROW + 2 * i + 1] = h1;
+            Qs[(r + 8) * QROW + 2 * i] = __float2bfloat16_rn(y0 - __bfloat162float(h0));
+            Qs[(r + 8) * QROW + 2 * i + 1] = __float2bfloat16_rn(y1 - __bfloat162float(h1));
         }
         __syncthreads();
-        // Q A-fragments: 8 k-steps of 16 dims (rows 0..15, only < gs nonzero)
+        // Q A-fragments: 8 k-steps of 16 dims (rows 0..7 hi, 8..15 lo, only heads < gs nonzero)
         uint32_t qa[8][4];
         {
             const uint32_t qb = smem_u32(Qs);
@@ -405,6 +411,11 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                 ldsm_x4(swz(kb + (kk >> 2) * 2048u, tok, dch), b0, b1, b2, b3);
                 mma16816(sc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
                 mma16816(sc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+            }
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {  // head lane/4: hi.k (row lane/4) + lo.k (row lane/4 + 8)
+                sc[nt][0] += sc[nt][2];
+                sc[nt][1] += sc[nt][3];
             }
             if (valid < 16) {  // partial page: token = nt*8 + t0 + e
 #pragma unroll

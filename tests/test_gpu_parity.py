@@ -163,7 +163,9 @@ def _session_case(W, orc, *, T, steps, hq, hkv, Wn, nseq, dtype, seed, w_std=0.1
             a, r = s.gather(0, b, h), refs[b].gather(0, h)
             assert np.array_equal(a["global_pos"], r["global_pos"])
             assert np.array_equal(a["local_pos"], r["local_pos"])
-            assert rel_err(a["global_v"], r["global_v"]) < 1e-2
+            assert np.shape(a["global_v"]) == np.shape(r["global_v"])
+            if np.size(r["global_v"]):  # an empty Global cache (nothing admitted yet) has nothing to compare
+                assert rel_err(a["global_v"], r["global_v"]) < 1e-2
     return s
 
 
