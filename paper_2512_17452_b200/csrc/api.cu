@@ -217,7 +217,8 @@ struct wgkv_ctx {
     float* ws_part = nullptr;
     int* ws_nchunks = nullptr;
     int* ws_tokpos = nullptr;  // [S*H] the new token's position per (seq, kv head) (deferred append)
-    AppendWork wk{};           // split-append scratch (append.cuh)
+    AppendWork wk{};           // split-append scratch (append.cuh); next / event / slot are [2][S*H]
+    FusedWork fw{};            // fused decode layer scratch (fused.cuh), parity-split halves as [2][...]
     // non-deferred decode: the append's gate CTAs run on gate_stream, forked after
     // the route kernel and joined after the attention of the same layer call
     cudaStream_t gate_stream = nullptr;
@@ -376,16 +377,26 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->near_cap = 1 << 20;
     ctx->ws_near = dalloc<int64_t>((size_t)ctx->near_cap, o);
     const int gs = c.q_heads / c.kv_heads;
-    ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2), o);
+    // (+4: the fused layer's bulk copies round a pair's partials up to 16 bytes)
+    ctx->ws_part = dalloc<float>((size_t)S * H * ctx->max_chunks * gs * (d + 2) + 4, o);
     // per-pair chunk counts | work-stealing counter | per-pair merge counters
     ctx->ws_nchunks = dalloc<int>(2 * (size_t)S * H + 1, o);
     ctx->ws_tokpos = dalloc<int>((size_t)S * H, o);
     ctx->wk.terms = dalloc<double>((size_t)S * H * c.hidden, o);
     ctx->wk.count = dalloc<int>((size_t)S * H, o);
-    ctx->wk.slot = dalloc<int>((size_t)S * H, o);
-    ctx->wk.event = dalloc<int>((size_t)S * H, o);
-    ctx->wk.next = dalloc<HeadState>((size_t)S * H, o);
+    // route outputs: two halves by layer parity (fused layer, fused.cuh)
+    ctx->wk.slot = dalloc<int>(2 * (size_t)S * H, o);
+    ctx->wk.event = dalloc<int>(2 * (size_t)S * H, o);
+    ctx->wk.next = dalloc<HeadState>(2 * (size_t)S * H, o);
     ctx->wk.pos = dalloc<int>((size_t)S * H, o);
+    ctx->fw.cnt_items = dalloc<int>((size_t)S * H, o);
+    ctx->fw.cnt_kv = dalloc<int>(2 * (size_t)S * H, o);
+    ctx->fw.cnt_gw = dalloc<int>(2 * (size_t)S * H, o);
+    ctx->fw.cnt_gate = dalloc<int>((size_t)S * H, o);
+    ctx->fw.g = dalloc<double>((size_t)S * H, o);
+    ctx->fw.pub = dalloc<int>(2 * (size_t)S * H, o);
+    ctx->fw.started = dalloc<int>(2, o);
+
     if (c.topk_budget > 0) {
         ctx->ws_score = dalloc<float>((size_t)S * c.q_heads * n_gp, o);
         ctx->ws_sel = dalloc<int32_t>((size_t)S * c.q_heads * n_gp, o);
@@ -415,6 +426,14 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     cudaMemset(pv.state, 0, sizeof(HeadState) * (size_t)L * S * H);
     cudaMemset(ctx->ws_nchunks, 0, sizeof(int) * (2 * (size_t)S * H + 1));  // K5 work counter starts at 0
     cudaMemset(ctx->wk.count, 0, sizeof(int) * (size_t)S * H);              // split-append arrivals
+    if (ctx->fw.cnt_items) {  // fused-layer counters start at 0 (each is reset by its last user)
+        cudaMemset(ctx->fw.cnt_items, 0, sizeof(int) * (size_t)S * H);
+        cudaMemset(ctx->fw.cnt_kv, 0, sizeof(int) * 2 * (size_t)S * H);
+        cudaMemset(ctx->fw.cnt_gw, 0, sizeof(int) * 2 * (size_t)S * H);
+        cudaMemset(ctx->fw.cnt_gate, 0, sizeof(int) * (size_t)S * H);
+        cudaMemset(ctx->fw.pub, 0, sizeof(int) * 2 * (size_t)S * H);
+        cudaMemset(ctx->fw.started, 0, sizeof(int) * 2);
+    }
     // zeroed pages: K3/K5 may stream stale slots of a partially filled page
     // (masked out), which must at least be finite
     cudaMemset(pv.data, 0, (size_t)cap * 2 * ps * d * ctx->esz);
@@ -921,6 +940,17 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     fin.forced_g = forced_g;
     fin.tr = tr;
     fin.wk = ctx->wk;
+    {  // this layer's parity halves (a fused launch may start before the previous layer's drained)
+        const size_t SH = (size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads, par = (size_t)(layer & 1) * SH;
+        fin.wk.slot += par;
+        fin.wk.event += par;
+        fin.wk.next += par;
+        fin.fw = ctx->fw;
+        fin.fw.cnt_kv += par;
+        fin.fw.cnt_gw += par;
+        fin.fw.pub += par;
+        fin.fw.started += layer & 1;
+    }
     // the append's gate CTAs on a side stream forked before K5 and joined after
     // the finish kernel (WGKV_GATE_PLACE=side): they need nothing K5 produces
     static const char* gp_env = getenv("WGKV_GATE_PLACE");

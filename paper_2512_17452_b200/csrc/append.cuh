@@ -104,6 +104,82 @@ __device__ __forceinline__ void append_arrive(const PoolView& pv, const GateArgs
 }
 
 // ---------------------------------------------------------------------------
+// the routing decision of one new token (thread 0): lazy promotion of the ring
+// victim on its stored bit, device page allocation, the victim's metadata copy
+// into Global and the new token's position in its slot (kvstore.cpp:102-158)
+// ---------------------------------------------------------------------------
+struct RouteDecision {
+    int ev;     // promotion event (0 none, 1 promoted, 2 dropped, -1 failed)
+    int gpage;  // promoted victim's Global page / slot
+    int gslot;
+    int npage;  // the new token's ring page / slot (npage < 0: failed)
+    int nslot;
+    HeadState ns;  // the head state after the append
+};
+__device__ __forceinline__ RouteDecision route_decide(const PoolView& pv, long hidx, const HeadState& st, long W,
+                                                      int lp0) {
+    const int ps = pv.page_size;
+    const long pos = st.tokens_seen;
+    const int slot = st.local_ptr;
+    const bool ring_full = st.local_len >= W;
+    int lp = lp0;
+    int ev = 0, vp = -1, gp = -1, gs_ = 0;
+    HeadState ns = st;
+    // the Global tail page (needed if the victim is promoted into a partly
+    // filled page), loaded alongside
+    const int gi = st.global_len;
+    const int gp_tail = (gi % ps != 0) ? pv.gpt[hidx * pv.n_gp + gi / ps] : -1;
+    // an allocation failure behaves like the reference's throw from
+    // alloc_page inside local_write (kvstore.cpp:23-31, 102-158): nothing of
+    // this head changes, the error is latched, the event reads -1
+    bool fail = false;
+    if (!ring_full) {
+        // not full: slot == local_len; a slot at a page boundary is the first
+        // touch of that ring page (kvstore.cpp:102-107)
+        if (slot % ps == 0) {
+            lp = pool_pop(pv);
+            if (lp >= 0) pv.lpt[hidx * pv.n_lp + slot / ps] = lp;
+        }
+        fail = lp < 0;
+        if (!fail) ns.local_len += 1;
+    } else if (lp < 0) {
+        fail = true;  // the head lost its pages to an earlier ENOPAGES
+    } else if (pv.adm[(size_t)lp * ps + slot % ps]) {
+        // the victim under local_ptr is admitted: promote (kvstore.cpp:122-147)
+        gp = gp_tail;
+        if (gi % ps == 0) {
+            gp = pool_pop(pv);
+            if (gp >= 0) pv.gpt[hidx * pv.n_gp + gi / ps] = gp;
+        }
+        if (gp < 0) {
+            fail = true;
+        } else {
+            ev = 1;
+            vp = lp;
+            gs_ = gi % ps;
+            ns.global_len += 1;
+        }
+    } else {
+        ev = 2;  // dropped
+    }
+    if (fail) {
+        ev = -1;
+        lp = -1;
+    } else {
+        ns.local_ptr = (int)((st.local_ptr + 1) % W);
+        ns.tokens_seen += 1;
+    }
+    if (ev == 1) {  // the victim's metadata, read before the new token overwrites the slot
+        const size_t a = (size_t)vp * ps + slot % ps, b = (size_t)gp * ps + gs_;
+        pv.gate[b] = pv.gate[a];
+        pv.pos[b] = pv.pos[a];
+        pv.adm[b] = pv.adm[a];
+    }
+    if (lp >= 0) pv.pos[(size_t)lp * ps + slot % ps] = (int32_t)pos;
+    return RouteDecision{ev, gp, gs_, lp, slot % ps, ns};
+}
+
+// ---------------------------------------------------------------------------
 // route CTA: RoPE, lazy promotion, ring write (no gate)
 // ---------------------------------------------------------------------------
 template <typename E>
@@ -119,7 +195,7 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
     const int tid = threadIdx.x, d = pv.head_dim, ps = pv.page_size;
     const long hidx = pv.head_index(layer, seq0 + s, h);
     const int pair = (seq0 + s) * pv.kv_heads + h;
-    __shared__ int vpage, vslot, gpage, gslot, npage, nslot, event;
+    __shared__ int gpage, gslot, npage, nslot, event;
     const size_t in = ((size_t)s * pv.kv_heads + h) * d;
     E* pool = reinterpret_cast<E*>(pv.data);
     // the new token's inputs do not depend on the cache state: loads first;
@@ -146,74 +222,19 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
         rope_pair_f32(x0, x1, c, sn, y0, y1);
     }
     if (tid == 0) {
-        int lp = lp0;
-        int ev = 0, vp = -1, gp = -1, gs_ = 0;
-        HeadState ns = st;
-        // the Global tail page (needed if the victim is promoted into a partly
-        // filled page), loaded alongside
-        const int gi = st.global_len;
-        const int gp_tail = (gi % ps != 0) ? pv.gpt[hidx * pv.n_gp + gi / ps] : -1;
-        // an allocation failure behaves like the reference's throw from
-        // alloc_page inside local_write (kvstore.cpp:23-31, 102-158): nothing of
-        // this head changes, the error is latched, the event reads -1
-        bool fail = false;
-        if (!ring_full) {
-            // not full: slot == local_len; a slot at a page boundary is the first
-            // touch of that ring page (kvstore.cpp:102-107)
-            if (slot % ps == 0) {
-                lp = pool_pop(pv);
-                if (lp >= 0) pv.lpt[hidx * pv.n_lp + slot / ps] = lp;
-            }
-            fail = lp < 0;
-            if (!fail) ns.local_len += 1;
-        } else if (lp < 0) {
-            fail = true;  // the head lost its pages to an earlier ENOPAGES
-        } else if (pv.adm[(size_t)lp * ps + slot % ps]) {
-            // the victim under local_ptr is admitted: promote (kvstore.cpp:122-147)
-            gp = gp_tail;
-            if (gi % ps == 0) {
-                gp = pool_pop(pv);
-                if (gp >= 0) pv.gpt[hidx * pv.n_gp + gi / ps] = gp;
-            }
-            if (gp < 0) {
-                fail = true;
-            } else {
-                ev = 1;
-                vp = lp;
-                gs_ = gi % ps;
-                ns.global_len += 1;
-            }
-        } else {
-            ev = 2;  // dropped
-        }
-        if (fail) {
-            ev = -1;
-            lp = -1;
-        } else {
-            ns.local_ptr = (int)((st.local_ptr + 1) % W);
-            ns.tokens_seen += 1;
-        }
-        event = ev;
-        vpage = vp;
-        vslot = slot % ps;
-        gpage = gp;
-        gslot = gs_;
-        npage = lp;
-        nslot = slot % ps;
-        wk.next[pair] = ns;
-        wk.event[pair] = ev;
+        const RouteDecision r = route_decide(pv, hidx, st, W, lp0);
+        event = r.ev;
+        gpage = r.gpage;
+        gslot = r.gslot;
+        npage = r.npage;
+        nslot = r.nslot;
+        wk.next[pair] = r.ns;
+        wk.event[pair] = r.ev;
         if (wk.early_state) {
             wk.pos[pair] = (int)pos;
-            if (ev >= 0) pv.state[hidx] = ns;
+            if (r.ev >= 0) pv.state[hidx] = r.ns;
         }
-        wk.slot[pair] = lp >= 0 ? lp * ps + slot % ps : -1;
-        if (ev == 1) {  // the victim's metadata, read before the new token overwrites the slot
-            const size_t a = (size_t)vp * ps + slot % ps, b = (size_t)gp * ps + gs_;
-            pv.gate[b] = pv.gate[a];
-            pv.pos[b] = pv.pos[a];
-            pv.adm[b] = pv.adm[a];
-        }
-        if (lp >= 0) pv.pos[(size_t)lp * ps + slot % ps] = (int32_t)pos;
+        wk.slot[pair] = r.npage >= 0 ? r.npage * ps + r.nslot : -1;
     }
     __syncthreads();
     if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -231,8 +252,6 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
         }
         if (et) kd[tid + (size_t)ps * d] = vnew;
     }
-    (void)vpage;
-    (void)vslot;
 }
 
 // ---------------------------------------------------------------------------
@@ -247,7 +266,7 @@ __device__ __forceinline__ void append_route(const PoolView& pv, const GateArgs&
 template <typename E>
 __device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s,
                                                  int h, int j, const E* __restrict__ k_pre, const AppendWork& wk,
-                                                 uint8_t* smem, bool pdl_wait = false) {
+                                                 uint8_t* smem, bool pdl_wait = false, bool early_pos = false) {
     const int tid = threadIdx.x, d = pv.head_dim, fd = 2 * d, hid = ga.hidden;
     const int pair = (seq0 + s) * pv.kv_heads + h;
     const int blk = layer * pv.kv_heads + h;
@@ -262,16 +281,37 @@ __device__ __forceinline__ void append_gate_part(const PoolView& pv, const GateA
         ws[r * (fd + 1) + 2 * c2] = w.x;
         ws[r * (fd + 1) + 2 * c2 + 1] = w.y;
     }
-    if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     // the state is published only by the pair's last arrival: tokens_seen is the new token's position
     // (split launch: the route CTA published it already and left the position in wk.pos)
-    const long pos = wk.early_state ? (long)wk.pos[pair] : pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
+    auto position = [&]() -> long {
+        return wk.early_state ? (long)wk.pos[pair] : pv.state[pv.head_index(layer, seq0 + s, h)].tokens_seen;
+    };
+    // early_pos (K5 launch whose predecessor is another layer's: this layer's
+    // state is final): the fp64 angles' cos / sin before the wait, off the path
+    double* cs = ws + kGateUnits * (fd + 1);  // [d/2][2] (early_pos)
+    if (early_pos) {
+        const long pos = position();
+        for (int i = tid; i < d / 2; i += blockDim.x) {
+            const double angle = __dmul_rn((double)pos, ga.freq[i]);
+            cs[2 * i] = cos(angle);
+            cs[2 * i + 1] = sin(angle);
+        }
+    }
+    if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const long pos = early_pos ? 0 : position();
     const size_t in = ((size_t)s * pv.kv_heads + h) * d;
     // the feature in the reference's arithmetic (numerics.cpp:53-62)
     for (int i = tid; i < d / 2; i += blockDim.x) {
         const double a = to_f(k_pre[in + 2 * i]), b = to_f(k_pre[in + 2 * i + 1]);
-        const double angle = __dmul_rn((double)pos, ga.freq[i]);
-        const double cd = cos(angle), sd = sin(angle);
+        double cd, sd;
+        if (early_pos) {
+            cd = cs[2 * i];
+            sd = cs[2 * i + 1];
+        } else {
+            const double angle = __dmul_rn((double)pos, ga.freq[i]);
+            cd = cos(angle);
+            sd = sin(angle);
+        }
         xs[2 * i] = a;
         xs[2 * i + 1] = b;
         xs[d + 2 * i] = __dsub_rn(__dmul_rn(a, cd), __dmul_rn(b, sd));

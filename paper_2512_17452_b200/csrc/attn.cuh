@@ -1,6 +1,7 @@
 // attn.cuh -- K3 / K5 argument blocks and launchers.
 #pragma once
 #include "append.cuh"
+#include "fused.cuh"
 #include "common.cuh"
 #include "gate.cuh"
 
@@ -52,6 +53,11 @@ struct DecArgs {
     int early_trigger;  // K5 releases its programmatic dependent right after its PDL wait
     int state_in_smem;  // K5 keeps every pair's HeadState in shared memory (fits for <= kDecSmemStatePairs)
     int prewait;        // K5's predecessor is another layer's finish kernel: plan before the PDL wait
+    // fused layer (fused.cuh, small batches): the launch also carries the
+    // append's route CTAs (first n_route_ctas) and merges + commits in place of
+    // the finish kernel
+    int fused;
+    int n_route_ctas;
 };
 
 // K6: select_topk_pages + per-q-head attention over the selection (topk.cu).
@@ -73,6 +79,8 @@ struct FinishArgs {
     AppendWork wk;
     bool prewait;  // K5 may plan and start its first loads before the PDL wait (see api.cu)
     bool gate_side;  // the append's gate CTAs run in their own launch on a side stream
+    FusedWork fw;    // fused layer scratch (this layer's parity halves); cnt_items null = not available
+    __nv_bfloat16* out;  // fused layer: the attention output [nseq][q_heads][d] (set by the launcher)
 };
 
 // counter_reset_by_append: the kernel just before on the stream zeroed the work

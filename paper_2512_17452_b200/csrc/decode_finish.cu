@@ -16,6 +16,7 @@
 //     victim slot, i.e. now.
 // Both roles run concurrently, so K4 costs no extra step on the layer's path.
 #include "attn.cuh"
+#include "timeline.cuh"
 
 namespace wgkv {
 
@@ -25,6 +26,8 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
                                                                        __nv_bfloat16* __restrict__ out, FinishArgs fin,
                                                                        int ncomb) {
     extern __shared__ __align__(16) uint8_t fsm[];
+    TL_DECL
+    TL_MARK(0);
     // the next kernel on the stream may launch now; it waits for our completion
     asm volatile("griddepcontrol.launch_dependents;");
     const int tid = threadIdx.x;
@@ -39,12 +42,14 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         const int s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
         append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, fsm);
         append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, arrivals);
+        TL_COMMIT(3, a.layer, 0);
         return;
     }
     if ((int)blockIdx.x >= ngate + ncomb) {  // ---- route CTAs of the append (K4, append.cuh)
         // reads and routing run while K5 streams; the ring-slot stores wait for it
         append_role<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, a.window, a.n_pairs, blockIdx.x - ngate - ncomb,
                                    0, arrivals, fin.k_new, fin.v_new, fin.forced_g, fin.tr, fin.wk, fsm, true);
+        TL_COMMIT(4, a.layer, 0);
         return;
     }
     // ---- combine role: one (seq, q head) --------------------------------------
@@ -61,6 +66,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     float* wacc = wl + NW;                       // [NW][d]
     // K5 has finished: partials written
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    TL_MARK(2);
     if (sp == 0 && tid == 0) *a.counter = 0;  // K5's work counter, for the next launch
     const int nch = min(a.nchunks[bh], kMaxChunks);
     float m = -INFINITY, l = 0.f;
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         }
         out[((size_t)s * a.q_heads + p) * d + e] = __float2bfloat16_rn(t / L);
     }
+    TL_COMMIT(1, a.layer, nch);
 }
 
 int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, const float* part, __nv_bfloat16* out,
@@ -171,3 +178,5 @@ int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, con
 }
 
 }  // namespace wgkv
+
+TL_EXPORT(wgkv_tl_fin)

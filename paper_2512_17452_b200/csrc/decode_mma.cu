@@ -17,6 +17,8 @@
 
 #include "attn.cuh"
 #include "tc.cuh"
+#include "timeline.cuh"
+#include "fused.cuh"
 
 namespace wgkv {
 
@@ -43,6 +45,20 @@ constexpr int PID_CAP = kDecPidCap;  // pages per work item (staged page ids)
 #define WGKV_GATE_K5_MAX 64
 #endif
 constexpr int kGateInK5MaxCtas = WGKV_GATE_K5_MAX;  // gate CTAs carried by the K5 launch at most
+#ifndef WGKV_K5_PARAM_WARM
+#define WGKV_K5_PARAM_WARM 0
+#endif
+#ifndef WGKV_K5_EVICT_FIRST
+#define WGKV_K5_EVICT_FIRST 0
+#endif
+#ifndef WGKV_FUSED_MAX_FRONT
+#define WGKV_FUSED_MAX_FRONT 148
+#endif
+constexpr int kFusedMaxFront = WGKV_FUSED_MAX_FRONT;  // fused layer: route + gate CTAs at most
+#ifndef WGKV_FUSED_MAX_PAIRS
+#define WGKV_FUSED_MAX_PAIRS 8
+#endif
+constexpr int kFusedMaxPairs = WGKV_FUSED_MAX_PAIRS;  // fused layer: (seq, kv head) pairs at most
 #ifndef WGKV_K5_IPC
 #define WGKV_K5_IPC 3  // work items per CTA (work stealing balance vs per-item fixed costs; 3 beats 2 by
                        // 1.5 % at 128K x 4 and 2.2 % on the serving mix with 6-warp CTAs)
@@ -83,6 +99,16 @@ __device__ __forceinline__ float ex2f(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    return x;
+}
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, off));
+    return x;
+}
 // address of the 16-byte chunk (row, chunk 0..7) of a [rows][64] SW128 tile
 __device__ __forceinline__ uint32_t swz(uint32_t base, uint32_t row, uint32_t chunk) {
     return base + row * 128u + ((chunk ^ (row & 7u)) << 4);
@@ -90,36 +116,242 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, uint32_t row, uint32_t ch
 
 }  // namespace
 
+// fused layer (fused.cuh): the last item of pair bh merges the pair's nc chunk
+// partials (m in natural-log units, l, unnormalised O) with the new token --
+// logit RoPE(q) . bf16(RoPE(k_new)) / sqrt(d) with q from Qs (hi rows 0..7 +
+// lo rows 8..15, pre-scaled by log2(e)/sqrt(d)), weight on v_new -- into the
+// output rows of the pair's gs q heads.  The pair's partials (contiguous) come
+// in by one bulk copy into the idle ring.  The last warp forms the new key and
+// value, then -- off the merge's path, since the commit needs only that every
+// item of the pair is done -- arrives for the merge party and, when last,
+// commits the append; warps 0..DW-2 merge.  This code runs once per pair and
+// launch, i.e. with a cold instruction cache (ncu: stall_no_instruction leads
+// the small-batch K5): it is kept short -- rolled loops, one instantiation.
+__device__ __forceinline__ void fused_tail(const DecArgs& a, const FinishArgs& fin, int bh, int nc, long pos,
+                                           const __nv_bfloat16* Qs, uint8_t* scratch, const float* __restrict__ part,
+                                           uint64_t* tbar, uint32_t& tpar TL_PARAM) {
+    constexpr int d = 128, NM = (DW - 1) * 32;  // merging threads
+    constexpr int RING = DW * DNS * PAGE_B;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gs = a.q_heads / a.pv.kv_heads;
+    const int s = bh / a.pv.kv_heads, h = bh % a.pv.kv_heads;
+    const int pairg = a.seq0 * a.pv.kv_heads + bh;
+    const size_t o = (size_t)bh;  // = s * kv_heads + h
+    const int pstride = gs * (d + 2);
+    const float* pb = part + (size_t)bh * a.max_chunks * pstride;
+    float* kn = reinterpret_cast<float*>(scratch);  // [d] the new key as cached
+    float* vn = kn + d;                              // [d] the new value
+    float* acc = vn + d;                             // [gs][d] (several batches)
+    float* wgt = acc + gs * d;                       // [nc][gs] chunk weights
+    const int rows_off = ((2 * d + gs * d + nc * gs) * 4 + 127) & ~127;
+    float* rows = reinterpret_cast<float*>(scratch + rows_off);  // [cb][pstride] a batch of partials
+    const int cap = (RING - rows_off) / (pstride * 4);             // chunks per batch
+    __shared__ float s_L[8], s_wn[8];
+    // a batch of chunks -> rows: one bulk copy (the partial buffer has 16 B of
+    // slack past its end for the rounding) by thread 0, which holds the item
+    // counter's acquire
+    auto load_batch = [&](int c0, int cb) {
+        if (tid == 0) {
+            const uint32_t bytes = ((uint32_t)(cb * pstride) * 4u + 15u) & ~15u;
+            tc::fence_proxy_async_global();
+            tc::fence_proxy_async_smem();  // the CTA's generic use of the ring (after a barrier) first
+            tc::mbar_arrive_expect_tx(tbar, bytes);
+            tc::bulk_load(rows, pb + (size_t)c0 * pstride, bytes, tbar);
+        }
+    };
+    load_batch(0, min(nc, cap));
+    if (warp == DW - 1) {
+        const size_t io = o * d;
+        const float v0 = __bfloat162float(fin.v_new[io + lane]), v1 = __bfloat162float(fin.v_new[io + lane + 32]),
+                    v2 = __bfloat162float(fin.v_new[io + lane + 64]), v3 = __bfloat162float(fin.v_new[io + lane + 96]);
+        const __nv_bfloat162 k0 = reinterpret_cast<const __nv_bfloat162*>(fin.k_new + io)[lane];
+        const __nv_bfloat162 k1 = reinterpret_cast<const __nv_bfloat162*>(fin.k_new + io)[lane + 32];
+        vn[lane] = v0;
+        vn[lane + 32] = v1;
+        vn[lane + 64] = v2;
+        vn[lane + 96] = v3;
+#pragma unroll 1
+        for (int j = 0; j < 2; ++j) {  // the key as it is cached: fp64 angle, fp32 rotation, bf16
+            const int i = lane + 32 * j;
+            const float2 kx = __bfloat1622float2(j ? k1 : k0);
+            float c, sn, y0, y1;
+            rope_cs(a.freq, i, pos, c, sn);
+            rope_pair_f32(kx.x, kx.y, c, sn, y0, y1);
+            kn[2 * i] = __bfloat162float(__float2bfloat16_rn(y0));
+            kn[2 * i + 1] = __bfloat162float(__float2bfloat16_rn(y1));
+        }
+    } else {
+        tc::mbar_wait(tbar, tpar);
+    }
+    tpar ^= 1u;
+    __syncthreads();
+    TL_MARK(3);
+    if (warp == DW - 1) {
+        // ---- the merge's arrival for the K/V commit (every item is done) and, when last, the commit
+        const bool last = __shfl_sync(0xffffffffu, lane == 0 ? (int)pair_arrive(&fin.fw.cnt_kv[pairg]) : 0, 0);
+        if (last)
+            fused_commit_kv<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.k_new, fin.v_new, fin.forced_g,
+                                           fin.tr, fin.wk, fin.fw, kn, vn);
+        return;
+    }
+    const bool single = nc <= cap;
+    // per head (a warp each): the new token's logit, the max, chunk weights, the denominator
+#pragma unroll 1
+    for (int g = warp; g < gs; g += DW - 1) {
+        float dot = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = 4 * lane + j;
+            dot = fmaf(__bfloat162float(Qs[g * QROW + i]) + __bfloat162float(Qs[(g + 8) * QROW + i]), kn[i], dot);
+        }
+        const float mn = warp_sum(dot) * 0.6931471805599453f;  // log2 units -> natural
+        float M = mn;
+#pragma unroll 1
+        for (int c = lane; c < nc; c += 32) {
+            const float* r = (single ? rows : pb) + (size_t)c * pstride + (size_t)g * (d + 2) + d;
+            const float m = single ? r[0] : __ldcg(r);
+            wgt[c * gs + g] = m;
+            M = fmaxf(M, m);
+        }
+        M = warp_max(M);
+        float L = 0.f;
+#pragma unroll 1
+        for (int c = lane; c < nc; c += 32) {
+            const float* r = (single ? rows : pb) + (size_t)c * pstride + (size_t)g * (d + 2) + d + 1;
+            const float m = wgt[c * gs + g], w = m == -INFINITY ? 0.f : __expf(m - M);
+            wgt[c * gs + g] = w;
+            L = fmaf(w, single ? r[0] : __ldcg(r), L);
+        }
+        L = warp_sum(L);
+        if (lane == 0) {
+            s_wn[g] = __expf(mn - M);
+            s_L[g] = L + s_wn[g];
+        }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NM) : "memory");  // merging warps only
+    TL_MARK(4);
+#pragma unroll 1
+    for (int c0 = 0; c0 < nc; c0 += cap) {
+        const int cb = min(cap, nc - c0);
+        if (c0 > 0) {  // the next batch (many chunks of a wide group)
+            asm volatile("bar.sync 1, %0;" ::"n"(NM) : "memory");
+            load_batch(c0, cb);
+            tc::mbar_wait(tbar, tpar);
+            tpar ^= 1u;
+        }
+#pragma unroll 1
+        for (int e = tid; e < gs * (d / 2); e += NM) {  // (head, column pair)
+            const int g = e / (d / 2), col = 2 * (e - g * (d / 2));
+            const float2* r = reinterpret_cast<const float2*>(rows + (size_t)g * (d + 2) + col);
+            const float* w = wgt + (size_t)c0 * gs + g;
+            float2 t = c0 == 0 ? make_float2(s_wn[g] * vn[col], s_wn[g] * vn[col + 1])
+                               : reinterpret_cast<const float2*>(acc)[e];
+#pragma unroll 4
+            for (int c = 0; c < cb; ++c) {
+                const float wc = w[c * gs];
+                const float2 x = r[(size_t)c * (pstride / 2)];
+                t.x = fmaf(wc, x.x, t.x);
+                t.y = fmaf(wc, x.y, t.y);
+            }
+            if (c0 + cb < nc) {
+                reinterpret_cast<float2*>(acc)[e] = t;
+            } else {
+                const float il = 1.f / s_L[g];
+                *reinterpret_cast<__nv_bfloat162*>(fin.out + ((size_t)s * a.q_heads + h * gs + g) * d + col) =
+                    __floats2bfloat162_rn(t.x * il, t.y * il);
+            }
+        }
+    }
+    TL_MARK(5);
+}
+
 // TOPK: the Global part of each (seq, kv head) is K6's union selection
 // (a.sel / a.nsel: logical page | q-head mask << 24) instead of every page;
 // rows (q heads) that did not select a page get -inf logits for it.
 template <bool TOPK>
 __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __grid_constant__ CUtensorMap tpool,
-                                                                      DecArgs a, const __nv_bfloat16* __restrict__ q,
+                                                                      const __grid_constant__ DecArgs a,
+                                                                      const __nv_bfloat16* __restrict__ q,
                                                                       float* __restrict__ part,
                                                                       int* __restrict__ nchunks,
                                                                       int* __restrict__ work_counter,
                                                                       const __grid_constant__ FinishArgs fin) {
     extern __shared__ uint8_t dsm_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned, by pointer arithmetic on the __shared__ array (an integer round
+    // trip would lose the address space: every access through sm would be generic)
+    uint8_t* sm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
     constexpr int d = 128;
     const int ps = 16;
     const int gs = a.q_heads / a.pv.kv_heads;
     const int npairs = a.n_pairs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (!TOPK && (int)blockIdx.x < a.n_gate_ctas) {
+    TL_DECL
+    TL_MARK(0);
+#if WGKV_K5_PARAM_WARM
+    {  // this launch's parameters into the SM's constant cache (a new block every
+       // launch): the roles' first touches of them would otherwise be serial L2
+       // round trips on the layer's critical path
+        const uint32_t* pa = reinterpret_cast<const uint32_t*>(&a);
+        const uint32_t* pf = reinterpret_cast<const uint32_t*>(&fin);
+        uint32_t x = 0;
+        for (int i = tid * 16; i < (int)(sizeof(DecArgs) / 4); i += blockDim.x * 16) x ^= pa[i];
+        for (int i = tid * 16; i < (int)(sizeof(FinishArgs) / 4); i += blockDim.x * 16) x ^= pf[i];
+        asm volatile("" ::"r"(x));
+    }
+#endif
+#if WGKV_K5_EVICT_FIRST
+    const uint64_t l2pol = tc::policy_evict_first();  // the cache is streamed once per token step
+#endif
+    __shared__ int s_rlast;
+    if (!TOPK && (int)blockIdx.x < a.n_route_ctas) {
+        // fused layer: the append's route CTA (fused.cuh), before the PDL wait
+        // when the predecessor is another layer's launch
+        const int pr = blockIdx.x, s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
+        fused_route<__nv_bfloat16>(a.pv, a.layer, a.seq0, s, h, a.window, fin.wk, fin.fw, !a.prewait);
+        __syncthreads();  // the route's writes, then its arrivals (thread 0)
+        if (tid == 0) {
+            const int pairg = a.seq0 * a.pv.kv_heads + pr;
+            // last on either only after a party that passed the PDL wait: the
+            // commits' caller outputs then follow it too
+            s_rlast = (pair_arrive(&fin.fw.cnt_kv[pairg]) ? 1 : 0) |
+                      (!fin.forced_g && pair_arrive(&fin.fw.cnt_gw[pairg]) ? 2 : 0);
+            if (s_rlast) asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (s_rlast & 2) fused_commit_gate(a.pv, fin.ga, a.seq0, s, h, fin.tr, fin.wk, fin.fw);
+        }
+        __syncthreads();
+        if ((s_rlast & 1) && warp == 0)
+            fused_commit_kv<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.k_new, fin.v_new, fin.forced_g,
+                                           fin.tr, fin.wk, fin.fw, nullptr, nullptr);
+        TL_COMMIT(5, a.layer, 0);
+        return;
+    }
+    if (!TOPK && (int)blockIdx.x < a.n_route_ctas + a.n_gate_ctas) {
         // deferred append's gate CTAs (append.cuh): the new token's exact fp64
         // gate (engine.cpp:300-303) is only consumed W steps later (when the
         // token leaves the ring), so it runs beside the attention instead of
         // behind it; W1 is staged before the PDL wait
         const int gpp = gate_ctas_per_pair(fin.ga.hidden);
-        const int pr = blockIdx.x / gpp, j = blockIdx.x % gpp;
+        const int gb = blockIdx.x - a.n_route_ctas;
+        const int pr = gb / gpp, j = gb % gpp;
         const int s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
-        append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, sm, true);
-        append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, gpp + 1);
+        append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, sm, true,
+                                        a.prewait != 0);
+        if (a.fused) {
+            // the last gate CTA of the pair sums z2, then arrives for the gate group (fused.cuh)
+            const int pairg = a.seq0 * a.pv.kv_heads + pr;
+            if (fused_gate_arrive(a.pv, fin.ga, a.layer, pairg, h, fin.wk, fin.fw, sm)) {
+                __syncthreads();  // fw.g written (thread 0)
+                if (tid == 0 && pair_arrive(&fin.fw.cnt_gw[pairg]))
+                    fused_commit_gate(a.pv, fin.ga, a.seq0, s, h, fin.tr, fin.wk, fin.fw);
+            }
+        } else {
+            append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, gpp + 1);
+        }
+        TL_COMMIT(2, a.layer, 0);
         return;
     }
-    const int kcta = (int)blockIdx.x - a.n_gate_ctas, kgrid = (int)gridDim.x - a.n_gate_ctas;
+    const int nfront = a.n_route_ctas + a.n_gate_ctas;
+    const int kcta = (int)blockIdx.x - nfront, kgrid = (int)gridDim.x - nfront;
     // Launched as a programmatic dependent of the previous kernel (K4, the
     // previous layer's finish kernel, or K6's compaction).  Deferred path: the
     // predecessor (finish of another layer) owns only the shared workspace
@@ -134,6 +366,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
     auto pdl_wait = [&]() {
         if (waited) return;
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        TL_MARK(2);
         // let the kernel that merges our partials launch now (it waits for our completion)
         if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;");
         waited = true;
@@ -224,10 +457,19 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         }
         if (tid == 0) s_cp = cp;
     }
+    __shared__ __align__(8) uint64_t s_tbar;  // fused layer: the tail's bulk copies
+    uint32_t tpar = 0;
     if (tid < DW * DNS) tc::mbar_init(&full[tid], 1);
+    if (tid == DW * DNS) tc::mbar_init(&s_tbar, 1);
     tc::fence_barrier_init();
     __syncthreads();
     const int cp = s_cp, nitems = s_items;
+    TL_MARK(1);
+    // fused layer: this CTA has planned from the old head states (the result
+    // is only looked at when the CTA ends: the last planner publishes)
+    int planned_rank = 0;
+    if (!TOPK && a.fused && tid == 0) planned_rank = atomicAdd(fin.fw.started, 1);
+    int tl_items = 0;
     const float qs = rsqrtf((float)d) * 1.4426950408889634f;
     const float LN2 = 0.6931471805599453f;
     const uint32_t wring = smem_u32(ring) + warp * DNS * PAGE_B;
@@ -240,7 +482,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         pdl_wait();
         if (published) return;
         published = true;
-        if (kcta != 0) return;
+        if (kcta != 0 || a.fused) return;
         for (int p = tid; p < npairs; p += blockDim.x) {
             nchunks[p] = item_base[p + 1] - item_base[p];
             if (!TOPK && a.defer)
@@ -251,17 +493,29 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         }
     };
     __shared__ int s_item;
+    int next_draw = 0;  // fused layer: the next item's draw, claimed at the end of the previous item
     // first item static (kcta): no atomic round trip in front of it; later items
     // are stolen from kgrid on (the merging kernel resets the counter to 0 --
     // only read after the PDL wait, which the first item passes)
     for (int first = 1;; first = 0) {
-        if (tid == 0) s_item = first ? kcta : kgrid + atomicAdd(work_counter, 1);
+        if (tid == 0) {
+            if (first) {
+                s_item = kcta;
+            } else {
+                const int v = a.fused ? next_draw : atomicAdd(work_counter, 1);
+                s_item = kgrid + v;
+                // fused layer: no merging kernel follows; the last of the
+                // min(kgrid, nitems) + max(0, nitems - kgrid) draws resets it
+                if (a.fused && v == min(kgrid, nitems) + max(0, nitems - kgrid) - 1) *work_counter = 0;
+            }
+        }
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) {
             publish_plan();
             break;
         }
+        ++tl_items;
         // pair of this item: the last bh with item_base[bh] <= item (binary search)
         int bh = 0;
         for (int lo = 0, hi = npairs - 1; lo <= hi;) {
@@ -349,7 +603,11 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             tc::mbar_arrive_expect_tx(bar, PAGE_B);
             // one box per page: {64 dims, 16 slots, 2 dim halves, K and V} lands as
             // K lo | K hi | V lo | V hi, each a [16][64] SW128 sub-tile
+#if WGKV_K5_EVICT_FIRST
+            tc::tma_load_4d_hint(dst, &tpool, bar, 0, 0, 0, 2 * page, l2pol);
+#else
             tc::tma_load_4d(dst, &tpool, bar, 0, 0, 0, 2 * page);
+#endif
         };
         if (lane == 0) {
             tc::fence_proxy_async_smem();
@@ -504,8 +762,36 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                 pout[g * (d + 2) + d + 1] = L;
             }
         }
+        if (!TOPK && a.fused) {
+            // the next item is claimed now: the atomic's round trip overlaps
+            // the merge below instead of following it
+            if (tid == 0) next_draw = atomicAdd(work_counter, 1);
+            // the pair's last item merges its chunks and the new token; the
+            // last party of the pair commits the append (fused.cuh)
+            const int pairg = a.seq0 * a.pv.kv_heads + bh;
+            if (cta_arrive(&fin.fw.cnt_items[pairg], item_base[bh + 1] - item_base[bh])) {
+                TL_MARK(1);
+                tl_items += 1000;
+                fused_tail(a, fin, bh, item_base[bh + 1] - item_base[bh], pos, Qs, ring, part, &s_tbar, tpar TL_ARG);
+            }
+        }
         __syncthreads();
     }
+    if (!TOPK && a.fused) {
+        // the last CTA to plan: every CTA has read the old head states, so a
+        // committed pair's new state may be published (handshake, fused.cuh)
+        __shared__ int s_lastplan;
+        if (tid == 0) {
+            s_lastplan = planned_rank == kgrid - 1;
+            if (s_lastplan) *fin.fw.started = 0;
+        }
+        __syncthreads();
+        if (s_lastplan)
+            for (int p = tid; p < npairs; p += blockDim.x)
+                fused_pub(a.pv, fin.wk, fin.fw, a.layer, a.seq0 * a.pv.kv_heads + p);
+    }
+    TL_COMMIT(0, a.layer, tl_items);
+    (void)tl_items;
 }
 
 int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, float* part, int* nchunks,
@@ -531,7 +817,15 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         tp_cap = a.pv.capacity;
     }
     a.n_pairs = nseq * a.pv.kv_heads;
-    const size_t smem_cap = (size_t)(228 / CPS - 1) * 1024;
+    // CPS CTAs per SM: 228 KB per SM, 1 KB reserved per CTA, the kernels' static smem
+    static size_t static_smem = 0;
+    if (!static_smem) {
+        cudaFuncAttributes fa0{}, fa1{};
+        cudaFuncGetAttributes(&fa0, decode_attn_mma_kernel<false>);
+        cudaFuncGetAttributes(&fa1, decode_attn_mma_kernel<true>);
+        static_smem = std::max(fa0.sharedSizeBytes, fa1.sharedSizeBytes) + 1;
+    }
+    const size_t smem_cap = (size_t)(228 / CPS - 1) * 1024 - ((static_smem + 127) & ~size_t(127));
     size_t smem = 1024 + DW * DNS * PAGE_B + 16 * QROW * 2 + DW * DNS * 8 + 4 * ((size_t)a.n_pairs + 1) + 4 * PID_CAP;
     if (smem > smem_cap) return WGKV_ENOTSUP;
     // per-pair state cached in smem when it still fits CPS CTAs per SM
@@ -557,14 +851,33 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     static const bool no_trigger = getenv("WGKV_K5_NO_TRIGGER") != nullptr;  // A/B switch
     FinishArgs fa{};
     a.n_gate_ctas = 0;
-    if (fin && !fin->forced_g && !fin->gate_side && a.n_pairs * gate_ctas_per_pair(fin->ga.hidden) <= gate_k5_max) {
-        a.n_gate_ctas = a.n_pairs * gate_ctas_per_pair(fin->ga.hidden);
+    a.n_route_ctas = 0;
+    a.fused = 0;
+    const int ngate = fin && !fin->forced_g ? a.n_pairs * gate_ctas_per_pair(fin->ga.hidden) : 0;
+    // fused layer (fused.cuh): while the route and gate CTAs fit in half a wave
+    static const char* fu_env = getenv("WGKV_DECODE_FUSED");  // A/B switch: "0" off
+    static const int fused_max = fu_env ? atoi(fu_env) : kFusedMaxFront;
+    int kgrid = CPS * num_sms();
+    // few pairs and narrow groups only: with more pairs (several items per CTA)
+    // the per-item arrivals and the one-CTA merges cost more than a second
+    // kernel's drain (profiles/r2_decode_fused_ab.txt)
+    if (fin && fin->fw.cnt_items && !fin->gate_side && a.pin_cp == 0 && a.n_pairs + ngate <= fused_max &&
+        a.n_pairs <= kFusedMaxPairs && gs <= 4) {
+        a.fused = 1;
+        a.n_route_ctas = a.n_pairs;
+        a.n_gate_ctas = ngate;
+        // every K5 CTA resident beside the route and gate CTAs (no late static items)
+        kgrid -= a.n_pairs + ngate;
+        fa = *fin;
+        fa.out = out;
+    } else if (fin && !fin->forced_g && !fin->gate_side && ngate <= gate_k5_max) {
+        a.n_gate_ctas = ngate;
         fa = *fin;
     }
     a.early_trigger = fin && !no_trigger;
     a.prewait = fin && fin->prewait;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.n_gate_ctas + CPS * num_sms());
+    cfg.gridDim = dim3(a.n_route_ctas + a.n_gate_ctas + kgrid);
     cfg.blockDim = dim3(DW * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -575,9 +888,12 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
     cfg.numAttrs = counter_reset_by_append ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, tp, a, q, part, nchunks, counter, fa);
     a.nchunks = nchunks;
+    if (a.fused) return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
     if (fin) return launch_decode_finish(a, nseq, q, part, out, *fin, st);
     extern int launch_decode_combine_bf16(const DecArgs&, int, const float*, __nv_bfloat16*, cudaStream_t);
     return launch_decode_combine_bf16(a, nseq, part, out, st);
 }
 
 }  // namespace wgkv
+
+TL_EXPORT(wgkv_tl_k5)

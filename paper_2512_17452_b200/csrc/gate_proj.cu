@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
                      __nv_bfloat16* __restrict__ k_post, float* __restrict__ g_out, uint8_t* __restrict__ bits_out,
                      int32_t* __restrict__ cand, int* __restrict__ pcnt) {
     extern __shared__ uint8_t gsm_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned, by pointer arithmetic on the __shared__ array (an integer round
+    // trip would lose the address space: every access through sm would be generic)
+    uint8_t* sm = gsm_raw + ((1024u - (smem_u32(gsm_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(sm);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + GP_OFF_BAR);
     uint64_t* b_full = bars + 0;
