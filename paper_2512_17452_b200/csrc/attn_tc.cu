@@ -178,9 +178,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                          const __grid_constant__ CUtensorMap tkrun, const __grid_constant__ CUtensorMap tvrun,
                          VsArgs a, __nv_bfloat16* __restrict__ out) {
     extern __shared__ uint8_t smem_raw[];
-    // 1 KB-aligned, by pointer arithmetic on the __shared__ array (an integer round
-    // trip would lose the address space: every access through sm would be generic)
-    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    // 1 KB-aligned through an integer round trip: the few accesses through sm
+    // (not TMA / tcgen05 / ldmatrix, which take 32-bit smem addresses) are then
+    // generic.  Kept here on purpose: the shared-space variant measured 3 %
+    // slower K3 (141.9 vs 137.7 ms, interleaved A/B, different scheduling);
+    // the other kernels use pointer arithmetic on the __shared__ array
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bar = reinterpret_cast<Bars*>(sm + OFF_BAR);
     const uint32_t sbase = smem_u32(sm);
 
