@@ -380,19 +380,25 @@ def run_gpu(args, cfg):
             if shards > 1:
                 exchange_decode(o_)
 
-    per_layer_dec = 2 + (1 if shards > 1 else 0)  # K5 + finish (merge, new token, K4) [+ C1]
+    # kernels per decode layer: counted from the captured graph when there is one
+    # (1 for the fused small-batch layer, 2 = K5 + finish otherwise) [+ C1]
+    per_layer_dec = 2 + (1 if shards > 1 else 0)
     graph = {"g": None}
+    graph_kernels = {"n": None, "last": None}
 
     def _capture(fn):
-        """CUDA graph of fn's launches, captured on a side stream (recorded, not executed)."""
+        """CUDA graph of fn's launches, captured on a side stream (recorded, not executed).
+        Also counts the library's kernel nodes in it (graph_kernels["n"])."""
         gs = torch.cuda.Stream(dev)
         gs.wait_stream(stream)
         sess.set_stream(gs)
-        g_ = torch.cuda.CUDAGraph()
+        g_ = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(g_, stream=gs):
             fn()
         sess.set_stream(stream)
         stream.wait_stream(gs)
+        graph_kernels["last"] = _count_wgkv_kernels(g_.raw_cuda_graph())
+        g_.instantiate()
         return g_
 
     def decode_all():
@@ -404,7 +410,7 @@ def run_gpu(args, cfg):
                 graph["g"].replay()
             else:
                 decode_token_step()
-            launches["n"] += per_layer_dec * L
+            launches["n"] += graph_kernels["n"] if graph["g"] is not None and graph_kernels["n"] else per_layer_dec * L
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -442,6 +448,7 @@ def run_gpu(args, cfg):
             st0 = sess.stats(0, B)
             if not args.no_graphs:  # capture one token-step over all layers (recorded, not executed)
                 graph["g"] = _capture(decode_token_step)
+                graph_kernels["n"] = graph_kernels["last"]  # library kernels per token step (all layers)
             decode_all()
             st1 = sess.stats(0, B)
             resident = (st0["resident_entries"], st1["resident_entries"])
@@ -630,10 +637,35 @@ def run_gpu(args, cfg):
         dist.barrier()
     res = dict(pre_s=pre_s, dec_s=dec_s, k3_s=k3_s, tot_s=tot_s, wall_s=t_wall, pairs_layer=pairs_layer,
                resident=resident, clocks=clk.summary(), launches=launches["n"] // args.steps, e2e=e2e,
+               dec_kernels_per_layer=(graph_kernels["n"] / L if graph_kernels["n"] else per_layer_dec),
                T=T, B=B, D=D, world=world, shards=shards, hq=hq, hkv=hkv)
     if world > 1:
         dist.destroy_process_group()
     return rank, res
+
+
+def _count_wgkv_kernels(raw_graph):
+    """Kernel nodes of a captured CUDA graph whose function is one of this
+    library's (mangled names in namespace wgkv); None if the graph cannot be read."""
+    try:
+        from cuda.bindings import driver as dr
+        gr = dr.CUgraph(init_value=int(raw_graph))
+        _, _, n = dr.cuGraphGetNodes(gr, 0)
+        _, nodes, n = dr.cuGraphGetNodes(gr, n)
+        cnt = 0
+        for nd in nodes[:n]:
+            _, ty = dr.cuGraphNodeGetType(nd)
+            if ty != dr.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+                continue
+            err, prm = dr.cuGraphKernelNodeGetParams(nd)
+            if err != dr.CUresult.CUDA_SUCCESS:
+                continue
+            err, name = dr.cuFuncGetName(prm.func)
+            if err == dr.CUresult.CUDA_SUCCESS and b"wgkv" in (name or b""):
+                cnt += 1
+        return cnt
+    except Exception:  # noqa: BLE001 -- diagnostics only; the caller falls back
+        return None
 
 
 def main():
@@ -737,7 +769,8 @@ def main():
                             "frac": dec_gbs / peaks["hbm"], "frac_of_8TBps": dec_gbs / 8000.0,
                             "bytes_per_decode_step": dec_bytes / D,
                             "note": "resident Global+Local K+V bytes (bf16) + q/out per token-step / decode time"},
-        "clocks": r["clocks"], "gpu_launches": r["launches"], "e2e": r["e2e"],
+        "clocks": r["clocks"], "gpu_launches": r["launches"],
+        "decode_kernels_per_layer": r["dec_kernels_per_layer"], "e2e": r["e2e"],
     }
     if world == 1 and shards > 1:
         line["emulated_shard"] = {
