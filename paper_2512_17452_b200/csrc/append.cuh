@@ -61,27 +61,28 @@ __host__ __device__ inline size_t append_smem_bytes(int d, int hidden) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void append_finalize(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s,
                                                 int h, const float* __restrict__ forced_g, const DecodeTrace& tr,
-                                                const AppendWork& wk) {
-    __threadfence();  // acquire: the other CTAs' terms / slot / state
+                                                const AppendWork& wk, const double* terms) {
     const int pair = (seq0 + s) * pv.kv_heads + h;
     const int blk = layer * pv.kv_heads + h;
+    const int sl = __ldcg(&wk.slot[pair]);
+    const int ev = __ldcg(&wk.event[pair]);
     double g;
     if (forced_g) {
         g = (double)forced_g[(size_t)s * pv.kv_heads + h];
     } else {  // z2 = b2 + sum_h terms, sequential (gating.cpp:162-166)
-        const volatile double* t = wk.terms + (size_t)pair * ga.hidden;
         double z2 = ga.b2d[blk];
-        for (int u = 0; u < ga.hidden; ++u) z2 = __dadd_rn(z2, t[u]);
+        for (int u = 0; u < ga.hidden; ++u) z2 = __dadd_rn(z2, terms[u]);
         g = gate_from_z2(z2);
     }
     const uint8_t bit = g >= ga.tau ? 1 : 0;
-    const int sl = *(volatile int*)&wk.slot[pair];
-    const int ev = *(volatile int*)&wk.event[pair];
     if (sl >= 0) {
         pv.gate[sl] = (float)g;
         pv.adm[sl] = bit;
     }
-    if (ev >= 0 && !wk.early_state) pv.state[pv.head_index(layer, seq0 + s, h)] = wk.next[pair];
+    if (ev >= 0 && !wk.early_state) {
+        const int4 ns = __ldcg(reinterpret_cast<const int4*>(wk.next + pair));
+        pv.state[pv.head_index(layer, seq0 + s, h)] = HeadState{ns.x, ns.y, ns.z, ns.w};
+    }
     const size_t o = (size_t)s * pv.kv_heads + h;
     if (tr.g) tr.g[o] = (float)g;
     if (tr.bits) tr.bits[o] = bit;
@@ -90,17 +91,27 @@ __device__ __forceinline__ void append_finalize(const PoolView& pv, const GateAr
     wk.count[pair] = 0;  // ready for the next step
 }
 
-// every CTA of a pair calls this once its writes are issued (whole CTA)
+// every CTA of a pair calls this once its writes are issued (whole CTA); the
+// last one finalises.  smem: >= hidden doubles (free by now): the gate CTAs'
+// terms come in one parallel round of loads for the sequential z2 sum
 __device__ __forceinline__ void append_arrive(const PoolView& pv, const GateArgs& ga, int layer, int seq0, int s, int h,
                                               const float* __restrict__ forced_g, const DecodeTrace& tr,
-                                              const AppendWork& wk, int arrivals) {
+                                              const AppendWork& wk, int arrivals, uint8_t* smem) {
     __shared__ int last;
+    const int pair = (seq0 + s) * pv.kv_heads + h;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();  // release this CTA's writes
-        last = atomicAdd(&wk.count[(seq0 + s) * pv.kv_heads + h], 1) == arrivals - 1;
-        if (last) append_finalize(pv, ga, layer, seq0, s, h, forced_g, tr, wk);
+        last = atomicAdd(&wk.count[pair], 1) == arrivals - 1;
+        if (last) __threadfence();  // acquire: the other CTAs' terms / slot / state
     }
+    __syncthreads();
+    if (!last) return;
+    double* terms = reinterpret_cast<double*>(smem);
+    if (!forced_g)
+        for (int u = threadIdx.x; u < ga.hidden; u += blockDim.x) terms[u] = __ldcg(wk.terms + (size_t)pair * ga.hidden + u);
+    __syncthreads();
+    if (threadIdx.x == 0) append_finalize(pv, ga, layer, seq0, s, h, forced_g, tr, wk, terms);
 }
 
 // ---------------------------------------------------------------------------
@@ -348,7 +359,7 @@ __device__ __forceinline__ void append_role(const PoolView& pv, const GateArgs& 
         append_route<E>(pv, ga, layer, seq0, s, h, W, k_pre, v, wk, pdl_wait);
     else
         append_gate_part<E>(pv, ga, layer, seq0, s, h, j, k_pre, wk, smem);
-    append_arrive(pv, ga, layer, seq0, s, h, forced_g, tr, wk, arrivals);
+    append_arrive(pv, ga, layer, seq0, s, h, forced_g, tr, wk, arrivals, smem);
 }
 
 }  // namespace wgkv

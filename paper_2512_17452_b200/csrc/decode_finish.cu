@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         const int pr = blockIdx.x / gpp, j = blockIdx.x % gpp;
         const int s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
         append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, fsm);
-        append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, arrivals);
+        append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, arrivals, fsm);
         TL_COMMIT(3, a.layer, 0);
         return;
     }
@@ -68,6 +68,34 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     asm volatile("griddepcontrol.wait;" ::: "memory");
     TL_MARK(2);
     if (sp == 0 && tid == 0) *a.counter = 0;  // K5's work counter, for the next launch
+    // one round of loads: the chunk count, the rows of this warp's first three
+    // chunks (speculatively: the partial buffer holds max_chunks of them), and
+    // in the last warp the new token's q / k / v and position
+    constexpr int SPEC = 3;
+    float mcs[SPEC], lcs[SPEC];
+    float2 xs[SPEC][2];
+#pragma unroll
+    for (int j = 0; j < SPEC; ++j) {
+        const int c = min(warp + j * NW, a.max_chunks - 1);
+        const float* rr = base + (size_t)c * pstride;
+        mcs[j] = rr[d];
+        lcs[j] = rr[d + 1];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) xs[j][i] = *reinterpret_cast<const float2*>(rr + 2 * lane + 64 * i);
+    }
+    const size_t qo = ((size_t)s * a.q_heads + p) * d, ko = ((size_t)s * a.pv.kv_heads + h) * d;
+    __nv_bfloat162 qv[2], kv[2], vv[2];
+    long pos = 0;
+    if (warp == NW - 1) {
+        pos = a.tokpos[bh];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int i = lane + 32 * j;  // pair index (d / 2 = 64 pairs)
+            qv[j] = reinterpret_cast<const __nv_bfloat162*>(q + qo)[i];
+            kv[j] = reinterpret_cast<const __nv_bfloat162*>(fin.k_new + ko)[i];
+            vv[j] = *reinterpret_cast<const __nv_bfloat162*>(fin.v_new + ko + 2 * lane + 64 * j);
+        }
+    }
     const int nch = min(a.nchunks[bh], kMaxChunks);
     float m = -INFINITY, l = 0.f;
     float2 acc[2];  // columns 2*lane + 64*j
@@ -83,10 +111,12 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         }
         m = mn;
     };
-    // each warp merges every NW-th chunk online; the row, m and l of a chunk
-    // are loaded together (one round of L2 reads per warp)
-#pragma unroll 4
-    for (int c = warp; c < nch; c += NW) {
+    // each warp merges every NW-th chunk online (m = -inf: an empty chunk)
+#pragma unroll
+    for (int j = 0; j < SPEC; ++j)
+        if (warp + j * NW < nch && mcs[j] != -INFINITY) merge(mcs[j], lcs[j], xs[j]);
+#pragma unroll 1
+    for (int c = warp + SPEC * NW; c < nch; c += NW) {
         const float* rr = base + (size_t)c * pstride;
         const float mc = rr[d], lc = rr[d + 1];
         float2 x[2];
@@ -97,21 +127,19 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
     }
     if (warp == NW - 1) {
         // the new token at its position: logit = RoPE(q) . bf16(RoPE(k)) / sqrt(d)
-        // (the key as it will be cached), weight on v.  (Not hoisted above the
-        // wait: tokpos comes from K5, and the head state may already hold the
-        // next position once this kernel's append has finalised.)
-        const long pos = a.tokpos[bh];
-        const size_t qo = ((size_t)s * a.q_heads + p) * d, ko = ((size_t)s * a.pv.kv_heads + h) * d;
+        // (the key as it will be cached), weight on v.  (tokpos comes from K5:
+        // the head state may already hold the next position once this kernel's
+        // append has finalised.)
         float dotp = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const int i = lane + 32 * j;  // pair index (d / 2 = 64 pairs)
+            const int i = lane + 32 * j;
             float c, sn;
             rope_cs(a.freq, i, pos, c, sn);
             float q0, q1, k0, k1;
-            rope_pair_f32(__bfloat162float(q[qo + 2 * i]), __bfloat162float(q[qo + 2 * i + 1]), c, sn, q0, q1);
-            rope_pair_f32(__bfloat162float(fin.k_new[ko + 2 * i]), __bfloat162float(fin.k_new[ko + 2 * i + 1]), c, sn,
-                          k0, k1);
+            const float2 qf = __bfloat1622float2(qv[j]), kf = __bfloat1622float2(kv[j]);
+            rope_pair_f32(qf.x, qf.y, c, sn, q0, q1);
+            rope_pair_f32(kf.x, kf.y, c, sn, k0, k1);
             k0 = __bfloat162float(__float2bfloat16_rn(k0));
             k1 = __bfloat162float(__float2bfloat16_rn(k1));
             dotp = fmaf(q0, k0, fmaf(q1, k1, dotp));
@@ -120,10 +148,7 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         for (int o = 16; o >= 1; o >>= 1) dotp += __shfl_xor_sync(0xffffffffu, dotp, o);
         float2 x[2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const __nv_bfloat162 vv = *reinterpret_cast<const __nv_bfloat162*>(fin.v_new + ko + 2 * lane + 64 * j);
-            x[j] = __bfloat1622float2(vv);
-        }
+        for (int j = 0; j < 2; ++j) x[j] = __bfloat1622float2(vv[j]);
         merge(dotp * rsqrtf((float)d), 1.f, x);
     }
     if (lane == 0) {

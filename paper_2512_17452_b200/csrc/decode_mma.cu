@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
                     fused_commit_gate(a.pv, fin.ga, a.seq0, s, h, fin.tr, fin.wk, fin.fw);
             }
         } else {
-            append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, gpp + 1);
+            append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, gpp + 1, sm);
         }
         TL_COMMIT(2, a.layer, 0);
         return;
