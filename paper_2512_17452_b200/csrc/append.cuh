@@ -49,7 +49,10 @@ struct AppendWork {
 };
 
 constexpr int kAppendThreads = 256;
-constexpr int kGateUnits = 16;  // hidden units per gate CTA
+#ifndef WGKV_GATE_UNITS
+#define WGKV_GATE_UNITS 16
+#endif
+constexpr int kGateUnits = WGKV_GATE_UNITS;  // hidden units per gate CTA
 __host__ __device__ inline int gate_ctas_per_pair(int hidden) { return (hidden + kGateUnits - 1) / kGateUnits; }
 // dynamic smem of the roles: gate = feature [2d] + W1 rows [16][2d + 1] doubles
 __host__ __device__ inline size_t append_smem_bytes(int d, int hidden) {
