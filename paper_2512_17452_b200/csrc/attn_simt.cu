@@ -318,10 +318,12 @@ __global__ void __launch_bounds__(128) decode_attn_simt_kernel(DecArgs a, const 
 // the row of a chunk are loaded together, the loads of successive chunks are
 // independent), so the partials are read in one round of L2 accesses; the
 // 8 warp results are merged through smem.
-template <typename E>
-__global__ void __launch_bounds__(256) decode_combine_kernel(DecArgs a, const float* __restrict__ part,
-                                                             E* __restrict__ out) {
-    constexpr int NW = 8;
+// NW warps per (seq, q head), each merging every NW-th chunk online; SPEC > 0:
+// the rows of each warp's first SPEC chunks are loaded in the same round as
+// the chunk count (speculatively: the partial buffer holds max_chunks of them)
+template <typename E, int NW, int SPEC, int NJ>  // NJ: float2 columns per lane (d <= 64 * NJ)
+__global__ void __launch_bounds__(NW * 32) decode_combine_kernel(DecArgs a, const float* __restrict__ part,
+                                                                 E* __restrict__ out) {
     const int d = a.pv.head_dim, gs = a.q_heads / a.pv.kv_heads;
     const int sp = blockIdx.x, s = sp / a.q_heads, p = sp % a.q_heads, h = p / gs, g = p % gs;
     const int bh = s * a.pv.kv_heads + h;
@@ -329,39 +331,54 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecArgs a, const fl
     const size_t pstride = (size_t)gs * (d + 2);
     const float* base = part + (size_t)bh * a.max_chunks * pstride + (size_t)g * (d + 2);
     __shared__ float wm[NW], wl[NW];
-    __shared__ float wacc[NW][256];
+    __shared__ float wacc[NW][64 * NJ];
     asm volatile("griddepcontrol.wait;" ::: "memory");  // partials of the attention kernel (PDL)
     if (blockIdx.x == 0 && tid == 0 && a.counter) *a.counter = 0;  // K5's work counter, for the next launch
-    const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, kMaxChunks);
     float m = -INFINITY, l = 0.f;
-    float2 acc[4];  // columns 2*lane + 64*j (d <= 256)
+    float2 acc[NJ];  // columns 2*lane + 64*j
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int c = warp; c < nch; c += NW) {
+    for (int j = 0; j < NJ; ++j) acc[j] = make_float2(0.f, 0.f);
+    auto load = [&](int c, float& mc, float& lc, float2 (&x)[NJ]) {
         const float* r = base + (size_t)c * pstride;
-        const float mc = r[d], lc = r[d + 1];
-        float2 x[4];
+        mc = r[d];
+        lc = r[d + 1];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
             x[j] = 2 * lane + 64 * j < d ? *reinterpret_cast<const float2*>(r + 2 * lane + 64 * j) : make_float2(0.f, 0.f);
-        if (mc == -INFINITY) continue;  // empty chunk (uniform across the warp)
+    };
+    auto merge = [&](float mc, float lc, const float2 (&x)[NJ]) {
+        if (mc == -INFINITY) return;  // empty chunk (uniform across the warp)
         const float mn = fmaxf(m, mc);
         const float sa = m == -INFINITY ? 0.f : __expf(m - mn), sb = __expf(mc - mn);
         l = l * sa + lc * sb;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             acc[j].x = acc[j].x * sa + x[j].x * sb;
             acc[j].y = acc[j].y * sa + x[j].y * sb;
         }
         m = mn;
+    };
+    float smc[SPEC > 0 ? SPEC : 1], slc[SPEC > 0 ? SPEC : 1];
+    float2 sx[SPEC > 0 ? SPEC : 1][NJ];
+#pragma unroll
+    for (int j = 0; j < SPEC; ++j) load(min(warp + j * NW, a.max_chunks - 1), smc[j], slc[j], sx[j]);
+    const int nch = min(a.nchunks ? a.nchunks[bh] : a.n_chunks, kMaxChunks);
+#pragma unroll
+    for (int j = 0; j < SPEC; ++j)
+        if (warp + j * NW < nch) merge(smc[j], slc[j], sx[j]);
+#pragma unroll 4
+    for (int c = warp + SPEC * NW; c < nch; c += NW) {
+        float mc, lc;
+        float2 x[NJ];
+        load(c, mc, lc, x);
+        merge(mc, lc, x);
     }
     if (lane == 0) {
         wm[warp] = m;
         wl[warp] = l;
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
         if (2 * lane + 64 * j < d) {
             wacc[warp][2 * lane + 64 * j] = acc[j].x;
             wacc[warp][2 * lane + 64 * j + 1] = acc[j].y;
@@ -389,22 +406,25 @@ int launch_decode_attn_simt(const DecArgs& a, int nseq, const E* q, float* part,
     const size_t smem = sizeof(float) * ((size_t)gs * d + (size_t)4 * gs * (d + 2));
     if (ensure_smem(decode_attn_simt_kernel<E>, smem) != cudaSuccess) return WGKV_ECUDA;
     decode_attn_simt_kernel<E><<<dim3(a.n_chunks, nseq * a.pv.kv_heads), 128, smem, st>>>(a, q, part);
-    decode_combine_kernel<E><<<nseq * a.q_heads, 256, 0, st>>>(a, part, out);
+    decode_combine_kernel<E, 8, 0, 4><<<nseq * a.q_heads, 256, 0, st>>>(a, part, out);
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
 int launch_decode_combine_bf16(const DecArgs& a, int nseq, const float* part, __nv_bfloat16* out, cudaStream_t st) {
     // programmatic dependent of the attention kernel: launch latency overlaps its tail
     cudaLaunchConfig_t cfg = {};
+    // 16 warps, 10 chunks each in the first round of loads: one round of L2 reads
+    // for up to 160 chunks (one kv head spread over every SM: ~150)
+    constexpr int NW = 16;
     cfg.gridDim = dim3(nseq * a.q_heads);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(NW * 32);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, decode_combine_kernel<__nv_bfloat16>, a, part, out);
+    cudaLaunchKernelEx(&cfg, decode_combine_kernel<__nv_bfloat16, NW, 10, 2>, a, part, out);  // d = 128
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
