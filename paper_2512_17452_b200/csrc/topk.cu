@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(128) topk_score_kernel(DecArgs a, const E* __r
 // keeps 2 pages (16 x 16-byte loads per lane) in flight.
 // ---------------------------------------------------------------------------
 constexpr int SC_WARPS = 8;
-constexpr int SC_PAGES = 64;  // pages per CTA (8 per warp)
+#ifndef WGKV_SC_PAGES
+#define WGKV_SC_PAGES 64
+#endif
+constexpr int SC_PAGES = WGKV_SC_PAGES;  // pages per CTA (8 per warp)
 
 __global__ void __launch_bounds__(SC_WARPS * 32) topk_score_mma_kernel(DecArgs a, const __nv_bfloat16* __restrict__ q,
                                                                         float* __restrict__ scores) {
