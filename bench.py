@@ -266,6 +266,16 @@ def run_gpu(args, cfg):
         box = [W.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         sess.comm_init(box[0], world, rank)
+    peer = shards > 1 and args.decode_exchange == "peer"
+    peer_regions = None
+    if peer:  # decode C1 over peer memory: every rank's exchange region mapped here
+        if world > 1:
+            sess.peer_init(world, rank, B)  # IPC handles exchanged over torch.distributed
+        else:  # emulated shard: the other ranks' regions live on this GPU, only rank 0's arrivals are awaited
+            nb = sess.peer_region_bytes(shards, B)
+            peer_regions = [torch.zeros(nb, dtype=torch.uint8, device=dev) for _ in range(shards)]
+            sess.peer_attach(shards, 0, B, peer_regions, wait_ranks=1)
+        sess.peer_decode(True)  # every decode layer pushes its rows from inside its merge
     # ---- resident inputs: `slots` distinct layer-input sets ------------------
     slots = max(1, min(args.slots, L))
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
@@ -365,8 +375,13 @@ def run_gpu(args, cfg):
     sk = [sk_all[i] for i in range(slots)]
     sv = [sv_all[i] for i in range(slots)]
 
-    def exchange_decode(o_):
-        if world > 1:
+    def exchange_decode(o_, l):
+        if args.decode_exchange == "none":
+            return
+        if peer:  # fused into the layer: its merge pushed, the next layer unpacks (the last: peer_wait)
+            if l == L - 1:
+                sess.peer_wait()
+        elif world > 1:
             sess.allgather_heads(o_, dfull)  # KB-sized: on the compute stream, inside the graph
         elif dstage is not None:
             W.assemble_heads(dstage, dfull, shards, B)
@@ -378,11 +393,12 @@ def run_gpu(args, cfg):
             o_ = dout if os_ is None else os_[l]
             check(lib.wgkv_decode_layer(h, l, 0, B, P(qi), P(ki), P(vi), None, P(o_), None, None), "decode")
             if shards > 1:
-                exchange_decode(o_)
+                exchange_decode(o_, l)
 
     # kernels per decode layer: counted from the captured graph when there is one
     # (1 for the fused small-batch layer, 2 = K5 + finish otherwise) [+ C1]
-    per_layer_dec = 2 + (1 if shards > 1 else 0)
+    per_layer_dec = 2 + (1 if shards > 1 and args.decode_exchange == "nccl" else 0)
+    assert not peer or L % 4 == 0, "peer exchanges rotate over 4 slots: a replayed token step holds a multiple of 4"
     graph = {"g": None}
     graph_kernels = {"n": None, "last": None}
 
@@ -685,6 +701,9 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="issue decode kernels eagerly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-T", type=int, default=16384)
+    ap.add_argument("--decode-exchange", default="peer", choices=["peer", "nccl", "none"],
+                    help="decode C1 (N > 1): push kernel over peer memory (wgkv_peer_*) or NCCL all-gather + assembly "
+                         "('none': no exchange, diagnostics only)")
     ap.add_argument("--emulate-shard", type=int, default=0,
                     help="one GPU runs rank 0's KV-head shard of N GPUs (8/N kv heads) incl. the head all-gather's "
                          "assembly; the NVLink transfer is not emulated and no scaling curve is measured")
@@ -775,9 +794,13 @@ def main():
     if world == 1 and shards > 1:
         line["emulated_shard"] = {
             "n": shards, "kv_heads_per_gpu": r["hkv"], "q_heads_per_gpu": r["hq"],
-            "note": "one GPU runs rank 0's shard (its heads of every token) plus the head all-gather's assembly "
-                    "kernel; 'value' is the whole-job prefill tok/s if every shard ran this fast on its own GPU, "
-                    "the NVLink transfer is NOT included and no scaling curve was measured"}
+            "decode_exchange": args.decode_exchange,
+            "note": "one GPU runs rank 0's shard (its heads of every token) plus the head all-gather's local part "
+                    "(prefill: the assembly kernel; decode with decode_exchange 'peer': each layer's merge stores "
+                    "rank 0's rows as LL words into all N ranks' regions -- here all on this GPU -- and the next "
+                    "layer unpacks rank 0's words; 'nccl': the assembly kernel); 'value' is the whole-job prefill "
+                    "tok/s if every shard ran this fast on its own GPU; the NVLink transfer latency is NOT included "
+                    "and no scaling curve was measured"}
     if not args.no_cpu_baseline:
         try:
             cb = cpu_reference(cfg, args.cpu_sample_T, 1)

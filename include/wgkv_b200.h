@@ -232,6 +232,39 @@ int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank); /*
 int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank);   /* caller-owned ncclComm_t */
 int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out, void* full_out, int async);
 int wgkv_comm_join(wgkv_ctx* ctx);
+/* ---- C1 over NVLink peer memory: the decode-sized all-gather ---------------
+ * A decode layer's head outputs are a few KB per rank: NCCL's all-gather is
+ * latency-bound there.  Instead every rank owns an exchange region
+ * (wgkv_peer_region_bytes) mapped into every other rank: wgkv_peer_alloc
+ * allocates it and exports a cudaIpcMemHandle_t (64 bytes), the caller
+ * exchanges the handles over its own plumbing, wgkv_peer_open maps them;
+ * wgkv_peer_attach takes already-mapped pointers instead (one process driving
+ * all GPUs with peer access, or regions on one GPU).  Protocol (LL, as NCCL's
+ * low-latency one): a rank stores its rows local_out [rows][q_heads][d] as
+ * 8-byte words {4 data bytes, flag} straight into every rank's region (NVLink
+ * stores, no fence, no counter); a reader polls the words themselves and
+ * writes the reference's concat layout [rows][world * q_heads][d]
+ * (engine.cpp:234-238) into its result slot.  Exchanges rotate over 4 slots.
+ * wgkv_peer_allgather_heads: a push kernel; wait = 1 also unpacks it now,
+ * else it stays pending.  wgkv_peer_decode(ctx, 1): every wgkv_decode_layer
+ * pushes its output rows from inside its merge (no extra kernel) and unpacks
+ * the pending exchange in one of its CTAs, so exchange k is complete once
+ * decode layer k + 1 (or wgkv_peer_wait) has run.  wgkv_peer_wait unpacks the
+ * pending exchange.  wgkv_peer_result(back): this rank's result slot of the
+ * exchange `back` exchanges ago (0 = the last), [rows][world * q_heads][d].
+ * Contract (as NCCL's): every rank makes the same sequence of exchanges with
+ * the same rows; a captured CUDA graph that replays exchanges holds a
+ * multiple of 4 of them and leaves none pending; bf16 contexts.  wait_ranks
+ * = world normally (fewer only to emulate a shard on one GPU: only ranks
+ * [0, wait_ranks) are awaited and unpacked). */
+int wgkv_peer_region_bytes(int world, long max_rows, int q_heads, int head_dim, int dtype, size_t* bytes);
+int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, uint8_t* ipc_handle64, void** base);
+int wgkv_peer_open(wgkv_ctx* ctx, int world, int rank, const uint8_t* handles /* world x 64 */, int wait_ranks);
+int wgkv_peer_attach(wgkv_ctx* ctx, int world, int rank, long max_rows, void* const* bases, int wait_ranks);
+int wgkv_peer_allgather_heads(wgkv_ctx* ctx, long rows, const void* local_out, int wait);
+int wgkv_peer_wait(wgkv_ctx* ctx);
+int wgkv_peer_decode(wgkv_ctx* ctx, int on);
+int wgkv_peer_result(wgkv_ctx* ctx, int back, void** ptr);
 /* ---- f3: output projection overlapped with the head all-gather -----------
  * Session's x[t] += Wo . concat[t] (engine.cpp:243-245 prefill, :331 decode)
  * on top of wgkv_allgather_heads: local_out [nseq][T][q_heads][d] (bf16, this

@@ -82,6 +82,14 @@ SIGNATURES = {
     "wgkv_comm_attach": ([_vp, _vp, _i, _i], _i),
     "wgkv_allgather_heads": ([_vp, _i, _l, _vp, _vp, _i], _i),
     "wgkv_comm_join": ([_vp], _i),
+    "wgkv_peer_region_bytes": ([_i, _l, _i, _i, _i, _vp], _i),
+    "wgkv_peer_alloc": ([_vp, _i, _l, _vp, _vp], _i),
+    "wgkv_peer_open": ([_vp, _i, _i, _vp, _i], _i),
+    "wgkv_peer_attach": ([_vp, _i, _i, _l, _vp, _i], _i),
+    "wgkv_peer_allgather_heads": ([_vp, _l, _vp, _i], _i),
+    "wgkv_peer_wait": ([_vp], _i),
+    "wgkv_peer_decode": ([_vp, _i], _i),
+    "wgkv_peer_result": ([_vp, _i, _vp], _i),
     "wgkv_output_proj": ([_vp, _i, _l, _vp, _vp, _i, _vp], _i),
     "wgkv_assemble_heads": ([_i, _l, C.c_size_t, _vp, _vp, _vp], _i),
 }

@@ -225,6 +225,64 @@ class Session:
     def comm_join(self):
         check(self.lib.wgkv_comm_join(self.h), "comm_join")
 
+    # ---- C1 over NVLink peer memory (decode-sized exchanges) -------------------
+    def peer_region_bytes(self, world: int, max_rows: int) -> int:
+        n = C.c_size_t(0)
+        check(self.lib.wgkv_peer_region_bytes(world, max_rows, self.cfg.q_heads, self.cfg.head_dim, self.cfg.dtype,
+                                              C.byref(n)),
+              "peer_region_bytes")
+        return n.value
+
+    def peer_alloc(self, world: int, max_rows: int) -> bytes:
+        """Allocate this rank's exchange region; returns its 64-byte IPC handle."""
+        buf = C.create_string_buffer(64)
+        base = C.c_void_p()
+        check(self.lib.wgkv_peer_alloc(self.h, world, max_rows, buf, C.byref(base)), "peer_alloc")
+        self._peer = dict(world=world, max_rows=max_rows, base=base.value, keep=None)
+        return buf.raw
+
+    def peer_open(self, world: int, rank: int, handles, wait_ranks=None):
+        """Map every rank's region from the handles (rank order; this rank's own entry is ignored)."""
+        blob = C.create_string_buffer(b"".join(bytes(h) for h in handles), 64 * world)
+        check(self.lib.wgkv_peer_open(self.h, world, rank, blob, wait_ranks or world), "peer_open")
+        self._peer.update(rank=rank)
+
+    def peer_init(self, world: int, rank: int, max_rows: int, group=None):
+        """peer_alloc + handle exchange over torch.distributed (the caller's
+        plumbing; any backend) + peer_open."""
+        import torch.distributed as dist
+        mine = self.peer_alloc(world, max_rows)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.peer_open(world, rank, allh)
+
+    def peer_attach(self, world: int, rank: int, max_rows: int, regions, wait_ranks=None):
+        """Attach already-mapped regions (uint8 tensors of peer_region_bytes each, rank order)."""
+        arr = (C.c_void_p * world)(*[r.data_ptr() for r in regions])
+        check(self.lib.wgkv_peer_attach(self.h, world, rank, max_rows, arr, wait_ranks or world), "peer_attach")
+        self._peer = dict(world=world, max_rows=max_rows, base=regions[rank].data_ptr(), keep=list(regions),
+                          rank=rank)
+
+    def peer_allgather_heads(self, local_out: torch.Tensor, wait: bool = True):
+        """local_out [rows][q_heads][d] of every rank -> this rank's result
+        [rows][world*q_heads][d] (returned as a view once wait; else pending)."""
+        rows = local_out.shape[0]
+        check(self.lib.wgkv_peer_allgather_heads(self.h, rows, _p(local_out), int(wait)), "peer_allgather_heads")
+        return self.peer_result(0, rows) if wait else None
+
+    def peer_wait(self):
+        check(self.lib.wgkv_peer_wait(self.h), "peer_wait")
+
+    def peer_decode(self, on: bool = True):
+        """Decode layers push their output rows from inside their merge (C1 fused into the layer)."""
+        check(self.lib.wgkv_peer_decode(self.h, int(on)), "peer_decode")
+
+    def peer_result(self, back: int, rows: int) -> torch.Tensor:
+        ptr = C.c_void_p()
+        check(self.lib.wgkv_peer_result(self.h, back, C.byref(ptr)), "peer_result")
+        world = self._peer["world"]
+        return _device_view(ptr.value, (rows, world * self.cfg.q_heads, self.cfg.head_dim), self.dtype, self.device)
+
     def output_proj(self, local_out: torch.Tensor, wo: torch.Tensor, x: torch.Tensor):
         """f3: x += concat . wo^T (engine.cpp:243-245 / :331) where concat is
         the all-gathered head output; local_out [nseq][T][q_heads][d] (decode:
@@ -241,6 +299,20 @@ class Session:
         v = (C.c_int64 * 2)()
         check(self.lib.wgkv_pool_info(self.h, v), "pool_info")
         return dict(capacity=v[0], free=v[1])
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over a raw device pointer (torch.as_tensor wraps it without a copy)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=typestr, data=(ptr, False), version=2,
+                                             strides=None)
+
+
+def _device_view(ptr, shape, dtype, device):
+    if dtype == torch.float32:
+        return torch.as_tensor(_CudaArray(ptr, shape, "<f4"), device=device)
+    return torch.as_tensor(_CudaArray(ptr, shape, "<i2"), device=device).view(torch.bfloat16)
 
 
 def nccl_unique_id() -> bytes:

@@ -246,6 +246,17 @@ struct wgkv_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_comm_in = nullptr, ev_comm_done = nullptr;
     uint8_t* stage = nullptr;  // [world][stage_rows][q_heads * d] elements
+    // C1 over peer memory (comm.cuh): every rank's exchange region as mapped here
+    PeerXchg px{};        // world = 0: not attached
+    int peer_wait_ranks = 0;
+    bool peer_decode = false;     // decode layers push their output rows themselves
+    uint64_t peer_seq = 0;        // exchanges so far (slot = seq % kPeerSlots)
+    int pend_slot = -1;           // the last exchange, not unpacked yet
+    long pend_rows = 0;
+    uint8_t* peer_own = nullptr;  // wgkv_peer_alloc's region
+    int peer_own_world = 0;
+    long peer_own_rows = 0;
+    std::vector<void*> peer_ipc;  // regions opened with cudaIpcOpenMemHandle
     long stage_rows = 0;
     // f3 (outproj.cu): cuBLAS handle and the two-slot concat ring of the chunked Wo
     void* blas = nullptr;
@@ -469,6 +480,8 @@ int wgkv_ctx_destroy(wgkv_ctx* ctx) {
     }
     if (ctx->ev_comm_in) cudaEventDestroy(ctx->ev_comm_in);
     if (ctx->ev_comm_done) cudaEventDestroy(ctx->ev_comm_done);
+    for (void* p : ctx->peer_ipc) cudaIpcCloseMemHandle(p);
+    if (ctx->peer_own) cudaFree(ctx->peer_own);
     for (void* p : ctx->owned) cudaFree(p);
     delete ctx;
     return WGKV_OK;
@@ -904,6 +917,10 @@ int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q
     return decode_attn_impl(ctx, layer, seq0, nseq, q, out, nullptr);
 }
 
+static PeerXchg peer_next(wgkv_ctx* ctx, bool push, bool unpack);
+static void peer_pushed(wgkv_ctx* ctx, long rows, bool unpacked_pending);
+static int peer_unpack_pending(wgkv_ctx* ctx);
+
 // One decode layer.  bf16 fast path: K5 streams the cache as it was before
 // this step's append and needs nothing in front of it; the finish kernel
 // merges K5's chunks with the new token and runs the append (K4, exact fp64
@@ -915,6 +932,8 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     ++ctx->api_gen;
     DecodeTrace tr{};
     if (trace) tr = DecodeTrace{trace->g, trace->bits, trace->near_tau, trace->events};
+    if (ctx->peer_decode && nseq > ctx->px.max_rows)
+        return fail(WGKV_EINVAL, "decode_layer: nseq exceeds the peer exchange's max_rows");
     if (!defer_append(ctx->cfg)) {
         int st = decode_append_impl(ctx, layer, seq0, nseq, k_pre, v, forced_g, tr, true);
         if (st) return st;
@@ -923,7 +942,13 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
             WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_gate, 0));
             ctx->gate_join = false;
         }
-        return st;
+        if (st || !ctx->peer_decode) return st;
+        // C1 over peer memory: a push kernel behind the layer (fp32 / top-k paths)
+        st = launch_peer_push(static_cast<const uint8_t*>(out), peer_next(ctx, true, false), nseq, ctx->stream);
+        if (st) return fail(st, "peer push kernel failed");
+        if ((st = peer_unpack_pending(ctx))) return st;
+        peer_pushed(ctx, nseq, false);
+        return WGKV_OK;
     }
     int st = decode_check(ctx, layer, seq0, nseq);
     if (st) return st;
@@ -940,6 +965,9 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     fin.forced_g = forced_g;
     fin.tr = tr;
     fin.wk = ctx->wk;
+    // C1 over peer memory: the layer's merges push its output rows into every
+    // rank's slot; the previous exchange is unpacked by one of its CTAs
+    if (ctx->peer_decode) fin.px = peer_next(ctx, true, true);
     {  // this layer's parity halves (a fused launch may start before the previous layer's drained)
         const size_t SH = (size_t)ctx->cfg.max_seqs * ctx->cfg.kv_heads, par = (size_t)(layer & 1) * SH;
         fin.wk.slot += par;
@@ -972,6 +1000,7 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     if (fin.gate_side) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_gate, 0));
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
+    if (ctx->peer_decode) peer_pushed(ctx, nseq, true);
     ctx->finish_gen = ctx->api_gen;
     ctx->finish_layer = layer;
     return WGKV_OK;
@@ -1299,6 +1328,185 @@ int wgkv_comm_join(wgkv_ctx* ctx) {
     DevGuard dg_(ctx->cfg.device);
     ++ctx->api_gen;
     if (ctx->comm_stream) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm_done, 0));
+    return WGKV_OK;
+}
+
+// ---- C1 over peer memory ----------------------------------------------------
+
+static size_t peer_region(int world, long max_rows, int blk) {
+    return kPeerHeader + kPeerSlots * (peer_ll_bytes(world, max_rows, blk) + peer_res_bytes(world, max_rows, blk));
+}
+
+int wgkv_peer_region_bytes(int world, long max_rows, int q_heads, int head_dim, int dtype, size_t* bytes) {
+    if (!bytes || world < 1 || world > kMaxPeers || max_rows < 1 || q_heads < 1 || head_dim < 1 ||
+        (dtype != WGKV_BF16 && dtype != WGKV_F32))
+        return fail(WGKV_EINVAL, "peer_region_bytes: bad argument");
+    *bytes = peer_region(world, max_rows, q_heads * head_dim * (dtype == WGKV_BF16 ? 2 : 4));
+    return WGKV_OK;
+}
+
+int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, uint8_t* ipc_handle64, void** base) {
+    if (!ctx || !ipc_handle64) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
+    if (ctx->peer_own) return fail(WGKV_ESTATE, "peer_alloc: region already allocated");
+    size_t bytes = 0;
+    int st = wgkv_peer_region_bytes(world, max_rows, ctx->cfg.q_heads, ctx->cfg.head_dim, ctx->cfg.dtype, &bytes);
+    if (st) return st;
+    WGKV_CUDA_TRY(cudaMalloc(&ctx->peer_own, bytes));
+    WGKV_CUDA_TRY(cudaMemset(ctx->peer_own, 0, bytes));
+    cudaIpcMemHandle_t h;
+    WGKV_CUDA_TRY(cudaIpcGetMemHandle(&h, ctx->peer_own));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(ipc_handle64, &h, 64);
+    ctx->peer_own_world = world;
+    ctx->peer_own_rows = max_rows;
+    if (base) *base = ctx->peer_own;
+    return WGKV_OK;
+}
+
+static int peer_check_args(wgkv_ctx* ctx, int world, int rank, long max_rows, int wait_ranks) {
+    if (ctx->px.world) return fail(WGKV_ESTATE, "peer: already attached");
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || max_rows < 1 || wait_ranks < 1 ||
+        wait_ranks > world)
+        return fail(WGKV_EINVAL, "peer: bad world / rank / max_rows / wait_ranks");
+    if (ctx->cfg.dtype != WGKV_BF16) return fail(WGKV_ENOTSUP, "peer: bf16 contexts only");
+    return WGKV_OK;
+}
+
+static int peer_bind(wgkv_ctx* ctx, int world, int rank, long max_rows, uint8_t* const* bases, int wait_ranks) {
+    PeerXchg x{};
+    for (int p = 0; p < world; ++p) x.peers.base[p] = bases[p];
+    x.world = world;
+    x.rank = rank;
+    x.blk = ctx->cfg.q_heads * ctx->cfg.head_dim * (int)ctx->esz;
+    x.max_rows = max_rows;
+    ctx->px = x;
+    ctx->peer_wait_ranks = wait_ranks;
+    ctx->peer_seq = 0;
+    ctx->pend_slot = -1;
+    return WGKV_OK;
+}
+
+int wgkv_peer_open(wgkv_ctx* ctx, int world, int rank, const uint8_t* handles, int wait_ranks) {
+    if (!ctx || !handles) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
+    if (!ctx->peer_own) return fail(WGKV_ESTATE, "peer_open: wgkv_peer_alloc first");
+    int st = peer_check_args(ctx, world, rank, ctx->peer_own_rows, wait_ranks);
+    if (st) return st;
+    if (world != ctx->peer_own_world) return fail(WGKV_EINVAL, "peer_open: world differs from peer_alloc's");
+    uint8_t* bases[kMaxPeers] = {};
+    for (int p = 0; p < world; ++p) {
+        if (p == rank) {
+            bases[p] = ctx->peer_own;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + 64 * (size_t)p, 64);
+        void* ptr = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (void* q : ctx->peer_ipc) cudaIpcCloseMemHandle(q);
+            ctx->peer_ipc.clear();
+            return fail(WGKV_ECUDA, std::string("peer_open: cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        }
+        ctx->peer_ipc.push_back(ptr);
+        bases[p] = static_cast<uint8_t*>(ptr);
+    }
+    return peer_bind(ctx, world, rank, ctx->peer_own_rows, bases, wait_ranks);
+}
+
+int wgkv_peer_attach(wgkv_ctx* ctx, int world, int rank, long max_rows, void* const* bases, int wait_ranks) {
+    if (!ctx || !bases) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    ++ctx->api_gen;
+    int st = peer_check_args(ctx, world, rank, max_rows, wait_ranks);
+    if (st) return st;
+    uint8_t* b[kMaxPeers] = {};
+    for (int p = 0; p < world; ++p) {
+        b[p] = static_cast<uint8_t*>(bases[p]);
+        if (!b[p] || reinterpret_cast<uintptr_t>(b[p]) % 16 != 0)
+            return fail(WGKV_EINVAL, "peer_attach: null or unaligned region");
+    }
+    return peer_bind(ctx, world, rank, max_rows, b, wait_ranks);
+}
+
+// the exchange description for the next push (rows) and the pending unpack
+static PeerXchg peer_next(wgkv_ctx* ctx, bool push, bool unpack) {
+    PeerXchg x = ctx->px;
+    x.do_push = push ? 1 : 0;
+    x.push_slot = (int)(ctx->peer_seq % kPeerSlots);
+    x.do_unpack = unpack && ctx->pend_slot >= 0 ? 1 : 0;
+    x.unpack_slot = ctx->pend_slot;
+    x.unpack_rows = (int)ctx->pend_rows;
+    x.unpack_ranks = ctx->peer_wait_ranks;
+    return x;
+}
+
+static void peer_pushed(wgkv_ctx* ctx, long rows, bool unpacked_pending) {
+    if (unpacked_pending) ctx->pend_slot = -1;
+    ctx->pend_slot = (int)(ctx->peer_seq % kPeerSlots);
+    ctx->pend_rows = rows;
+    ++ctx->peer_seq;
+}
+
+// a peer kernel right behind a decode layer keeps that layer's launch chain:
+// the next layer's K5 may still plan before its PDL wait (see wgkv_decode_layer)
+static void peer_keep_chain(wgkv_ctx* ctx, uint64_t gen_before) {
+    if (ctx->finish_gen == gen_before) ctx->finish_gen = ctx->api_gen;
+}
+
+static int peer_unpack_pending(wgkv_ctx* ctx) {
+    if (ctx->pend_slot < 0) return WGKV_OK;
+    const int st = launch_peer_unpack(peer_next(ctx, false, true), ctx->stream);
+    if (st) return fail(st, "peer unpack kernel failed");
+    ctx->pend_slot = -1;
+    return WGKV_OK;
+}
+
+int wgkv_peer_allgather_heads(wgkv_ctx* ctx, long rows, const void* local_out, int wait) {
+    if (!ctx || !local_out) return fail(WGKV_EINVAL, "null argument");
+    DevGuard dg_(ctx->cfg.device);
+    const uint64_t g0 = ctx->api_gen++;
+    if (!ctx->px.world) return fail(WGKV_ESTATE, "peer_allgather_heads: no peer regions attached");
+    if (rows < 1 || rows > ctx->px.max_rows) return fail(WGKV_EINVAL, "peer_allgather_heads: rows outside [1, max_rows]");
+    int st = launch_peer_push(static_cast<const uint8_t*>(local_out), peer_next(ctx, true, false), rows, ctx->stream);
+    if (st) return fail(st, "peer push kernel failed");
+    if ((st = peer_unpack_pending(ctx))) return st;  // exchanges are unpacked in order
+    peer_pushed(ctx, rows, false);
+    if (wait && (st = peer_unpack_pending(ctx))) return st;
+    peer_keep_chain(ctx, g0);
+    return WGKV_OK;
+}
+
+int wgkv_peer_wait(wgkv_ctx* ctx) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    DevGuard dg_(ctx->cfg.device);
+    const uint64_t g0 = ctx->api_gen++;
+    if (!ctx->px.world) return fail(WGKV_ESTATE, "peer_wait: no peer regions attached");
+    const int st = peer_unpack_pending(ctx);
+    if (st) return st;
+    peer_keep_chain(ctx, g0);
+    return WGKV_OK;
+}
+
+int wgkv_peer_decode(wgkv_ctx* ctx, int on) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    ++ctx->api_gen;
+    if (on && !ctx->px.world) return fail(WGKV_ESTATE, "peer_decode: no peer regions attached");
+    ctx->peer_decode = on != 0;
+    return WGKV_OK;
+}
+
+int wgkv_peer_result(wgkv_ctx* ctx, int back, void** ptr) {
+    if (!ctx || !ptr) return fail(WGKV_EINVAL, "null argument");
+    ++ctx->api_gen;
+    if (!ctx->px.world) return fail(WGKV_ESTATE, "peer_result: no peer regions attached");
+    if (back < 0 || back >= kPeerSlots || (uint64_t)back >= ctx->peer_seq)
+        return fail(WGKV_EINVAL, "peer_result: no such exchange");
+    const int slot = (int)((ctx->peer_seq - 1 - back) % kPeerSlots);
+    *ptr = ctx->px.peers.base[ctx->px.rank] + peer_res_off(ctx->px, slot);
     return WGKV_OK;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include "append.cuh"
 #include "fused.cuh"
+#include "comm.cuh"
 #include "common.cuh"
 #include "gate.cuh"
 
@@ -81,6 +82,9 @@ struct FinishArgs {
     bool gate_side;  // the append's gate CTAs run in their own launch on a side stream
     FusedWork fw;    // fused layer scratch (this layer's parity halves); cnt_items null = not available
     __nv_bfloat16* out;  // fused layer: the attention output [nseq][q_heads][d] (set by the launcher)
+    // C1 over peer memory (comm.cuh): the merges also push the output rows into
+    // every rank's exchange slot; one extra K5 CTA unpacks the previous exchange
+    PeerXchg px;
 };
 
 // counter_reset_by_append: the kernel just before on the stream zeroed the work

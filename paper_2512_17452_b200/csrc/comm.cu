@@ -136,4 +136,50 @@ int launch_assemble(const uint8_t* stage, uint8_t* out, long rows, int world, si
     return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
 }
 
+
+// ---- C1 over peer memory (decode-sized exchanges; layout in comm.cuh) ----------
+namespace {
+
+// this rank's rows [rows][blk] as LL words into every rank's push slot
+__global__ void __launch_bounds__(256) peer_push_kernel(const uint8_t* __restrict__ src, PeerXchg x, long rows) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // src: the attention output in front of us
+    const uint32_t flag = peer_push_flag(x);
+    const int wpr = x.blk / 4;
+    const long total = rows * wpr;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x)
+        peer_push_word(x, flag, i / wpr, (int)(i % wpr), reinterpret_cast<const uint32_t*>(src)[i]);
+}
+
+__global__ void __launch_bounds__(256) peer_unpack_kernel(PeerXchg x) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    peer_unpack_cta(x);
+}
+
+template <typename K, typename... Args>
+int launch_pdl(K kern, int grid, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
+
+}  // namespace
+
+int launch_peer_push(const uint8_t* src, const PeerXchg& x, long rows, cudaStream_t st) {
+    const long total = rows * (x.blk / 4);
+    return launch_pdl(peer_push_kernel, (int)std::max<long>(1, std::min<long>((total + 255) / 256, 64)), st, src, x,
+                      rows);
+}
+
+int launch_peer_unpack(const PeerXchg& x, cudaStream_t st) { return launch_pdl(peer_unpack_kernel, 1, st, x); }
+
 }  // namespace wgkv

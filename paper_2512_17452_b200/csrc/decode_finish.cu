@@ -45,6 +45,10 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         TL_COMMIT(3, a.layer, 0);
         return;
     }
+    if (fin.px.do_unpack && blockIdx.x == gridDim.x - 1) {  // ---- C1: the previous layer's peer exchange
+        peer_unpack_cta(fin.px);
+        return;
+    }
     if ((int)blockIdx.x >= ngate + ncomb) {  // ---- route CTAs of the append (K4, append.cuh)
         // reads and routing run while K5 streams; the ring-slot stores wait for it
         append_role<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, a.window, a.n_pairs, blockIdx.x - ngate - ncomb,
@@ -174,6 +178,12 @@ __global__ void __launch_bounds__(kAppendThreads) decode_finish_kernel(DecArgs a
         }
         out[((size_t)s * a.q_heads + p) * d + e] = __float2bfloat16_rn(t / L);
     }
+    if (fin.px.do_push) {  // C1: this row into every rank's exchange slot (LL words)
+        __syncthreads();   // the row's stores above, by the other threads
+        const uint32_t flag = peer_push_flag(fin.px);
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(out + ((size_t)s * a.q_heads + p) * d);
+        for (int j = tid; j < d / 2; j += blockDim.x) peer_push_word(fin.px, flag, s, (p * d) / 2 + j, row[j]);
+    }
     TL_COMMIT(1, a.layer, nch);
 }
 
@@ -189,7 +199,7 @@ int launch_decode_finish(const DecArgs& a, int nseq, const __nv_bfloat16* q, con
     if (ensure_smem(decode_finish_kernel, smem) != cudaSuccess) return WGKV_ECUDA;
     // programmatic dependent of K5: the launch overlaps K5's tail
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ncomb + napp);
+    cfg.gridDim = dim3(ncomb + napp + (fin.px.do_unpack ? 1 : 0));
     cfg.blockDim = dim3(kAppendThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;

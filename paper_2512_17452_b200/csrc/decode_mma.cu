@@ -257,8 +257,11 @@ __device__ __forceinline__ void fused_tail(const DecArgs& a, const FinishArgs& f
                 reinterpret_cast<float2*>(acc)[e] = t;
             } else {
                 const float il = 1.f / s_L[g];
-                *reinterpret_cast<__nv_bfloat162*>(fin.out + ((size_t)s * a.q_heads + h * gs + g) * d + col) =
-                    __floats2bfloat162_rn(t.x * il, t.y * il);
+                const __nv_bfloat162 ov = __floats2bfloat162_rn(t.x * il, t.y * il);
+                *reinterpret_cast<__nv_bfloat162*>(fin.out + ((size_t)s * a.q_heads + h * gs + g) * d + col) = ov;
+                if (fin.px.do_push)  // C1: the same 4 bytes into every rank's exchange slot (LL words)
+                    peer_push_word(fin.px, peer_push_flag(fin.px), s, ((h * gs + g) * d + col) / 2,
+                                   *reinterpret_cast<const uint32_t*>(&ov));
             }
         }
     }
@@ -322,6 +325,9 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         if ((s_rlast & 1) && warp == 0)
             fused_commit_kv<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.k_new, fin.v_new, fin.forced_g,
                                            fin.tr, fin.wk, fin.fw, nullptr, nullptr);
+        // C1 (fused layer): route CTA 0 also unpacks the previous layer's peer
+        // exchange (it has finished its own role; nothing waits for it here)
+        if (pr == 0 && fin.px.do_unpack) peer_unpack_cta(fin.px);
         TL_COMMIT(5, a.layer, 0);
         return;
     }
@@ -874,6 +880,9 @@ int launch_decode_attn_mma(const DecArgs& a0, int nseq, const __nv_bfloat16* q, 
         a.n_gate_ctas = ngate;
         fa = *fin;
     }
+    // C1 over peer memory: the fused layer's merges push and its route CTA 0
+    // unpacks; otherwise the finish kernel does both (fin->px)
+    if (!a.fused) fa.px = PeerXchg{};
     a.early_trigger = fin && !no_trigger;
     a.prewait = fin && fin->prewait;
     cudaLaunchConfig_t cfg = {};
