@@ -267,15 +267,22 @@ def run_gpu(args, cfg):
         dist.broadcast_object_list(box, src=0)
         sess.comm_init(box[0], world, rank)
     peer = shards > 1 and args.decode_exchange == "peer"
+    peer_pf = shards > 1 and args.prefill_exchange == "peer"
     peer_regions = None
-    if peer:  # decode C1 over peer memory: every rank's exchange region mapped here
+    if peer or peer_pf:  # C1 over peer memory: every rank's exchange region mapped here
+        bulk = B * T if peer_pf else 0
         if world > 1:
-            sess.peer_init(world, rank, B)  # IPC handles exchanged over torch.distributed
-        else:  # emulated shard: the other ranks' regions live on this GPU, only rank 0's arrivals are awaited
-            nb = sess.peer_region_bytes(shards, B)
-            peer_regions = [torch.zeros(nb, dtype=torch.uint8, device=dev) for _ in range(shards)]
-            sess.peer_attach(shards, 0, B, peer_regions, wait_ranks=1)
-        sess.peer_decode(True)  # every decode layer pushes its rows from inside its merge
+            sess.peer_init(world, rank, B, bulk)  # IPC handles exchanged over torch.distributed
+        else:  # emulated shard: the other ranks' regions live on this GPU (one region stands for all of
+            # them: rank 0's stores to each remote rank land in it), only rank 0's words / signal are awaited
+            nb = sess.peer_region_bytes(shards, B, bulk)
+            peer_regions = [torch.zeros(nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+            sess.peer_attach(shards, 0, B, [peer_regions[0]] + [peer_regions[1]] * (shards - 1), wait_ranks=1,
+                             max_bulk_rows=bulk)
+        if peer:
+            sess.peer_decode(True)  # every decode layer pushes its rows from inside its merge
+        if peer_pf:
+            sess.peer_prefill(True)  # K3's epilogue stores its rows into every rank's bulk slot
     # ---- resident inputs: `slots` distinct layer-input sets ------------------
     slots = max(1, min(args.slots, L))
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
@@ -301,11 +308,14 @@ def run_gpu(args, cfg):
     # comm stream while layer l+1's attention writes the other buffer
     outs = [torch.empty(B, T, hq, d, dtype=torch.bfloat16, device=dev) for _ in range(2 if shards > 1 else 1)]
     dout = torch.empty(B, hq, d, dtype=torch.bfloat16, device=dev)
-    full = torch.empty(B, T, Hq, d, dtype=torch.bfloat16, device=dev) if shards > 1 else None
+    full = (torch.empty(B, T, Hq, d, dtype=torch.bfloat16, device=dev)
+            if shards > 1 and args.prefill_exchange == "nccl" else None)
     dfull = torch.empty(B, Hq, d, dtype=torch.bfloat16, device=dev) if shards > 1 else None
     # emulated shard: the rank-major receive buffer NCCL would fill
-    stage = torch.zeros(shards, B * T, hq * d, dtype=torch.bfloat16, device=dev) if world == 1 and shards > 1 else None
-    dstage = torch.zeros(shards, B, hq * d, dtype=torch.bfloat16, device=dev) if stage is not None else None
+    stage = (torch.zeros(shards, B * T, hq * d, dtype=torch.bfloat16, device=dev)
+             if world == 1 and shards > 1 and args.prefill_exchange == "nccl" else None)
+    dstage = (torch.zeros(shards, B, hq * d, dtype=torch.bfloat16, device=dev)
+              if world == 1 and shards > 1 and args.decode_exchange == "nccl" else None)
 
     # ---- calibrate b2 per (layer, kv head) to admission a ---------------------
     ztau = math.log(cfg["tau"] / (1 - cfg["tau"]))
@@ -330,7 +340,10 @@ def run_gpu(args, cfg):
     def exchange_prefill(o_):
         """C1 after a layer's attention: the all-gather of head outputs on the
         context's comm stream (overlapping the next layer), or its local part
-        (the assembly) when one GPU emulates a shard."""
+        (the assembly) when one GPU emulates a shard; nothing with the peer
+        exchange (K3 itself stored the rows into every rank's bulk slot)."""
+        if peer_pf:
+            return
         if world > 1:
             sess.comm_join()  # the previous layer's exchange is done: its buffer may be rewritten
             sess.allgather_heads(o_, full, async_=True)
@@ -660,6 +673,16 @@ def run_gpu(args, cfg):
     return rank, res
 
 
+def _e2e_per_gpu(e2e, world, shards):
+    """An emulated shard (one GPU, N shards) reports decode per GPU of the
+    N-GPU job like the device-timed line: the job's tok/s over N GPUs."""
+    if e2e is None or not (world == 1 and shards > 1):
+        return e2e
+    e2e = dict(e2e)
+    e2e["decode_tok_s_per_gpu"] = e2e["decode_tok_s_per_gpu"] / shards
+    return e2e
+
+
 def _count_wgkv_kernels(raw_graph):
     """Kernel nodes of a captured CUDA graph whose function is one of this
     library's (mangled names in namespace wgkv); None if the graph cannot be read."""
@@ -701,6 +724,8 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="issue decode kernels eagerly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-T", type=int, default=16384)
+    ap.add_argument("--prefill-exchange", default="peer", choices=["peer", "nccl"],
+                    help="prefill C1 (N > 1): fused into K3's epilogue over peer memory, or NCCL all-gather + assembly")
     ap.add_argument("--decode-exchange", default="peer", choices=["peer", "nccl", "none"],
                     help="decode C1 (N > 1): push kernel over peer memory (wgkv_peer_*) or NCCL all-gather + assembly "
                          "('none': no exchange, diagnostics only)")
@@ -789,18 +814,19 @@ def main():
                             "bytes_per_decode_step": dec_bytes / D,
                             "note": "resident Global+Local K+V bytes (bf16) + q/out per token-step / decode time"},
         "clocks": r["clocks"], "gpu_launches": r["launches"],
-        "decode_kernels_per_layer": r["dec_kernels_per_layer"], "e2e": r["e2e"],
+        "decode_kernels_per_layer": r["dec_kernels_per_layer"], "e2e": _e2e_per_gpu(r["e2e"], world, shards),
     }
     if world == 1 and shards > 1:
         line["emulated_shard"] = {
             "n": shards, "kv_heads_per_gpu": r["hkv"], "q_heads_per_gpu": r["hq"],
-            "decode_exchange": args.decode_exchange,
-            "note": "one GPU runs rank 0's shard (its heads of every token) plus the head all-gather's local part "
-                    "(prefill: the assembly kernel; decode with decode_exchange 'peer': each layer's merge stores "
-                    "rank 0's rows as LL words into all N ranks' regions -- here all on this GPU -- and the next "
-                    "layer unpacks rank 0's words; 'nccl': the assembly kernel); 'value' is the whole-job prefill "
-                    "tok/s if every shard ran this fast on its own GPU; the NVLink transfer latency is NOT included "
-                    "and no scaling curve was measured"}
+            "decode_exchange": args.decode_exchange, "prefill_exchange": args.prefill_exchange,
+            "note": "one GPU runs rank 0's shard (its heads of every token) plus the head all-gather's local part. "
+                    "Prefill 'peer': K3's epilogue stores rank 0's rows into all N ranks' bulk slots (the N-1 remote "
+                    "ones land in one region on this GPU), then the signal / wait kernels; 'nccl': the assembly "
+                    "kernel. Decode 'peer': each layer's merge stores rank 0's rows as LL words into all N ranks' "
+                    "regions and the next layer unpacks rank 0's words; 'nccl': the assembly kernel. 'value' is the "
+                    "whole-job prefill tok/s if every shard ran this fast on its own GPU; the NVLink transfer latency "
+                    "is NOT included and no scaling curve was measured"}
     if not args.no_cpu_baseline:
         try:
             cb = cpu_reference(cfg, args.cpu_sample_T, 1)

@@ -257,14 +257,27 @@ int wgkv_comm_join(wgkv_ctx* ctx);
  * multiple of 4 of them and leaves none pending; bf16 contexts.  wait_ranks
  * = world normally (fewer only to emulate a shard on one GPU: only ranks
  * [0, wait_ranks) are awaited and unpacked). */
-int wgkv_peer_region_bytes(int world, long max_rows, int q_heads, int head_dim, int dtype, size_t* bytes);
-int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, uint8_t* ipc_handle64, void** base);
+int wgkv_peer_region_bytes(int world, long max_rows, long max_bulk_rows, int q_heads, int head_dim, int dtype,
+                           size_t* bytes);
+int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, long max_bulk_rows, uint8_t* ipc_handle64,
+                    void** base);
 int wgkv_peer_open(wgkv_ctx* ctx, int world, int rank, const uint8_t* handles /* world x 64 */, int wait_ranks);
-int wgkv_peer_attach(wgkv_ctx* ctx, int world, int rank, long max_rows, void* const* bases, int wait_ranks);
+int wgkv_peer_attach(wgkv_ctx* ctx, int world, int rank, long max_rows, long max_bulk_rows, void* const* bases,
+                     int wait_ranks);
 int wgkv_peer_allgather_heads(wgkv_ctx* ctx, long rows, const void* local_out, int wait);
 int wgkv_peer_wait(wgkv_ctx* ctx);
 int wgkv_peer_decode(wgkv_ctx* ctx, int on);
 int wgkv_peer_result(wgkv_ctx* ctx, int back, void** ptr);
+/* prefill: with a bulk part (max_bulk_rows > 0: two slots of [max_bulk_rows]
+ * [world * q_heads][d]) and wgkv_peer_prefill(ctx, 1), wgkv_vs_prefill's
+ * tcgen05 epilogue stores each output row into every rank's bulk slot as well
+ * as into `out` (the all-gather fused into the attention: NVLink stores
+ * overlap the tensor-core work), then a signal kernel (system fence, this
+ * rank's flag into every region) and a wait kernel (every rank's flag here).
+ * Rows are (seq - seq0) * T + t of the call.  wgkv_peer_bulk_result(back):
+ * the bulk slot of the last (0) or previous (1) prefill exchange. */
+int wgkv_peer_prefill(wgkv_ctx* ctx, int on);
+int wgkv_peer_bulk_result(wgkv_ctx* ctx, int back, void** ptr);
 /* ---- f3: output projection overlapped with the head all-gather -----------
  * Session's x[t] += Wo . concat[t] (engine.cpp:243-245 prefill, :331 decode)
  * on top of wgkv_allgather_heads: local_out [nseq][T][q_heads][d] (bf16, this

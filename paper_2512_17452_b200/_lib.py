@@ -82,10 +82,12 @@ SIGNATURES = {
     "wgkv_comm_attach": ([_vp, _vp, _i, _i], _i),
     "wgkv_allgather_heads": ([_vp, _i, _l, _vp, _vp, _i], _i),
     "wgkv_comm_join": ([_vp], _i),
-    "wgkv_peer_region_bytes": ([_i, _l, _i, _i, _i, _vp], _i),
-    "wgkv_peer_alloc": ([_vp, _i, _l, _vp, _vp], _i),
+    "wgkv_peer_region_bytes": ([_i, _l, _l, _i, _i, _i, _vp], _i),
+    "wgkv_peer_alloc": ([_vp, _i, _l, _l, _vp, _vp], _i),
     "wgkv_peer_open": ([_vp, _i, _i, _vp, _i], _i),
-    "wgkv_peer_attach": ([_vp, _i, _i, _l, _vp, _i], _i),
+    "wgkv_peer_attach": ([_vp, _i, _i, _l, _l, _vp, _i], _i),
+    "wgkv_peer_prefill": ([_vp, _i], _i),
+    "wgkv_peer_bulk_result": ([_vp, _i, _vp], _i),
     "wgkv_peer_allgather_heads": ([_vp, _l, _vp, _i], _i),
     "wgkv_peer_wait": ([_vp], _i),
     "wgkv_peer_decode": ([_vp, _i], _i),

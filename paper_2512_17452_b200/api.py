@@ -226,18 +226,18 @@ class Session:
         check(self.lib.wgkv_comm_join(self.h), "comm_join")
 
     # ---- C1 over NVLink peer memory (decode-sized exchanges) -------------------
-    def peer_region_bytes(self, world: int, max_rows: int) -> int:
+    def peer_region_bytes(self, world: int, max_rows: int, max_bulk_rows: int = 0) -> int:
         n = C.c_size_t(0)
-        check(self.lib.wgkv_peer_region_bytes(world, max_rows, self.cfg.q_heads, self.cfg.head_dim, self.cfg.dtype,
-                                              C.byref(n)),
+        check(self.lib.wgkv_peer_region_bytes(world, max_rows, max_bulk_rows, self.cfg.q_heads, self.cfg.head_dim,
+                                              self.cfg.dtype, C.byref(n)),
               "peer_region_bytes")
         return n.value
 
-    def peer_alloc(self, world: int, max_rows: int) -> bytes:
+    def peer_alloc(self, world: int, max_rows: int, max_bulk_rows: int = 0) -> bytes:
         """Allocate this rank's exchange region; returns its 64-byte IPC handle."""
         buf = C.create_string_buffer(64)
         base = C.c_void_p()
-        check(self.lib.wgkv_peer_alloc(self.h, world, max_rows, buf, C.byref(base)), "peer_alloc")
+        check(self.lib.wgkv_peer_alloc(self.h, world, max_rows, max_bulk_rows, buf, C.byref(base)), "peer_alloc")
         self._peer = dict(world=world, max_rows=max_rows, base=base.value, keep=None)
         return buf.raw
 
@@ -247,19 +247,20 @@ class Session:
         check(self.lib.wgkv_peer_open(self.h, world, rank, blob, wait_ranks or world), "peer_open")
         self._peer.update(rank=rank)
 
-    def peer_init(self, world: int, rank: int, max_rows: int, group=None):
+    def peer_init(self, world: int, rank: int, max_rows: int, max_bulk_rows: int = 0, group=None):
         """peer_alloc + handle exchange over torch.distributed (the caller's
         plumbing; any backend) + peer_open."""
         import torch.distributed as dist
-        mine = self.peer_alloc(world, max_rows)
+        mine = self.peer_alloc(world, max_rows, max_bulk_rows)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         self.peer_open(world, rank, allh)
 
-    def peer_attach(self, world: int, rank: int, max_rows: int, regions, wait_ranks=None):
+    def peer_attach(self, world: int, rank: int, max_rows: int, regions, wait_ranks=None, max_bulk_rows: int = 0):
         """Attach already-mapped regions (uint8 tensors of peer_region_bytes each, rank order)."""
         arr = (C.c_void_p * world)(*[r.data_ptr() for r in regions])
-        check(self.lib.wgkv_peer_attach(self.h, world, rank, max_rows, arr, wait_ranks or world), "peer_attach")
+        check(self.lib.wgkv_peer_attach(self.h, world, rank, max_rows, max_bulk_rows, arr, wait_ranks or world),
+              "peer_attach")
         self._peer = dict(world=world, max_rows=max_rows, base=regions[rank].data_ptr(), keep=list(regions),
                           rank=rank)
 
@@ -276,6 +277,16 @@ class Session:
     def peer_decode(self, on: bool = True):
         """Decode layers push their output rows from inside their merge (C1 fused into the layer)."""
         check(self.lib.wgkv_peer_decode(self.h, int(on)), "peer_decode")
+
+    def peer_prefill(self, on: bool = True):
+        """K3's epilogue stores its output rows into every rank's bulk slot (C1 fused into the attention)."""
+        check(self.lib.wgkv_peer_prefill(self.h, int(on)), "peer_prefill")
+
+    def peer_bulk_result(self, back: int, rows: int) -> torch.Tensor:
+        ptr = C.c_void_p()
+        check(self.lib.wgkv_peer_bulk_result(self.h, back, C.byref(ptr)), "peer_bulk_result")
+        world = self._peer["world"]
+        return _device_view(ptr.value, (rows, world * self.cfg.q_heads, self.cfg.head_dim), self.dtype, self.device)
 
     def peer_result(self, back: int, rows: int) -> torch.Tensor:
         ptr = C.c_void_p()

@@ -250,12 +250,14 @@ struct wgkv_ctx {
     PeerXchg px{};        // world = 0: not attached
     int peer_wait_ranks = 0;
     bool peer_decode = false;     // decode layers push their output rows themselves
+    bool peer_prefill = false;    // K3 stores its output rows into every rank's bulk slot
+    uint64_t peer_bulk_seq = 0;   // bulk exchanges so far (slot = seq % 2)
     uint64_t peer_seq = 0;        // exchanges so far (slot = seq % kPeerSlots)
     int pend_slot = -1;           // the last exchange, not unpacked yet
     long pend_rows = 0;
     uint8_t* peer_own = nullptr;  // wgkv_peer_alloc's region
     int peer_own_world = 0;
-    long peer_own_rows = 0;
+    long peer_own_rows = 0, peer_own_bulk = 0;
     std::vector<void*> peer_ipc;  // regions opened with cudaIpcOpenMemHandle
     long stage_rows = 0;
     // f3 (outproj.cu): cuBLAS handle and the two-slot concat ring of the chunked Wo
@@ -736,6 +738,14 @@ int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const 
     a.freq = ctx->freq;
     a.bits = bits;
     a.chunk_off = ctx->ws_chunk;
+    if (ctx->peer_prefill) {  // C1 fused into K3: its epilogue also stores into every rank's bulk slot
+        if ((long)nseq * T > ctx->px.max_bulk_rows)
+            return fail(WGKV_EINVAL, "vs_prefill: nseq * T exceeds the peer exchange's max_bulk_rows");
+        a.pb.peers = ctx->px.peers;
+        a.pb.world = ctx->px.world;
+        a.pb.rank = ctx->px.rank;
+        a.pb.slot_off = peer_bulk_off(ctx->px, (int)(ctx->peer_bulk_seq % 2));
+    }
     if (ctx->use_tc())
         st = launch_vs_prefill_tc(a, nseq, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k_post,
                                   (const __nv_bfloat16*)v, (__nv_bfloat16*)out, ctx->stream);
@@ -749,6 +759,11 @@ int wgkv_vs_prefill(wgkv_ctx* ctx, int layer, int seq0, int nseq, long T, const 
         const std::string detail = wgkv_last_error();  // the launcher's own message, if it set one
         return fail(st, std::string("vs prefill kernel: ") + cudaGetErrorString(cudaGetLastError()) +
                             (detail.empty() ? "" : " [" + detail + "]"));
+    }
+    if (ctx->peer_prefill) {  // completion: this rank's flag in every region, then every rank's here
+        st = launch_peer_bulk_signal_wait(ctx->px, ctx->peer_wait_ranks, ctx->stream);
+        if (st) return fail(st, "peer bulk signal / wait kernels failed");
+        ++ctx->peer_bulk_seq;
     }
     return WGKV_OK;
 }
@@ -1333,25 +1348,24 @@ int wgkv_comm_join(wgkv_ctx* ctx) {
 
 // ---- C1 over peer memory ----------------------------------------------------
 
-static size_t peer_region(int world, long max_rows, int blk) {
-    return kPeerHeader + kPeerSlots * (peer_ll_bytes(world, max_rows, blk) + peer_res_bytes(world, max_rows, blk));
-}
-
-int wgkv_peer_region_bytes(int world, long max_rows, int q_heads, int head_dim, int dtype, size_t* bytes) {
-    if (!bytes || world < 1 || world > kMaxPeers || max_rows < 1 || q_heads < 1 || head_dim < 1 ||
-        (dtype != WGKV_BF16 && dtype != WGKV_F32))
+int wgkv_peer_region_bytes(int world, long max_rows, long max_bulk_rows, int q_heads, int head_dim, int dtype,
+                           size_t* bytes) {
+    if (!bytes || world < 1 || world > kMaxPeers || max_rows < 1 || max_bulk_rows < 0 || q_heads < 1 ||
+        head_dim < 1 || (dtype != WGKV_BF16 && dtype != WGKV_F32))
         return fail(WGKV_EINVAL, "peer_region_bytes: bad argument");
-    *bytes = peer_region(world, max_rows, q_heads * head_dim * (dtype == WGKV_BF16 ? 2 : 4));
+    *bytes = peer_region_size(world, max_rows, max_bulk_rows, q_heads * head_dim * (dtype == WGKV_BF16 ? 2 : 4));
     return WGKV_OK;
 }
 
-int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, uint8_t* ipc_handle64, void** base) {
+int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, long max_bulk_rows, uint8_t* ipc_handle64,
+                    void** base) {
     if (!ctx || !ipc_handle64) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
     ++ctx->api_gen;
     if (ctx->peer_own) return fail(WGKV_ESTATE, "peer_alloc: region already allocated");
     size_t bytes = 0;
-    int st = wgkv_peer_region_bytes(world, max_rows, ctx->cfg.q_heads, ctx->cfg.head_dim, ctx->cfg.dtype, &bytes);
+    int st = wgkv_peer_region_bytes(world, max_rows, max_bulk_rows, ctx->cfg.q_heads, ctx->cfg.head_dim,
+                                    ctx->cfg.dtype, &bytes);
     if (st) return st;
     WGKV_CUDA_TRY(cudaMalloc(&ctx->peer_own, bytes));
     WGKV_CUDA_TRY(cudaMemset(ctx->peer_own, 0, bytes));
@@ -1361,6 +1375,7 @@ int wgkv_peer_alloc(wgkv_ctx* ctx, int world, long max_rows, uint8_t* ipc_handle
     std::memcpy(ipc_handle64, &h, 64);
     ctx->peer_own_world = world;
     ctx->peer_own_rows = max_rows;
+    ctx->peer_own_bulk = max_bulk_rows;
     if (base) *base = ctx->peer_own;
     return WGKV_OK;
 }
@@ -1374,16 +1389,19 @@ static int peer_check_args(wgkv_ctx* ctx, int world, int rank, long max_rows, in
     return WGKV_OK;
 }
 
-static int peer_bind(wgkv_ctx* ctx, int world, int rank, long max_rows, uint8_t* const* bases, int wait_ranks) {
+static int peer_bind(wgkv_ctx* ctx, int world, int rank, long max_rows, long max_bulk_rows, uint8_t* const* bases,
+                     int wait_ranks) {
     PeerXchg x{};
     for (int p = 0; p < world; ++p) x.peers.base[p] = bases[p];
     x.world = world;
     x.rank = rank;
     x.blk = ctx->cfg.q_heads * ctx->cfg.head_dim * (int)ctx->esz;
     x.max_rows = max_rows;
+    x.max_bulk_rows = max_bulk_rows;
     ctx->px = x;
     ctx->peer_wait_ranks = wait_ranks;
     ctx->peer_seq = 0;
+    ctx->peer_bulk_seq = 0;
     ctx->pend_slot = -1;
     return WGKV_OK;
 }
@@ -1414,22 +1432,24 @@ int wgkv_peer_open(wgkv_ctx* ctx, int world, int rank, const uint8_t* handles, i
         ctx->peer_ipc.push_back(ptr);
         bases[p] = static_cast<uint8_t*>(ptr);
     }
-    return peer_bind(ctx, world, rank, ctx->peer_own_rows, bases, wait_ranks);
+    return peer_bind(ctx, world, rank, ctx->peer_own_rows, ctx->peer_own_bulk, bases, wait_ranks);
 }
 
-int wgkv_peer_attach(wgkv_ctx* ctx, int world, int rank, long max_rows, void* const* bases, int wait_ranks) {
+int wgkv_peer_attach(wgkv_ctx* ctx, int world, int rank, long max_rows, long max_bulk_rows, void* const* bases,
+                     int wait_ranks) {
     if (!ctx || !bases) return fail(WGKV_EINVAL, "null argument");
     DevGuard dg_(ctx->cfg.device);
     ++ctx->api_gen;
     int st = peer_check_args(ctx, world, rank, max_rows, wait_ranks);
     if (st) return st;
+    if (max_bulk_rows < 0) return fail(WGKV_EINVAL, "peer_attach: max_bulk_rows < 0");
     uint8_t* b[kMaxPeers] = {};
     for (int p = 0; p < world; ++p) {
         b[p] = static_cast<uint8_t*>(bases[p]);
         if (!b[p] || reinterpret_cast<uintptr_t>(b[p]) % 16 != 0)
             return fail(WGKV_EINVAL, "peer_attach: null or unaligned region");
     }
-    return peer_bind(ctx, world, rank, max_rows, b, wait_ranks);
+    return peer_bind(ctx, world, rank, max_rows, max_bulk_rows, b, wait_ranks);
 }
 
 // the exchange description for the next push (rows) and the pending unpack
@@ -1496,6 +1516,26 @@ int wgkv_peer_decode(wgkv_ctx* ctx, int on) {
     ++ctx->api_gen;
     if (on && !ctx->px.world) return fail(WGKV_ESTATE, "peer_decode: no peer regions attached");
     ctx->peer_decode = on != 0;
+    return WGKV_OK;
+}
+
+int wgkv_peer_prefill(wgkv_ctx* ctx, int on) {
+    if (!ctx) return fail(WGKV_EINVAL, "null ctx");
+    ++ctx->api_gen;
+    if (on && (!ctx->px.world || ctx->px.max_bulk_rows < 1))
+        return fail(WGKV_ESTATE, "peer_prefill: no peer regions with a bulk part attached");
+    if (on && !ctx->use_tc()) return fail(WGKV_ENOTSUP, "peer_prefill: the tcgen05 prefill path only");
+    ctx->peer_prefill = on != 0;
+    return WGKV_OK;
+}
+
+int wgkv_peer_bulk_result(wgkv_ctx* ctx, int back, void** ptr) {
+    if (!ctx || !ptr) return fail(WGKV_EINVAL, "null argument");
+    ++ctx->api_gen;
+    if (!ctx->px.world || ctx->px.max_bulk_rows < 1) return fail(WGKV_ESTATE, "peer_bulk_result: no bulk part");
+    if (back < 0 || back >= 2 || (uint64_t)back >= ctx->peer_bulk_seq)
+        return fail(WGKV_EINVAL, "peer_bulk_result: no such exchange");
+    *ptr = ctx->px.peers.base[ctx->px.rank] + peer_bulk_off(ctx->px, (int)((ctx->peer_bulk_seq - 1 - back) % 2));
     return WGKV_OK;
 }
 

@@ -15,6 +15,7 @@ struct VsArgs {
     const double* freq;        // [d/2]
     const uint8_t* bits;       // [nseq][kv_heads][T]
     const int32_t* chunk_off;  // [nseq][kv_heads][nchunk+1] admitted-before-chunk (K2)
+    PeerBulk pb;               // C1 fused into K3 (tcgen05 path): output rows into every rank's bulk slot
 };
 
 // partial-buffer chunks per (seq, kv head): enough for a single kv head to

@@ -579,12 +579,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc::tmem_ld_wait();
             if (i < T) {
                 uint4* dst = reinterpret_cast<uint4*>(orow + 32 * k);
+                uint4 ov[4];
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4)
-                    dst[q4] = make_uint4(tc::pack_bf16x2(__uint_as_float(o[8 * q4]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
-                                         tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
-                                         tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
-                                         tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    ov[q4] = make_uint4(tc::pack_bf16x2(__uint_as_float(o[8 * q4]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
+                                        tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
+                                        tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
+                                        tc::pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
+                    dst[q4] = ov[q4];
+                }
+                if (a.pb.world) {  // C1: the same 64 bytes into every rank's bulk slot (NVLink stores)
+                    const size_t off = a.pb.slot_off +
+                                       ((((size_t)s * T + i) * a.pb.world + a.pb.rank) * Hq + p0 + t) * 256 +
+                                       (size_t)(HC * c + 32 * k) * 2;
+#pragma unroll 1
+                    for (int pp = 0; pp < a.pb.world; ++pp) {
+                        uint4* pd = reinterpret_cast<uint4*>(a.pb.peers.base[pp] + off);
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) pd[q4] = ov[q4];
+                    }
+                }
             }
         }
     }

@@ -157,6 +157,34 @@ __global__ void __launch_bounds__(256) peer_unpack_kernel(PeerXchg x) {
     peer_unpack_cta(x);
 }
 
+// after K3 (stream order: its stores, local and remote, are performed): a
+// system-scope fence, then this rank's flag (bulk epoch + 1) in every region
+__global__ void peer_bulk_signal_kernel(PeerXchg x) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(x.peers.base[x.rank] + 4 * kPeerBulkEpoch) + 1u;
+    for (int p = 0; p < x.world; ++p)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.peers.base[p] + 4 * (kPeerBulkFlag + x.rank)),
+                     "r"(e)
+                     : "memory");
+}
+
+// every awaited rank's flag has reached this exchange (>=: a faster rank may
+// already have signalled the next one), then the epoch advances
+__global__ void peer_bulk_wait_kernel(PeerXchg x, int ranks) {
+    if (threadIdx.x != 0) return;
+    uint8_t* own = x.peers.base[x.rank];
+    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(own + 4 * kPeerBulkEpoch) + 1u;
+    for (int r = 0; r < ranks; ++r) {
+        uint32_t f;
+        do {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(own + 4 * (kPeerBulkFlag + r)) : "memory");
+            if ((int)(f - e) < 0) __nanosleep(64);
+        } while ((int)(f - e) < 0);
+    }
+    *reinterpret_cast<volatile uint32_t*>(own + 4 * kPeerBulkEpoch) = e;
+}
+
 template <typename K, typename... Args>
 int launch_pdl(K kern, int grid, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
@@ -181,5 +209,11 @@ int launch_peer_push(const uint8_t* src, const PeerXchg& x, long rows, cudaStrea
 }
 
 int launch_peer_unpack(const PeerXchg& x, cudaStream_t st) { return launch_pdl(peer_unpack_kernel, 1, st, x); }
+
+int launch_peer_bulk_signal_wait(const PeerXchg& x, int ranks, cudaStream_t st) {
+    peer_bulk_signal_kernel<<<1, 32, 0, st>>>(x);
+    peer_bulk_wait_kernel<<<1, 32, 0, st>>>(x, ranks);
+    return cudaGetLastError() == cudaSuccess ? WGKV_OK : WGKV_ECUDA;
+}
 
 }  // namespace wgkv

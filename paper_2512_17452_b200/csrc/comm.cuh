@@ -20,14 +20,20 @@ int launch_assemble(const uint8_t* stage, uint8_t* out, long rows, int world, si
 
 // ---- C1 over peer memory (comm.cu) --------------------------------------------
 // Every rank owns an exchange region, mapped into every rank:
-//   [kPeerHeader: uint32 epoch per slot][kPeerSlots LL slots][kPeerSlots result slots]
+//   [kPeerHeader: uint32 epoch per slot, bulk epoch, bulk flags][kPeerSlots LL slots]
+//   [kPeerSlots result slots][2 bulk slots]
 // LL slot: [max_rows][world][blk / 4] 8-byte words {4 data bytes, 4 flag bytes}
 // (the flag is the slot's epoch + 1: a reader polls the data itself, so a push
 // needs no fence and no counter); result slot: [max_rows][world * blk] bytes,
 // the reference's concat layout.  Exchange k uses slot k % kPeerSlots.
+// Bulk slot (prefill): [max_bulk_rows][world * blk], written by K3's epilogue
+// straight into every rank's region (plain stores: the data is large, the
+// completion is one flag per rank: fence + release store, acquire polls).
 constexpr int kMaxPeers = 8;
 constexpr int kPeerSlots = 4;        // see wgkv_b200.h: the slot reuse distance that no rank can outrun
 constexpr size_t kPeerHeader = 256;  // uint32 epoch per slot, padded
+constexpr int kPeerBulkEpoch = 16;   // header word: bulk exchanges completed here
+constexpr int kPeerBulkFlag = 32;    // header words [32, 32 + kMaxPeers): rank r's last bulk signal
 
 struct PeerBases {
     uint8_t* base[kMaxPeers];  // every rank's region, as mapped in this process
@@ -40,6 +46,7 @@ struct PeerXchg {
     int world, rank;
     int blk;        // bytes of one row of one rank (q_heads * d * esz)
     long max_rows;
+    long max_bulk_rows;
     int do_push, push_slot;                               // push this layer's output rows
     int do_unpack, unpack_slot, unpack_rows, unpack_ranks;  // unpack a pending exchange (one CTA)
 };
@@ -51,6 +58,13 @@ __host__ __device__ inline size_t peer_ll_bytes(int world, long max_rows, int bl
 __host__ __device__ inline size_t peer_res_bytes(int world, long max_rows, int blk) {
     return peer_round((size_t)max_rows * world * blk);
 }
+__host__ __device__ inline size_t peer_bulk_bytes(int world, long max_bulk_rows, int blk) {
+    return peer_round((size_t)max_bulk_rows * world * blk);
+}
+__host__ __device__ inline size_t peer_region_size(int world, long max_rows, long max_bulk_rows, int blk) {
+    return kPeerHeader + kPeerSlots * (peer_ll_bytes(world, max_rows, blk) + peer_res_bytes(world, max_rows, blk)) +
+           2 * peer_bulk_bytes(world, max_bulk_rows, blk);
+}
 __host__ __device__ inline size_t peer_ll_off(const PeerXchg& x, int slot) {
     return kPeerHeader + (size_t)slot * peer_ll_bytes(x.world, x.max_rows, x.blk);
 }
@@ -58,6 +72,18 @@ __host__ __device__ inline size_t peer_res_off(const PeerXchg& x, int slot) {
     return kPeerHeader + kPeerSlots * peer_ll_bytes(x.world, x.max_rows, x.blk) +
            (size_t)slot * peer_res_bytes(x.world, x.max_rows, x.blk);
 }
+
+__host__ __device__ inline size_t peer_bulk_off(const PeerXchg& x, int slot) {
+    return kPeerHeader + kPeerSlots * (peer_ll_bytes(x.world, x.max_rows, x.blk) + peer_res_bytes(x.world, x.max_rows, x.blk)) +
+           (size_t)slot * peer_bulk_bytes(x.world, x.max_bulk_rows, x.blk);
+}
+
+// K3's view of a bulk exchange: its output rows also go to every rank's bulk slot
+struct PeerBulk {
+    PeerBases peers;
+    int world, rank;   // world = 0: off
+    size_t slot_off;   // byte offset of the bulk slot in every region
+};
 
 #ifdef __CUDACC__
 // the flag of this rank's push into x.push_slot: the slot's epoch (unpacks so
@@ -105,5 +131,7 @@ __device__ __forceinline__ void peer_unpack_cta(const PeerXchg& x) {
 // standalone kernels (wgkv_peer_allgather_heads, wgkv_peer_wait, non-deferred decode)
 int launch_peer_push(const uint8_t* src, const PeerXchg& x, long rows, cudaStream_t st);
 int launch_peer_unpack(const PeerXchg& x, cudaStream_t st);
+// bulk completion: this rank's signal to every rank, then the wait for ranks [0, ranks)
+int launch_peer_bulk_signal_wait(const PeerXchg& x, int ranks, cudaStream_t st);
 
 }  // namespace wgkv

@@ -177,6 +177,43 @@ def test_peer_topk_decode(W, orc):
         assert torch.equal(s.peer_result(back, B), got[-1 - back]), back
 
 
+@pytest.mark.parametrize("N", [2, 4])
+def test_peer_prefill_virtual_shards(W, orc, N):
+    """C1 fused into K3 (wgkv_peer_prefill): each virtual rank's tcgen05
+    epilogue stores its output rows into all N regions' bulk slots; after every
+    rank's layer each region's bulk slot equals the unsharded context's prefill
+    output BITWISE (the reference's concat layout), for two layers (both bulk
+    slots), and the layer outputs are unchanged by the exchange.  wait_ranks =
+    1: a virtual rank only awaits rank 0's signal, which precedes it on the
+    stream (no kernel waits on one enqueued after it)."""
+    B, T, hq, hkv, d, Wn, L = 2, 1000, 32, 8, 128, 256, 2
+    q, k, v, _, _, _ = _decode_inputs(21, L, B, T, hq, hkv, d, 1)
+    bank = orc.gate_random_init(L, hkv, d, d, 23, 0.1, -2.0)
+    mk = lambda hqs, hks, off: W.Session(L, hqs, hks, d, d, Wn, max_seqs=B, max_tokens=T,  # noqa: E731
+                                         gate_bank=bank, kv_head_offset=off, attn_impl=W.ATTN_TCGEN05)
+    full = mk(hq, hkv, 0)
+    ref = [full.prefill_layer(l, q[l], k[l], v[l]).clone() for l in range(L)]
+    full.sync()
+    hk, hqs = hkv // N, hq // N
+    parts = [mk(hqs, hk, r * hk) for r in range(N)]
+    nbytes = parts[0].peer_region_bytes(N, B, B * T)
+    regions = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(N)]
+    sl = lambda x, r, w: x[..., r * w:(r + 1) * w, :].contiguous()  # noqa: E731
+    for r, s in enumerate(parts):
+        s.peer_attach(N, r, B, regions, wait_ranks=1, max_bulk_rows=B * T)
+        s.peer_prefill(True)
+    for l in range(L):
+        for r, s in enumerate(parts):
+            out = s.prefill_layer(l, sl(q[l], r, hqs), sl(k[l], r, hk), sl(v[l], r, hk))
+            torch.cuda.synchronize()
+            assert torch.equal(out, sl(ref[l], r, hqs)), (N, l, r)
+        for r, s in enumerate(parts):
+            got = s.peer_bulk_result(0, B * T).view(B, T, hq, d)
+            assert torch.equal(got, ref[l]), (N, l, r)
+    for r, s in enumerate(parts):  # the previous layer's slot is intact
+        assert torch.equal(s.peer_bulk_result(1, B * T).view(B, T, hq, d), ref[L - 2]), (N, r)
+
+
 def test_peer_argument_errors(W, orc):
     hq, hkv, d, B = 8, 2, 128, 2
     s = W.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=64, gate_bank=orc.gate_random_init(1, hkv, d, d, 3))
@@ -197,6 +234,8 @@ def test_peer_argument_errors(W, orc):
         s.peer_allgather_heads(torch.zeros(B + 1, hq, d, dtype=torch.bfloat16, device="cuda"))
     with pytest.raises(ValueError):  # no exchange yet
         s.peer_result(0, B)
+    with pytest.raises(W._lib.LifecycleError):  # no bulk part attached
+        s.peer_prefill(True)
     out = s.peer_allgather_heads(x + 1)
     s.sync()
     assert out.shape == (B, 2 * hq, d)
@@ -206,3 +245,61 @@ def test_peer_argument_errors(W, orc):
     with pytest.raises(W._lib.NotSupported):  # fp32 contexts: no peer exchange
         f = W.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=64, dtype=W.F32)
         f.peer_attach(1, 0, B, [reg])
+
+
+def _ipc_rank(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        import paper_2512_17452_b200 as W_
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        hq, hkv, d, B = 4, 1, 128, 3
+        # the whole model's gate bank (every kv head); the shard keeps its rows
+        bank = 0.02 * np.random.default_rng(7).standard_normal((1, hkv * world, d * 2 * d + 2 * d + 1))
+        s = W_.Session(1, hq, hkv, d, d, 64, max_seqs=B, max_tokens=64, kv_head_offset=rank * hkv, gate_bank=bank)
+        s.peer_init(world, rank, B)  # cudaIpcMemHandle exchange over gloo + cudaIpcOpenMemHandle
+        xs = [torch.full((B, hq, d), float(r + 1), device="cuda").to(torch.bfloat16) +
+              torch.arange(B * hq * d, device="cuda").view(B, hq, d).to(torch.bfloat16) for r in range(world)]
+        for it in range(5):  # more exchanges than slots
+            s.peer_allgather_heads(xs[rank] * (it + 1), wait=False)
+            torch.cuda.synchronize()
+            dist.barrier()  # every rank's words are in before anyone unpacks: no kernel waits on another process
+            s.peer_wait()
+            torch.cuda.synchronize()
+            want = torch.cat([x * (it + 1) for x in xs], dim=1)
+            assert torch.equal(s.peer_result(0, B), want), (rank, it)
+            dist.barrier()
+        q.put((rank, "ok"))
+    except Exception as exc:  # reported to the parent
+        q.put((rank, repr(exc)))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_peer_ipc_two_processes(W):
+    """wgkv_peer_alloc / wgkv_peer_open across two processes (one process per
+    rank, as on an N-GPU box; here both on this GPU): the regions are mapped
+    through real cudaIpcMemHandle exchanges and each rank's LL words land in
+    the other's region.  Pushes complete (host barrier) before any rank
+    unpacks, so no kernel ever spins on another process's kernel."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p_ in ps:
+        p_.join(60)
+    assert res == {0: "ok", 1: "ok"}, res
