@@ -499,6 +499,10 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         }
     };
     __shared__ int s_item;
+#ifndef WGKV_K5_EARLY_ITEM
+#define WGKV_K5_EARLY_ITEM 1
+#endif
+    const bool early_item = WGKV_K5_EARLY_ITEM && !TOPK && a.defer && a.prewait && !a.fused;
     int next_draw = 0;  // fused layer: the next item's draw, claimed at the end of the previous item
     // first item static (kcta): no atomic round trip in front of it; later items
     // are stolen from kgrid on (the merging kernel resets the counter to 0 --
@@ -619,7 +623,11 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             tc::fence_proxy_async_smem();
             for (int k = 0; k < min(DNS, nmine); ++k) issue(k);
         }
-        publish_plan();
+        // two-kernel deferred layer behind another layer's finish kernel: the
+        // first item runs whole before the PDL wait (its pages, state and q
+        // are not the predecessor's; only its partial goes to the shared
+        // workspace, written after the wait below)
+        if (!(early_item && first)) publish_plan();
         // RoPE(q) at pos, pre-scaled by log2(e)/sqrt(d), split q = hi + lo into two
         // bf16 halves (to ~2^-17 relative): row r < 8 holds hi, row r + 8 its lo, so
         // the one m16 S MMA yields both halves' dots (gs <= 8) and the only score
@@ -751,6 +759,7 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
             }
         }
         __syncthreads();
+        publish_plan();  // the partial buffer is the predecessor's workspace (no-op after the first item)
         for (int e = tid; e < gs * d; e += blockDim.x) {
             const int g = e / d, c = e % d;
             float M = -INFINITY;
