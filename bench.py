@@ -44,7 +44,7 @@ CONFIGS = {
     # configs[1]: full 32-layer stack, 32K prefill, batch 1
     "32k": dict(workload="llama3.1-8b attention x32 layers, 32K prefill x batch 1 + decode (BASELINE configs[1])",
                 layers=32, q_heads=32, kv_heads=8, d=128, hidden=128, T=32768, batch=1, window=1024, admit=0.25,
-                tau=0.1, rope_base=5e5, page=16, decode_steps=64),
+                tau=0.1, rope_base=5e5, page=16, decode_steps=1024),  # configs[1]: 1K decode steps
 }
 
 
