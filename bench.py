@@ -121,6 +121,24 @@ def pair_count(bits, window):
     return band + c.sum(dim=-1)
 
 
+def executed_pairs(bits, window):
+    """(q, k) pairs K3's tcgen05 tiles actually compute per (seq, kv head) row
+    of bits [..., T] for ONE q head: every 128-row query tile runs full 128 x 128
+    S/PV blocks over its vertical prefix (ceil(C / 128) blocks, C = admitted
+    keys before the band) and its band (ceil(band / 128) blocks) -- the
+    masked-off entries of the edge blocks included (attn_tc.cu's block count)."""
+    import torch
+
+    T = bits.shape[-1]
+    pc = torch.nn.functional.pad(torch.cumsum(bits.to(torch.int64), dim=-1), (1, 0))  # admitted before x
+    i0 = torch.arange(0, T, 128, device=bits.device)
+    s_lo = torch.clamp(i0 - window + 1, min=0)
+    band = torch.clamp(i0 + 127, max=T - 1) - s_lo + 1
+    nv = (pc[..., s_lo] + 127) // 128
+    nb = (band + 127) // 128
+    return ((nv + nb) * 128 * 128).sum(dim=-1)
+
+
 # ------------------------------------------------------------ reference arm --
 def _ref_session(O, ref, cfg, hq, hkv, T, bank):
     return O.Session(ref, 1, hq, hkv, cfg["d"], cfg["hidden"], cfg["window"], tau=cfg["tau"],
@@ -465,13 +483,14 @@ def run_gpu(args, cfg):
         return e, k3
 
     # ---- warm-up (also: pair counts and resident bytes for the roofline) ----
-    pairs_layer = []
+    pairs_layer, exec_layer = [], []
     resident = None
     for wi in range(args.warmup):
         if wi == 0:
             for l in range(L):
                 prefill_layer(l)
                 pairs_layer.append(int(pair_count(bits_ws, Wn).sum().item()) * (hq // hkv))
+                exec_layer.append(int(executed_pairs(bits_ws, Wn).sum().item()) * (hq // hkv))
             if world > 1:
                 sess.comm_join()
             st0 = sess.stats(0, B)
@@ -665,6 +684,7 @@ def run_gpu(args, cfg):
     if world > 1:
         dist.barrier()
     res = dict(pre_s=pre_s, dec_s=dec_s, k3_s=k3_s, tot_s=tot_s, wall_s=t_wall, pairs_layer=pairs_layer,
+               exec_layer=exec_layer,
                resident=resident, clocks=clk.summary(), launches=launches["n"] // args.steps, e2e=e2e,
                dec_kernels_per_layer=(graph_kernels["n"] / L if graph_kernels["n"] else per_layer_dec),
                T=T, B=B, D=D, world=world, shards=shards, hq=hq, hkv=hkv)
@@ -779,6 +799,8 @@ def main():
     pairs = sum(r["pairs_layer"])  # this rank's q heads, all layers
     flops = 4.0 * d * pairs
     k3_tfs = flops / r["k3_s"] / 1e12
+    exec_flops = 4.0 * d * sum(r["exec_layer"])  # full 128 x 128 blocks K3 computes (north_star: FLOPs executed)
+    k3_exec_tfs = exec_flops / r["k3_s"] / 1e12
     # decode bytes per step (resident Global+Local K+V, bf16, each byte once per GQA group) + q/out
     res0, res1 = r["resident"]
     avg_res = 0.5 * (res0 + res1)
@@ -808,6 +830,10 @@ def main():
                      "frac_of_burst": k3_tfs / peaks["tf"], "peak_source": peaks["src"] + " bf16_tflops_sustained",
                      "traffic": traffic, "k3_share_of_prefill": r["k3_s"] / r["pre_s"],
                      "algorithmic_flops_per_step": flops,
+                     "executed": {"flops_per_step": exec_flops, "achieved": k3_exec_tfs,
+                                  "frac": k3_exec_tfs / peaks["tf_sus"],
+                                  "note": "the sparse FLOPs K3 actually executes (full 128x128 blocks of every "
+                                          "query tile's vertical prefix and band, edge masks included)"},
                      "note": "achieved = 4*d*sum(vs_mask_pair_count) over (seq, q head, layer) / K3 time (CUDA events)"},
         "decode_roofline": {"bound": "hbm", "achieved": dec_gbs, "peak": peaks["hbm"], "unit": "GB/s",
                             "frac": dec_gbs / peaks["hbm"], "frac_of_8TBps": dec_gbs / 8000.0,
