@@ -289,6 +289,9 @@ class Session:
         return _device_view(ptr.value, (rows, world * self.cfg.q_heads, self.cfg.head_dim), self.dtype, self.device)
 
     def peer_result(self, back: int, rows: int) -> torch.Tensor:
+        """View of this rank's result slot of the exchange `back` exchanges ago
+        (valid once unpacked; the view does not own the memory: it lives as
+        long as this Session)."""
         ptr = C.c_void_p()
         check(self.lib.wgkv_peer_result(self.h, back, C.byref(ptr)), "peer_result")
         world = self._peer["world"]

@@ -933,7 +933,7 @@ int wgkv_decode_attn(wgkv_ctx* ctx, int layer, int seq0, int nseq, const void* q
 }
 
 static PeerXchg peer_next(wgkv_ctx* ctx, bool push, bool unpack);
-static void peer_pushed(wgkv_ctx* ctx, long rows, bool unpacked_pending);
+static void peer_pushed(wgkv_ctx* ctx, long rows);
 static int peer_unpack_pending(wgkv_ctx* ctx);
 
 // One decode layer.  bf16 fast path: K5 streams the cache as it was before
@@ -962,7 +962,7 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
         st = launch_peer_push(static_cast<const uint8_t*>(out), peer_next(ctx, true, false), nseq, ctx->stream);
         if (st) return fail(st, "peer push kernel failed");
         if ((st = peer_unpack_pending(ctx))) return st;
-        peer_pushed(ctx, nseq, false);
+        peer_pushed(ctx, nseq);
         return WGKV_OK;
     }
     int st = decode_check(ctx, layer, seq0, nseq);
@@ -1015,7 +1015,7 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
     if (fin.gate_side) WGKV_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_gate, 0));
     if (st) return st;
     for (int s = seq0; s < seq0 + nseq; ++s) ctx->tokens[(size_t)layer * ctx->cfg.max_seqs + s] += 1;
-    if (ctx->peer_decode) peer_pushed(ctx, nseq, true);
+    if (ctx->peer_decode) peer_pushed(ctx, nseq);
     ctx->finish_gen = ctx->api_gen;
     ctx->finish_layer = layer;
     return WGKV_OK;
@@ -1464,8 +1464,9 @@ static PeerXchg peer_next(wgkv_ctx* ctx, bool push, bool unpack) {
     return x;
 }
 
-static void peer_pushed(wgkv_ctx* ctx, long rows, bool unpacked_pending) {
-    if (unpacked_pending) ctx->pend_slot = -1;
+// the exchange just pushed becomes the pending one (the previous pending one
+// was unpacked by the caller: peer_unpack_pending or the decode layer's CTA)
+static void peer_pushed(wgkv_ctx* ctx, long rows) {
     ctx->pend_slot = (int)(ctx->peer_seq % kPeerSlots);
     ctx->pend_rows = rows;
     ++ctx->peer_seq;
@@ -1494,7 +1495,7 @@ int wgkv_peer_allgather_heads(wgkv_ctx* ctx, long rows, const void* local_out, i
     int st = launch_peer_push(static_cast<const uint8_t*>(local_out), peer_next(ctx, true, false), rows, ctx->stream);
     if (st) return fail(st, "peer push kernel failed");
     if ((st = peer_unpack_pending(ctx))) return st;  // exchanges are unpacked in order
-    peer_pushed(ctx, rows, false);
+    peer_pushed(ctx, rows);
     if (wait && (st = peer_unpack_pending(ctx))) return st;
     peer_keep_chain(ctx, g0);
     return WGKV_OK;
