@@ -60,8 +60,10 @@ constexpr int kFusedMaxFront = WGKV_FUSED_MAX_FRONT;  // fused layer: route + ga
 #endif
 constexpr int kFusedMaxPairs = WGKV_FUSED_MAX_PAIRS;  // fused layer: (seq, kv head) pairs at most
 #ifndef WGKV_K5_IPC
-#define WGKV_K5_IPC 3  // work items per CTA (work stealing balance vs per-item fixed costs; 3 beats 2 by
-                       // 1.5 % at 128K x 4 and 2.2 % on the serving mix with 6-warp CTAs)
+#define WGKV_K5_IPC 0  // work items per CTA, 0 = by pair count: work stealing balance vs per-item fixed
+                       // costs.  With the first item before the PDL wait, 2 beats 3 by 2.4 % at 128K x 4
+                       // (32 pairs) and 1.8 % at 64K x 8 (64 pairs); 3 beats 2 by 1.5-3 % on the serving
+                       // mix (512 pairs) (profiles/r2_decode_peer_ab.txt)
 #endif
 #ifndef WGKV_K5_RULE
 #define WGKV_K5_RULE 1
@@ -428,7 +430,8 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         }
         const long total = tot;
         // ~2 items per CTA, taken dynamically (work stealing) for balance
-        int cp = (int)((total + WGKV_K5_IPC * kgrid - 1) / (WGKV_K5_IPC * kgrid));
+        const int ipc = WGKV_K5_IPC ? WGKV_K5_IPC : (npairs <= 64 ? 2 : 3);
+        int cp = (int)((total + ipc * kgrid - 1) / (ipc * (long)kgrid));
         cp = max(cp, WGKV_K5_MIN_PAGES);  // per-item fixed costs (page ids, ring fill, merge) amortised
 #if WGKV_K5_RULE == 1
         // few, long pairs (small batches): cap the chunks per pair near 24 (the
