@@ -395,7 +395,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     // per-pair chunk counts | work-stealing counter | per-pair merge counters
     ctx->ws_nchunks = dalloc<int>(2 * (size_t)S * H + 1, o);
     ctx->ws_tokpos = dalloc<int>((size_t)S * H, o);
-    ctx->wk.terms = dalloc<double>((size_t)S * H * c.hidden, o);
+    ctx->wk.terms = dalloc<double>(2 * (size_t)S * H * c.hidden, o);  // [parity] (deferred decode)
     ctx->wk.count = dalloc<int>((size_t)S * H, o);
     // route outputs: two halves by layer parity (fused layer, fused.cuh)
     ctx->wk.slot = dalloc<int>(2 * (size_t)S * H, o);
@@ -405,8 +405,8 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
     ctx->fw.cnt_items = dalloc<int>((size_t)S * H, o);
     ctx->fw.cnt_kv = dalloc<int>(2 * (size_t)S * H, o);
     ctx->fw.cnt_gw = dalloc<int>(2 * (size_t)S * H, o);
-    ctx->fw.cnt_gate = dalloc<int>((size_t)S * H, o);
-    ctx->fw.g = dalloc<double>((size_t)S * H, o);
+    ctx->fw.cnt_gate = dalloc<int>(2 * (size_t)S * H, o);
+    ctx->fw.g = dalloc<double>(2 * (size_t)S * H, o);
     ctx->fw.pub = dalloc<int>(2 * (size_t)S * H, o);
     ctx->fw.started = dalloc<int>(2, o);
 
@@ -443,7 +443,7 @@ int wgkv_ctx_create(const wgkv_config* cfg_in, wgkv_ctx** out) {
         cudaMemset(ctx->fw.cnt_items, 0, sizeof(int) * (size_t)S * H);
         cudaMemset(ctx->fw.cnt_kv, 0, sizeof(int) * 2 * (size_t)S * H);
         cudaMemset(ctx->fw.cnt_gw, 0, sizeof(int) * 2 * (size_t)S * H);
-        cudaMemset(ctx->fw.cnt_gate, 0, sizeof(int) * (size_t)S * H);
+        cudaMemset(ctx->fw.cnt_gate, 0, sizeof(int) * 2 * (size_t)S * H);
         cudaMemset(ctx->fw.pub, 0, sizeof(int) * 2 * (size_t)S * H);
         cudaMemset(ctx->fw.started, 0, sizeof(int) * 2);
     }
@@ -988,7 +988,10 @@ int wgkv_decode_layer_traced(wgkv_ctx* ctx, int layer, int seq0, int nseq, const
         fin.wk.slot += par;
         fin.wk.event += par;
         fin.wk.next += par;
-        fin.fw = ctx->fw;
+        fin.wk.terms += par * ctx->cfg.hidden;  // the gate scratch too: a fused layer's gate CTAs
+        fin.fw = ctx->fw;                        // run before the previous launch has drained
+        fin.fw.cnt_gate += par;
+        fin.fw.g += par;
         fin.fw.cnt_kv += par;
         fin.fw.cnt_gw += par;
         fin.fw.pub += par;

@@ -65,6 +65,9 @@ constexpr int kFusedMaxPairs = WGKV_FUSED_MAX_PAIRS;  // fused layer: (seq, kv h
                        // (32 pairs) and 1.8 % at 64K x 8 (64 pairs); 3 beats 2 by 1.5-3 % on the serving
                        // mix (512 pairs) (profiles/r2_decode_peer_ab.txt)
 #endif
+#ifndef WGKV_GATE_EARLY
+#define WGKV_GATE_EARLY 1  // fused layer: the gate CTAs compute before the PDL wait (parity-split scratch)
+#endif
 #ifndef WGKV_K5_RULE
 #define WGKV_K5_RULE 1
 #endif
@@ -342,15 +345,22 @@ __global__ void __launch_bounds__(DW * 32, CPS) decode_attn_mma_kernel(const __g
         const int gb = blockIdx.x - a.n_route_ctas;
         const int pr = gb / gpp, j = gb % gpp;
         const int s = pr / a.pv.kv_heads, h = pr % a.pv.kv_heads;
-        append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, sm, true,
+        // fused layer behind another layer's launch: the gate scratch (terms,
+        // counters, g) is split by layer parity, so only the commit (caller
+        // trace outputs) waits for the predecessor; the other gate CTAs exit early
+        const bool gate_early = WGKV_GATE_EARLY && a.fused && a.prewait;
+        append_gate_part<__nv_bfloat16>(a.pv, fin.ga, a.layer, a.seq0, s, h, j, fin.k_new, fin.wk, sm, !gate_early,
                                         a.prewait != 0);
         if (a.fused) {
             // the last gate CTA of the pair sums z2, then arrives for the gate group (fused.cuh)
             const int pairg = a.seq0 * a.pv.kv_heads + pr;
             if (fused_gate_arrive(a.pv, fin.ga, a.layer, pairg, h, fin.wk, fin.fw, sm)) {
                 __syncthreads();  // fw.g written (thread 0)
-                if (tid == 0 && pair_arrive(&fin.fw.cnt_gw[pairg]))
-                    fused_commit_gate(a.pv, fin.ga, a.seq0, s, h, fin.tr, fin.wk, fin.fw);
+                if (tid == 0) {
+                    if (gate_early) asm volatile("griddepcontrol.wait;" ::: "memory");
+                    if (pair_arrive(&fin.fw.cnt_gw[pairg]))
+                        fused_commit_gate(a.pv, fin.ga, a.seq0, s, h, fin.tr, fin.wk, fin.fw);
+                }
             }
         } else {
             append_arrive(a.pv, fin.ga, a.layer, a.seq0, s, h, fin.forced_g, fin.tr, fin.wk, gpp + 1, sm);
