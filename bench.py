@@ -747,11 +747,11 @@ def main():
     ap.add_argument("--prefill-exchange", default="peer", choices=["peer", "nccl"],
                     help="prefill C1 (N > 1): fused into K3's epilogue over peer memory, or NCCL all-gather + assembly")
     ap.add_argument("--decode-exchange", default="peer", choices=["peer", "nccl", "none"],
-                    help="decode C1 (N > 1): push kernel over peer memory (wgkv_peer_*) or NCCL all-gather + assembly "
-                         "('none': no exchange, diagnostics only)")
+                    help="decode C1 (N > 1): fused into the decode layer over peer memory (wgkv_peer_decode: LL words "
+                         "from the merge) or NCCL all-gather + assembly ('none': no exchange, diagnostics only)")
     ap.add_argument("--emulate-shard", type=int, default=0,
                     help="one GPU runs rank 0's KV-head shard of N GPUs (8/N kv heads) incl. the head all-gather's "
-                         "assembly; the NVLink transfer is not emulated and no scaling curve is measured")
+                         "local part; the NVLink transfer is not emulated and no scaling curve is measured")
     args = ap.parse_args()
     if args.config in ("serve", "1m"):
         import bench_configs
