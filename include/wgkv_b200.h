@@ -232,7 +232,9 @@ int wgkv_comm_init(wgkv_ctx* ctx, const uint8_t* id128, int world, int rank); /*
 int wgkv_comm_attach(wgkv_ctx* ctx, void* nccl_comm, int world, int rank);   /* caller-owned ncclComm_t */
 int wgkv_allgather_heads(wgkv_ctx* ctx, int nseq, long T, const void* local_out, void* full_out, int async);
 int wgkv_comm_join(wgkv_ctx* ctx);
-/* ---- C1 over NVLink peer memory: the decode-sized all-gather ---------------
+/* ---- C1 over NVLink peer memory (no reference equivalent: the reference runs
+ * every head in one process; this replaces its concat, engine.cpp:234-238,
+ * across KV-head shards -- SURVEY.md §8e) ------------------------------------
  * A decode layer's head outputs are a few KB per rank: NCCL's all-gather is
  * latency-bound there.  Instead every rank owns an exchange region
  * (wgkv_peer_region_bytes) mapped into every other rank: wgkv_peer_alloc
