@@ -175,11 +175,15 @@ __global__ void peer_bulk_wait_kernel(PeerXchg x, int ranks) {
     if (threadIdx.x != 0) return;
     uint8_t* own = x.peers.base[x.rank];
     const uint32_t e = *reinterpret_cast<volatile uint32_t*>(own + 4 * kPeerBulkEpoch) + 1u;
+    const unsigned long long t0 = peer_now();
     for (int r = 0; r < ranks; ++r) {
         uint32_t f;
         do {
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(f) : "l"(own + 4 * (kPeerBulkFlag + r)) : "memory");
-            if ((int)(f - e) < 0) __nanosleep(64);
+            if ((int)(f - e) < 0) {
+                if (peer_now() - t0 > kPeerTimeoutNs) __trap();  // a rank never signalled (comm.cuh)
+                __nanosleep(64);
+            }
         } while ((int)(f - e) < 0);
     }
     *reinterpret_cast<volatile uint32_t*>(own + 4 * kPeerBulkEpoch) = e;

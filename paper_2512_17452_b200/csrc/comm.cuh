@@ -86,6 +86,15 @@ struct PeerBulk {
 };
 
 #ifdef __CUDACC__
+// a peer that never arrives (a rank died or diverged from the exchange
+// sequence) must not hang the GPU forever: after kPeerTimeoutNs of polling the
+// kernel traps, and the host sees a launch failure instead of a hang
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long peer_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 // the flag of this rank's push into x.push_slot: the slot's epoch (unpacks so
 // far, identical on every rank) + 1
 __device__ __forceinline__ uint32_t peer_push_flag(const PeerXchg& x) {
@@ -118,9 +127,14 @@ __device__ __forceinline__ void peer_unpack_cta(const PeerXchg& x) {
         const int r = (int)((i / wpr) % x.unpack_ranks), j = (int)(i % wpr);
         const uint8_t* src = ll + (((size_t)row * x.world + r) * wpr + j) * 8;
         uint32_t dv, fv;
-        do {
-            asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(dv), "=r"(fv) : "l"(src) : "memory");
-        } while (fv != flag);
+        asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(dv), "=r"(fv) : "l"(src) : "memory");
+        if (fv != flag) {
+            const unsigned long long t0 = peer_now();
+            do {
+                if (peer_now() - t0 > kPeerTimeoutNs) __trap();
+                asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(dv), "=r"(fv) : "l"(src) : "memory");
+            } while (fv != flag);
+        }
         *reinterpret_cast<uint32_t*>(res + (size_t)row * x.world * x.blk + (size_t)r * x.blk + (size_t)j * 4) = dv;
     }
     __syncthreads();
