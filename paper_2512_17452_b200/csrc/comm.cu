@@ -16,6 +16,11 @@
 // NCCL is resolved at run time (dlopen "libnccl.so.2", reusing the copy torch
 // already loaded if any), so the library itself loads on hosts without it;
 // only wgkv_comm_init / wgkv_comm_attach need it.
+//
+// The same exchange without NCCL (wgkv_peer_*, layout and device helpers in
+// comm.cuh): the decode merge and K3's epilogue store their rows straight into
+// every rank's mapped region; this file holds the standalone push / unpack /
+// bulk signal / wait kernels around them.
 #include <dlfcn.h>
 #include <nccl.h>
 
